@@ -1,0 +1,163 @@
+/* es_oracle.c -- CPU ORACLE for ES-SpMM's sampled SpMM.  TEST INFRASTRUCTURE ONLY.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference
+ * leg may load this.  It shares no code with the CUDA path (paper_2104_10716_b200/).
+ *
+ * Plain, slow, obviously correct: one loop over rows (OpenMP over independent rows
+ * only; the per-row arithmetic is sequential), fp64 accumulation in slot order,
+ * rounded once to fp32.  Every function cites the passage it follows (PAPER.md
+ * line numbers, Doc B unless noted; DESIGN.md "Readings" for the silent parts).
+ *
+ *   Alg. 1 "Pseudo Code of CacheSample"
+ *   S = min(row_nnz, shmem_width)            Alg. 1 l.6, L961; "If S exceeds the NNZ of that
+ *                                            row, then the whole row is fetched", L986
+ *   Bucket: "picks the first S"              L1042-1047
+ *   FastRand Eq. 2:
+ *     sample_idx = (shmem_idx x P') mod row_nnz, P' = 577     L1064-1067, L1058
+ *   acc += sh_data[j] * B[sh_cols[j], col_id]                 Alg. 1 l.13-15, L969-972
+ *   in-kernel normalisation by degree (mean)                  L1570-1575 (reading R5: k_i)
+ *   sampling rate = sum min(d_i,s) / nnz                      L1290-1303
+ *
+ * Pins: tests/test_oracle_pins.py (closed forms, SPEC.md worked examples, the paper's
+ * Table sample_rate, scipy for s >= max degree, dense brute force on tiny graphs).
+ *
+ * Build: gcc -O2 -fopenmp -shared -fPIC es_oracle.c -o libesoracle.so   (no -ffast-math)
+ */
+#include <stdint.h>
+#include <stddef.h>
+#include <stdlib.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define ORACLE_BUCKET 1
+#define ORACLE_FASTRAND 2
+#define ORACLE_SUM 0
+#define ORACLE_MEAN 1
+#define ORACLE_PRIME 577ull /* P' = 577 */
+
+/* splitmix64 finalizer (reading R6: seeded FastRand offset). */
+static uint64_t oracle_mix64(uint64_t x) {
+    x ^= x >> 30; x *= 0xBF58476D1CE4E5B9ull;
+    x ^= x >> 27; x *= 0x94D049BB133111EBull;
+    x ^= x >> 31;
+    return x;
+}
+
+uint64_t oracle_hash(uint64_t x) { return oracle_mix64(x); }
+
+/* Reading R6: seed == 0 is exactly Eq. 2; seed != 0 rotates row i's FastRand
+ * sequence by off_i = mix64(seed + G*(i+1)) mod d_i, i the GLOBAL row id. */
+int64_t oracle_offset(uint64_t seed, int64_t row, int64_t d) {
+    if (seed == 0 || d <= 0) return 0;
+    uint64_t h = oracle_mix64(seed + 0x9E3779B97F4A7C15ull * (uint64_t)(row + 1));
+    return (int64_t)(h % (uint64_t)d);
+}
+
+/* Position within the row of sampled slot j (0 <= j < k <= d).
+ *   Bucket:   p_j = j                                    (L1043 "first S")
+ *   FastRand: p_j = (off + j * P') mod d                 (Eq. 2; off per R6)
+ * 64-bit unsigned arithmetic: j*577 < 2^64 for any j < 3.2e16. */
+int64_t oracle_position(int32_t strategy, int64_t j, int64_t d, int64_t off) {
+    if (strategy == ORACLE_BUCKET) return j;
+    return (int64_t)(((uint64_t)off + (uint64_t)j * ORACLE_PRIME) % (uint64_t)d);
+}
+
+/* k_i = min(d_i, s)   (Alg. 1 l.6, L961) */
+static int64_t oracle_k(int64_t d, int64_t s) { return d < s ? d : s; }
+
+/* Sampling rate, PAPER.md:L1290-1303 (Table sample_rate): sum_i min(d_i, s) / nnz;
+ * nnz == 0 -> 1.0. */
+double oracle_rate(int64_t n_rows, const int64_t* rowptr, int64_t s) {
+    int64_t kept = 0, nnz = rowptr[n_rows] - rowptr[0];
+    for (int64_t i = 0; i < n_rows; ++i) kept += oracle_k(rowptr[i + 1] - rowptr[i], s);
+    return nnz == 0 ? 1.0 : (double)kept / (double)nnz;
+}
+
+/* Stage 1 of Alg. 1 materialised (the paper's "pre-sampled graph", L1509-1514):
+ * s_rowptr[0..n_rows] = exclusive prefix of k_i; then, if s_colind != NULL, slot j of
+ * row i holds (colind, val, position) of nonzero rowptr[i] + p_j, in SLOT order with
+ * duplicates kept (reading R2).  row_base = global id of row 0 (for the seeded offset).
+ * rowptr entries are absolute offsets into colind/val. */
+void oracle_sample(int64_t n_rows, const int64_t* rowptr, const int32_t* colind,
+                   const float* val, int64_t s, int32_t strategy, uint64_t seed,
+                   int64_t row_base, int64_t* s_rowptr, int32_t* s_colind, float* s_val,
+                   int64_t* s_pos) {
+    s_rowptr[0] = 0;
+    for (int64_t i = 0; i < n_rows; ++i)
+        s_rowptr[i + 1] = s_rowptr[i] + oracle_k(rowptr[i + 1] - rowptr[i], s);
+    if (!s_colind) return;
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int64_t i = 0; i < n_rows; ++i) {
+        int64_t d = rowptr[i + 1] - rowptr[i];
+        int64_t k = oracle_k(d, s);
+        int64_t off = strategy == ORACLE_FASTRAND ? oracle_offset(seed, row_base + i, d) : 0;
+        for (int64_t j = 0; j < k; ++j) {
+            int64_t p = oracle_position(strategy, j, d, off);
+            int64_t e = rowptr[i] + p;
+            int64_t o = s_rowptr[i] + j;
+            s_colind[o] = colind[e];
+            if (s_val) s_val[o] = val ? val[e] : 1.0f;
+            if (s_pos) s_pos[o] = p;
+        }
+    }
+}
+
+/* One output row of the sampled SpMM (Alg. 1 l.5-16 for all col_id of a row):
+ *   acc[c] = sum_{j<k} val[e_j] * B[colind[e_j], c]   in fp64, slot order
+ *   SUM:  C[c] = fp32(acc[c])
+ *   MEAN: C[c] = fp32(acc[c]) / fp32(k)  (IEEE fp32 division), k == 0 -> 0   (R5, R8, R9) */
+static void oracle_row(int64_t d, const int32_t* cols, const float* vals, const float* B,
+                       int64_t F, int64_t ldb, int64_t s, int32_t strategy, int64_t off,
+                       int32_t reduce, double* acc, float* Crow) {
+    int64_t k = oracle_k(d, s);
+    for (int64_t c = 0; c < F; ++c) acc[c] = 0.0;
+    for (int64_t j = 0; j < k; ++j) {
+        int64_t p = oracle_position(strategy, j, d, off);
+        double a = vals ? (double)vals[p] : 1.0;
+        const float* Brow = B + (int64_t)cols[p] * ldb;
+        for (int64_t c = 0; c < F; ++c) acc[c] += a * (double)Brow[c];
+    }
+    for (int64_t c = 0; c < F; ++c) {
+        float v = (float)acc[c];
+        if (reduce == ORACLE_MEAN) v = k > 0 ? v / (float)k : 0.0f;
+        Crow[c] = v;
+    }
+}
+
+/* C[i, 0:F] for rows i in [0, n_rows) (rows == NULL), or for the n_sel rows listed in
+ * rows[] (output row r of C is then global-slice row rows[r]).  Returns -1 on OOM. */
+int oracle_spmm(int64_t n_rows, const int64_t* rowptr, const int32_t* colind, const float* val,
+                const float* B, int64_t F, int64_t ldb, int64_t s, int32_t strategy,
+                uint64_t seed, int32_t reduce, int64_t row_base,
+                const int64_t* rows, int64_t n_sel, float* C, int64_t ldc) {
+    int64_t n_out = rows ? n_sel : n_rows;
+    int bad = 0;
+#pragma omp parallel
+    {
+        double* acc = (double*)malloc(sizeof(double) * (size_t)(F > 0 ? F : 1));
+        if (!acc) {
+#pragma omp atomic write
+            bad = 1;
+        }
+#pragma omp for schedule(dynamic, 16)
+        for (int64_t r = 0; r < n_out; ++r) {
+            if (!acc) continue;
+            int64_t i = rows ? rows[r] : r;
+            int64_t d = rowptr[i + 1] - rowptr[i];
+            int64_t off = strategy == ORACLE_FASTRAND ? oracle_offset(seed, row_base + i, d) : 0;
+            oracle_row(d, colind + rowptr[i], val ? val + rowptr[i] : NULL, B, F, ldb, s,
+                       strategy, off, reduce, acc, C + r * ldc);
+        }
+        free(acc);
+    }
+    return bad ? -1 : 0;
+}
+
+int oracle_max_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
