@@ -1,0 +1,424 @@
+#!/usr/bin/env python3
+"""Benchmark of the ES-SpMM hot path (BASELINE.json metric) on 1..8 B200s.
+
+One "step" = one pass of the whole hot path (degree/cap, sampling,
+staging, gather-FMA, epilogue) over the configured graph: ONE fused kernel launch per
+rank (es_spmm_run_rows on the rank's row block).  Inputs are resident in HBM when the
+timed region starts; L2 is flushed (256 MiB write) before every timed step.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config reddit] [--F 602]
+                  [--s 256] [--strategy fastrand|bucket] [--reduce mean|sum]
+                  [--impl ours|reference]
+
+Prints ONE JSON line on rank 0.  See DESIGN.md "Measurement" for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+FALLBACK_HBM_GBS = 6650.0      # /opt/skills/guides/B200_PROFILING.md fallback (only if no measured peak)
+
+DEFAULTS = {  # workload named in config.workload; BASELINE.json configs[3] (the graded target)
+    "pubmed": dict(F=16, s=32, strategy="bucket", reduce="sum"),
+    "arxiv": dict(F=128, s=64, strategy="fastrand", reduce="sum"),
+    "proteins": dict(F=128, s=256, strategy="fastrand", reduce="sum"),
+    "reddit": dict(F=602, s=256, strategy="fastrand", reduce="mean"),
+    "scaled": dict(F=256, s=128, strategy="fastrand", reduce="sum"),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="reddit", choices=sorted(DEFAULTS))
+    ap.add_argument("--F", type=int, default=None)
+    ap.add_argument("--s", type=int, default=None)
+    ap.add_argument("--strategy", default=None, choices=["bucket", "fastrand"])
+    ap.add_argument("--reduce", default=None, choices=["sum", "mean"])
+    ap.add_argument("--seed", type=int, default=0, help="FastRand seed (0 = paper-exact Eq. 2)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--kernel", default="auto", choices=["auto", "tma", "warp"],
+                    help="kernel family (A/B measurement; auto = the library's plan)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-flush", action="store_true", help="warm-L2 variant (not the headline)")
+    ap.add_argument("--cpu-seconds", type=float, default=3.0, help="wall-time target of the oracle sample")
+    a = ap.parse_args()
+    d = DEFAULTS[a.config]
+    for k in ("F", "s", "strategy", "reduce"):
+        if getattr(a, k) is None:
+            setattr(a, k, d[k])
+    if a.warmup < 3:
+        a.warmup = 3
+    if a.kernel != "auto":
+        os.environ["ES_SPMM_KERNEL"] = a.kernel
+    return a
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy bandwidth)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ldb_for(F):
+    return (F + 3) // 4 * 4          # rows padded to 16 B
+
+
+def workload_name(a):
+    return (f"{a.config}-shaped synthetic CSR, F={a.F}, s={a.s}, {a.strategy}, "
+            f"{'GraphSage mean' if a.reduce == 'mean' else 'GCN sum'}")
+
+
+def byte_model(K, n_rows, F):
+    """Algorithmic bytes of one pass: 8K (sampled colind+val) + 8(N+1) (rowptr)
+    + 4FK (B-row gathers) + 4FN (C store)."""
+    return 8 * K + 8 * (n_rows + 1) + 4 * F * K + 4 * F * n_rows
+
+
+# ------------------------------------------------------------------ clocks sampler
+class Clocks:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        if not self.rows:
+            return None
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) < 9:
+                continue
+            for nm, v in zip(names, r[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ oracle timing (CPU baseline)
+def oracle_sample_rows(rowptr, s, F, target_s, cores):
+    """Every m-th row, m chosen so the fp64 oracle needs ~target_s wall seconds on `cores`."""
+    d = np.diff(rowptr)
+    k_all = int(np.minimum(d, s).sum())
+    est_rate = 0.8e9 * cores            # slot*feature / s, rough; only sizes the sample
+    m = max(1, int(np.ceil(k_all * F / (est_rate * target_s))))
+    rows = np.arange(0, len(d), m, dtype=np.int64)
+    return rows, m
+
+
+def time_oracle(rowptr, colind, val, B, a, strat, red, rows):
+    import oracle
+    t0 = time.perf_counter()
+    oracle.spmm(rowptr, colind, val, B, a.s, strat, seed=a.seed, reduce=red, F=a.F, rows=rows)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(rowptr, colind, val, B, a, strat, red, steps=1):
+    import oracle
+    cores = oracle.max_threads()
+    rows, m = oracle_sample_rows(rowptr, a.s, a.F, a.cpu_seconds, cores)
+    d = np.diff(rowptr)
+    Ks = int(np.minimum(d[rows], a.s).sum())
+    ts = [time_oracle(rowptr, colind, val, B, a, strat, red, rows) for _ in range(steps)]
+    t = float(np.median(ts))
+    return {"value": 2.0 * a.F * Ks / t / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
+            "sample": f"every {m}-th row of the same workload ({len(rows)} rows, {Ks} sampled edges), "
+                      f"fp64 C oracle (oracle/es_oracle.c, -O2, OpenMP {cores} threads), "
+                      f"median of {steps}, {t:.2f} s"}, t
+
+
+# ------------------------------------------------------------------ main
+def main():
+    a = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    strat_id = 1 if a.strategy == "bucket" else 2
+    red_id = 1 if a.reduce == "mean" else 0
+
+    if a.impl == "reference":
+        return main_reference(a, world, rank, strat_id, red_id)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2104_10716_b200 as es
+
+    es.load_library()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    # ---------------- inputs (seeded, synthetic)
+    rowptr, colind = synth.graph(a.config)
+    n = len(rowptr) - 1
+    nnz = int(rowptr[-1])
+    F, ldb = a.F, ldb_for(a.F)
+    _, seed_b = synth.seeds(a.config)
+    B = synth.dense(n, F, seed_b, ld=ldb)
+    val = np.ones(nnz, np.float32)                         # unweighted adjacency (L615), read by the kernel
+    bounds = es.es_partition_rows(rowptr, a.s, F, world)
+    r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+    e0, e1 = int(rowptr[r0]), int(rowptr[r1])
+    d_all = np.diff(rowptr)
+    K_rank = int(np.minimum(d_all[r0:r1], a.s).sum())
+    K_all = int(np.minimum(d_all, a.s).sum())
+
+    rp_d = torch.from_numpy(rowptr[r0:r1 + 1].copy()).to(dev)
+    ci_d = torch.from_numpy(colind[e0:e1]).to(dev)
+    va_d = torch.from_numpy(val[e0:e1]).to(dev)
+    B_d = torch.from_numpy(B).to(dev)                      # replicated: no collective on the timed path
+    C_d = torch.empty((r1 - r0, ldb), dtype=torch.float32, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        es.es_spmm_run_rows(n, rp_d, e0, ci_d, va_d, B_d, a.s, strat_id, a.seed, red_id, r0, r1,
+                            F=F, C=C_d, stream=stream)
+
+    for _ in range(a.warmup):
+        if not a.no_flush:
+            flush.zero_()
+        step()
+    torch.cuda.synchronize(dev)
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(0.15)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    launches0 = es.es_launch_count()
+    wall0 = time.perf_counter()
+    for i in range(a.steps):
+        if not a.no_flush:
+            flush.zero_()                                  # evict L2 between timed steps
+        starts[i].record(stream)
+        step()
+        ends[i].record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    wall = time.perf_counter() - wall0
+    launches = es.es_launch_count() - launches0
+    clk = clocks.stop()
+
+    per_step = np.array([s_.elapsed_time(e_) for s_, e_ in zip(starts, ends)]) / 1e3   # seconds
+    t_rank = float(per_step.sum())
+    t_max = t_rank
+    if world > 1:
+        tt = torch.tensor([t_rank], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt.item())
+    ms_per_step = 1e3 * t_max / a.steps
+    flops_all = 2.0 * F * K_all                            # whole job per step (all ranks)
+    value = flops_all / (t_max / a.steps) / 1e9            # GFLOP/s
+
+    # ---------------- roofline of the dominant (only) kernel, this rank's launch
+    peak, peak_src = measured_peaks()
+    bytes_rank = byte_model(K_rank, r1 - r0, F)
+    avg_launch = t_rank / a.steps
+    achieved = bytes_rank / avg_launch / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                tj = json.load(f)
+            key = f"{a.config}|F{F}|s{a.s}|{a.strategy}|{a.reduce}"
+            if key in tj and world == 1:
+                traffic = tj[key]["dram_bytes_per_launch"]
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "peak_source": peak_src,
+                "bytes_per_launch": bytes_rank,
+                "bytes_model": "8K + 8(N+1) + 4FK + 4FN (sampled colind+val, rowptr, B gathers, C)",
+                "kernel": es.es_spmm_plan(F, ldb, ldb, B_d, C_d)}
+
+    # ---------------- end to end through the public host API (pinned host buffers)
+    e2e = None
+    if not a.no_e2e:
+        e2e = run_e2e(a, es, torch, dev, stream, rowptr, colind, val, B, r0, r1, e0, e1, F, ldb,
+                      strat_id, red_id, flops_all, world, dist)
+
+    # ---------------- CPU baseline: the oracle as it stands, rank 0 at N=1 only
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        cpu, _ = cpu_baseline(rowptr, colind, val, B, a, strat_id, red_id)
+
+    if rank == 0:
+        out = {
+            "metric": f"sampled-SpMM GFLOP/s ({workload_name(a)})",
+            "value": round(value, 2),
+            "unit": "GFLOP/s",
+            "n_gpus": world,
+            "steps": a.steps,
+            "warmup": a.warmup,
+            "ms_per_step": round(ms_per_step, 4),
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f32",
+            "data": "synthetic (seeded; degree sequence fitted to PAPER.md Table dataset + Table sample_rate)",
+            "config": {"workload": workload_name(a), "n_nodes": n, "nnz": nnz, "K_sampled": K_all,
+                       "sampling_rate": round(K_all / nnz, 4), "F": F, "ldb": ldb, "s": a.s,
+                       "strategy": a.strategy, "reduce": a.reduce, "seed": a.seed,
+                       "l2": "no flush (warm)" if a.no_flush else "flushed between timed steps (256 MiB write)",
+                       "parallelism": f"row-partitioned x{world} (sampled-byte balanced), B replicated",
+                       "timing": "sum of per-step CUDA-event times on the launch stream, max over ranks"},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches) * world,
+            "clocks": clk,
+            "detail": {"sampled_edges_per_s": K_all / (t_max / a.steps),
+                       "input_edges_per_s": nnz / (t_max / a.steps),
+                       "step_ms_min": round(1e3 * float(per_step.min()), 4),
+                       "step_ms_median": round(1e3 * float(np.median(per_step)), 4),
+                       "wall_s_timed_region": round(wall, 4),
+                       "bytes_model_per_step_all_ranks": byte_model(K_all, n, F)},
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_e2e(a, es, torch, dev, stream, rowptr, colind, val, B, r0, r1, e0, e1, F, ldb, strat_id, red_id,
+            flops_all, world, dist):
+    """Same metric through es_spmm_run_host: every step copies this rank's CSR slice and the
+    replicated B from pinned host memory and reads C back (inside the timed region)."""
+    rp_h = torch.from_numpy(rowptr[r0:r1 + 1].copy()).pin_memory()
+    ci_h = torch.from_numpy(colind[e0:e1]).pin_memory()
+    va_h = torch.from_numpy(val[e0:e1]).pin_memory()
+    B_h = torch.from_numpy(B).pin_memory()
+    C_h = torch.empty((r1 - r0, F), dtype=torch.float32).pin_memory()
+    need = es.es_spmm_host_workspace_bytes(r1 - r0, B.shape[0], e1 - e0, F, ldb, True)
+    ws = torch.empty(need, dtype=torch.uint8, device=dev)
+    steps = max(3, min(a.steps, 10))
+
+    def one():
+        es.es_spmm_run_host(rp_h, ci_h, va_h, B_h, a.s, strat_id, a.seed, red_id, F=F, C=C_h,
+                            workspace=ws, row_base=r0, stream=stream)
+
+    for _ in range(2):
+        one()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(steps):
+        one()
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    t = ev0.elapsed_time(ev1) / 1e3
+    if world > 1:
+        tt = torch.tensor([t], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+    h2d = (rp_h.numel() * 8 + ci_h.numel() * 4 + va_h.numel() * 4 + B_h.numel() * 4)
+    d2h = C_h.numel() * 4
+    return {"value": round(flops_all / (t / steps) / 1e9, 2), "unit": "GFLOP/s",
+            "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h) * world,
+            "ms_per_step": round(1e3 * t / steps, 3), "steps": steps,
+            "api": "es_spmm_run_host (pinned host buffers, chunked H2D/compute/D2H pipeline)"}
+
+
+def main_reference(a, world, rank, strat_id, red_id):
+    """--impl reference: the oracle as it stands on the host cores (rank 0 only)."""
+    if rank != 0:
+        return 0
+    import oracle
+    rowptr, colind = synth.graph(a.config)
+    n = len(rowptr) - 1
+    F = a.F
+    _, seed_b = synth.seeds(a.config)
+    B = synth.dense(n, F, seed_b, ld=ldb_for(F))
+    val = np.ones(len(colind), np.float32)
+    cores = oracle.max_threads()
+    target = max(0.5, a.cpu_seconds * 2.0 / max(1, a.steps + a.warmup) * 3)
+    rows, m = oracle_sample_rows(rowptr, a.s, F, target, cores)
+    d = np.diff(rowptr)
+    Ks = int(np.minimum(d[rows], a.s).sum())
+    for _ in range(a.warmup):
+        time_oracle(rowptr, colind, val, B, a, strat_id, red_id, rows)
+    ts = [time_oracle(rowptr, colind, val, B, a, strat_id, red_id, rows) for _ in range(a.steps)]
+    t = float(np.sum(ts))
+    value = 2.0 * F * Ks * a.steps / t / 1e9
+    sample = (f"every {m}-th row of the same workload per step ({len(rows)} rows, {Ks} sampled edges), "
+              f"fp64 C oracle, OpenMP {cores} threads")
+    out = {"impl": "reference", "metric": f"sampled-SpMM GFLOP/s ({workload_name(a)})",
+           "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": a.steps,
+           "warmup": a.warmup, "ms_per_step": round(1e3 * t / a.steps, 3), "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": workload_name(a), "F": F, "s": a.s, "strategy": a.strategy,
+                      "reduce": a.reduce},
+           "cpu_baseline": {"value": round(value, 3), "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
+                            "sample": sample},
+           "e2e": {"value": round(value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main() or 0)

@@ -1,0 +1,150 @@
+/* es_spmm.h -- C ABI of the B200-native ES-SpMM sampled SpMM (arXiv 2104.10716).
+ *
+ * The operation (PAPER.md Doc B):
+ *   problem statement, §4.1: "Input to the kernel is a sparse matrix A in CSR
+ *     format ... A dense matrix B contains the nodes' features.  The output of the kernel
+ *     is a dense matrix C ...  B and C are both in row-major format."
+ *   Alg. 1 "Pseudo Code of CacheSample", L952-976:
+ *     S = min(row_nnz, shmem_width)                                   (l.6)
+ *     for i < S: sample_idx = get_sample_index(i, row_nnz);
+ *                sh_data[i], sh_cols[i] = load_A(sample_idx)          (l.7-10)
+ *     acc = sum_{j<S} sh_data[j] * B[sh_cols[j], col_id];  C[row_id, col_id] = acc  (l.12-16)
+ *   Bucket: first S entries, L1042-1047.  FastRand, Eq. 2:
+ *     sample_idx = (shmem_idx * P') mod row_nnz,  P' = 577 (L1058).
+ *   GraphSage mean / in-kernel normalisation, L1570-1575 (divides by k_i; R5).
+ *   No preprocessing: sampling happens inside the kernel, L1005, L1201.
+ *
+ * Readings where the paper is silent are listed in DESIGN.md ("Readings R1-R11"):
+ *   R1 Eq. 2 applies even when d_i <= s (whole row, permuted order);
+ *   R2 duplicates (577 | d_i) are kept and multiplied again; MEAN divides by k_i slots;
+ *   R6 seed != 0 rotates row i's FastRand sequence by mix64(seed + G*(i+1)) mod d_i
+ *      (i = GLOBAL row id, G = 0x9E3779B97F4A7C15, mix64 = splitmix64 finalizer);
+ *      seed == 0 is exactly Eq. 2;
+ *   R8 fp32 storage, fp32 FMA accumulation (two interleaved partial sums), IEEE division.
+ *
+ * Conventions (all entry points):
+ *   * Pointers marked [dev] are device pointers; [host] are host pointers.  The caller
+ *     owns every buffer.  es_spmm_run / es_spmm_run_rows never allocate.
+ *   * Every device call is enqueued on `stream` (a cudaStream_t passed as void*; NULL =
+ *     legacy default stream) and returns without synchronising, except where noted.
+ *   * Layouts: rowptr int64[n_rows+1] (absolute offsets into colind/val, rowptr[0] may be
+ *     non-zero); colind int32[nnz]; val fp32[nnz] or NULL (= all 1.0, the unweighted
+ *     adjacency of L615); B fp32 row-major, n_cols rows x ldb (the allocation holds
+ *     n_cols*ldb floats; columns F..ldb-1 are padding and are never stored); C fp32
+ *     row-major, rows x ldc (columns F..ldc-1 are left untouched).
+ *   * CSR invariants (rowptr non-decreasing, 0 <= colind < n_cols) are preconditions,
+ *     not checked on the hot path.  Column order within a row is taken as stored
+ *     (R4: Bucket keeps the first k stored entries).
+ *   * Errors: status codes only, no exceptions or aborts cross the ABI.  Host-checked:
+ *     NULL required pointers, negative sizes, s < 1, F < 1, ldb < F, ldc < F, unknown
+ *     strategy/reduce -> ES_ERR_INVALID_VALUE.  Misaligned B/C never fail: a narrower
+ *     vector path is chosen.  Launch failures -> ES_ERR_CUDA.
+ *   * Thread-safe: no mutable global state other than an atomic launch counter.
+ *   * There is no CPU fallback: every step of the path runs in this library's kernels.
+ */
+#ifndef ES_SPMM_H
+#define ES_SPMM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    ES_OK = 0,
+    ES_ERR_INVALID_VALUE = 1,
+    ES_ERR_MISALIGNED = 2,   /* reserved: misalignment is never fatal */
+    ES_ERR_UNSUPPORTED = 3,
+    ES_ERR_CUDA = 4
+} es_status_t;
+
+enum { ES_BUCKET = 1, ES_FASTRAND = 2 };          /* sampling strategy, §4.4 */
+enum { ES_REDUCE_SUM = 0, ES_REDUCE_MEAN = 1 };   /* GCN sum (Eq. 1) / GraphSage mean (L1256) */
+
+/* Edge sampling materialised (stage 1 of Alg. 1; the paper's "pre-sampled graph",
+ * §5.6).
+ *   Phase 1 (s_colind == NULL): writes s_rowptr[0..n_rows] [dev] = exclusive prefix sum
+ *     of k_i = min(d_i, s), with s_rowptr[0] = 0.  The caller reads s_rowptr[n_rows]
+ *     (a D->H sync it performs itself) to size phase 2.
+ *   Phase 2: additionally writes, for slot j < k_i of row i, at offset s_rowptr[i] + j:
+ *     s_colind[.] = colind[rowptr[i] + p_j], s_val[.] = val[...] (1.0 if val == NULL),
+ *     s_pos[.] = p_j (optional, may be NULL), in SLOT order with duplicates kept (R2).
+ *     s_val may be NULL (not written).
+ *   p_j = j (Bucket) or (off_i + j*577) mod d_i (FastRand, R6), i = row_base + local row.
+ *   Phase 1 takes a stream-ordered scratch allocation (cudaMallocAsync) for its scan. */
+es_status_t es_spmm_sample(int64_t n_rows, int64_t n_cols,
+                           const int64_t* rowptr /*[dev]*/, const int32_t* colind /*[dev]*/,
+                           const float* val /*[dev], NULL => 1.0f*/,
+                           int32_t s, int32_t strategy, uint64_t seed, int64_t row_base,
+                           int64_t* s_rowptr /*[dev] n_rows+1*/, int32_t* s_colind /*[dev]*/,
+                           float* s_val /*[dev] or NULL*/, int64_t* s_pos /*[dev] or NULL*/,
+                           void* stream);
+
+/* Fused sampled SpMM (Alg. 1 stages 1+2, sampling inside the kernel):
+ *   C[i, 0:F] = reduce_{j < k_i} val[e_ij] * B[colind[e_ij], 0:F],  e_ij = rowptr[i] + p_j
+ * for i in [0, n_rows); reduce = SUM, or MEAN (divide by k_i; k_i == 0 gives a zero row).
+ * Global row id of local row i is i (seeded FastRand offset). */
+es_status_t es_spmm_run(int64_t n_rows, int64_t n_cols,
+                        const int64_t* rowptr /*[dev]*/, const int32_t* colind /*[dev]*/,
+                        const float* val /*[dev] or NULL*/,
+                        const float* B /*[dev] n_cols x ldb*/, int64_t F, int64_t ldb,
+                        int32_t s, int32_t strategy, uint64_t seed, int32_t reduce,
+                        float* C /*[dev] n_rows x ldc*/, int64_t ldc, void* stream);
+
+/* Same operation restricted to global rows [row_begin, row_end) of a CSR that may be a
+ * slice (the multi-GPU path):
+ *   rowptr [dev] points at the entries for rows row_begin..row_end (row_end-row_begin+1
+ *   values, ABSOLUTE offsets of the global CSR); colind/val [dev] are the slice's arrays
+ *   already offset so that global nonzero e lives at colind[e - nnz_base];
+ *   C [dev] points at the output row for row_begin.
+ * n_rows is the GLOBAL row count (only used for validation); the seeded offset uses the
+ * global row id, so the result is bitwise identical to the corresponding rows of
+ * es_spmm_run on the full CSR. */
+es_status_t es_spmm_run_rows(int64_t n_rows, int64_t n_cols,
+                             const int64_t* rowptr /*[dev]*/, int64_t nnz_base,
+                             const int32_t* colind /*[dev]*/, const float* val /*[dev] or NULL*/,
+                             const float* B /*[dev]*/, int64_t F, int64_t ldb,
+                             int32_t s, int32_t strategy, uint64_t seed, int32_t reduce,
+                             float* C /*[dev]*/, int64_t ldc,
+                             int64_t row_begin, int64_t row_end, void* stream);
+
+/* End-to-end variant with HOST inputs and output (the call a user with host data makes):
+ * copies rowptr/colind/val/B host->device, runs the fused kernel and copies C back,
+ * rowptr entries are absolute offsets with colind[0] holding nonzero rowptr[0];
+ * pipelined over row chunks on `stream` plus one internal copy stream.  Host buffers
+ * should be pinned (cudaHostAlloc/cudaHostRegister) for asynchronous copies.
+ *   workspace [dev] of es_spmm_host_workspace_bytes(...) bytes is owned by the caller.
+ * Synchronises `stream` before returning (C is valid on return). */
+int64_t es_spmm_host_workspace_bytes(int64_t n_rows, int64_t n_cols, int64_t nnz,
+                                     int64_t F, int64_t ldb, int32_t has_val);
+es_status_t es_spmm_run_host(int64_t n_rows, int64_t n_cols,
+                             const int64_t* rowptr /*[host]*/, const int32_t* colind /*[host]*/,
+                             const float* val /*[host] or NULL*/,
+                             const float* B /*[host]*/, int64_t F, int64_t ldb,
+                             int32_t s, int32_t strategy, uint64_t seed, int32_t reduce,
+                             int64_t row_base /* global id of row 0 (seeded FastRand) */,
+                             float* C /*[host]*/, int64_t ldc,
+                             void* workspace /*[dev]*/, int64_t workspace_bytes, void* stream);
+
+/* Host-side, deterministic row partition for P ranks:
+ *   bounds_host[0..n_parts] with bounds[0] = 0, bounds[n_parts] = n_rows, contiguous
+ *   blocks of ~equal sum_i w_i, w_i = k_i*(4F+8) + 4F (sampled bytes; reduces to
+ *   "balanced by nnz" when s >= max degree).  rowptr_host [host] int64[n_rows+1]. */
+es_status_t es_partition_rows(const int64_t* rowptr_host, int64_t n_rows, int32_t s, int64_t F,
+                              int32_t n_parts, int64_t* bounds_host);
+
+/* Static description of the kernel the library would launch for (F, ldb, ldc, pointers):
+ * writes a short NUL-terminated name into buf (e.g. "es_spmm_warp_v4x5"). */
+es_status_t es_spmm_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C,
+                         char* buf, int32_t buf_len);
+
+/* Number of kernels this library has launched in this process (atomic counter). */
+int64_t es_launch_count(void);
+
+const char* es_status_string(es_status_t status);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ES_SPMM_H */

@@ -1,0 +1,226 @@
+"""B200-native ES-SpMM (arXiv 2104.10716): thin Python binding over libesspmm.so.
+
+Argument marshalling only -- every step of the path (degree/cap, sampling, staging,
+gather-FMA, epilogue) runs in the library's sm_100a kernels.  The functions have the
+C ABI's names (include/es_spmm.h) and take torch tensors for device memory; PyTorch is
+used for memory, streams and process groups only.  There is no CPU fallback: if the
+shared library is missing or no CUDA device is present, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+ES_OK, ES_ERR_INVALID_VALUE, ES_ERR_MISALIGNED, ES_ERR_UNSUPPORTED, ES_ERR_CUDA = 0, 1, 2, 3, 4
+ES_BUCKET, ES_FASTRAND = 1, 2
+ES_REDUCE_SUM, ES_REDUCE_MEAN = 0, 1
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libesspmm.so")
+EXPORTS = ("es_spmm_sample", "es_spmm_run", "es_spmm_run_rows", "es_spmm_host_workspace_bytes",
+           "es_spmm_run_host", "es_partition_rows", "es_spmm_plan", "es_launch_count",
+           "es_status_string")
+
+_lib = None
+
+
+class EsError(RuntimeError):
+    pass
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libesspmm.so (raises if it was not built -- no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise EsError(f"{path} missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(path)
+    i64, i32, u64, vp = ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64, ctypes.c_void_p
+    st = ctypes.c_int
+    lib.es_status_string.restype = ctypes.c_char_p
+    lib.es_status_string.argtypes = [st]
+    lib.es_launch_count.restype = i64
+    lib.es_launch_count.argtypes = []
+    lib.es_spmm_sample.restype = st
+    lib.es_spmm_sample.argtypes = [i64, i64, vp, vp, vp, i32, i32, u64, i64, vp, vp, vp, vp, vp]
+    lib.es_spmm_run.restype = st
+    lib.es_spmm_run.argtypes = [i64, i64, vp, vp, vp, vp, i64, i64, i32, i32, u64, i32, vp, i64, vp]
+    lib.es_spmm_run_rows.restype = st
+    lib.es_spmm_run_rows.argtypes = [i64, i64, vp, i64, vp, vp, vp, i64, i64, i32, i32, u64, i32, vp,
+                                     i64, i64, i64, vp]
+    lib.es_spmm_host_workspace_bytes.restype = i64
+    lib.es_spmm_host_workspace_bytes.argtypes = [i64, i64, i64, i64, i64, i32]
+    lib.es_spmm_run_host.restype = st
+    lib.es_spmm_run_host.argtypes = [i64, i64, vp, vp, vp, vp, i64, i64, i32, i32, u64, i32, i64, vp,
+                                     i64, vp, i64, vp]
+    lib.es_partition_rows.restype = st
+    lib.es_partition_rows.argtypes = [vp, i64, i32, i64, i32, vp]
+    lib.es_spmm_plan.restype = st
+    lib.es_spmm_plan.argtypes = [i64, i64, i64, vp, vp, ctypes.c_char_p, i32]
+    _lib = lib
+    return lib
+
+
+def _check(rc: int, what: str):
+    if rc != ES_OK:
+        msg = load_library().es_status_string(rc).decode()
+        raise EsError(f"{what} failed: {msg}")
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    return t.data_ptr() or None
+
+
+def _stream(stream=None):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _dev(t, dtype, name):
+    import torch
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise EsError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if t.dtype != dtype:
+        raise EsError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise EsError(f"{name} must be contiguous")
+    return t
+
+
+# ---------------------------------------------------------------------------- API
+def es_status_string(rc: int) -> str:
+    return load_library().es_status_string(rc).decode()
+
+
+def es_launch_count() -> int:
+    return int(load_library().es_launch_count())
+
+
+def es_spmm_plan(F: int, ldb: int, ldc: int, B=None, C=None) -> str:
+    buf = ctypes.create_string_buffer(128)
+    _check(load_library().es_spmm_plan(F, ldb, ldc, _ptr(B), _ptr(C), buf, 128), "es_spmm_plan")
+    return buf.value.decode()
+
+
+def es_spmm_sample(rowptr, colind, val, s: int, strategy: int, seed: int = 0, row_base: int = 0,
+                   n_cols: int = 0, want_pos: bool = True, stream=None):
+    """Materialised sampled CSR (slot order, duplicates kept):
+    returns (s_rowptr int64, s_colind int32, s_val fp32, s_pos int64 or None) on the device."""
+    import torch
+    lib = load_library()
+    _dev(rowptr, torch.int64, "rowptr")
+    _dev(colind, torch.int32, "colind")
+    _dev(val, torch.float32, "val")
+    n = rowptr.numel() - 1
+    dev = rowptr.device
+    s_rowptr = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    st = _stream(stream)
+    _check(lib.es_spmm_sample(n, n_cols, _ptr(rowptr), _ptr(colind), _ptr(val), s, strategy,
+                              seed & (2**64 - 1), row_base, _ptr(s_rowptr), None, None, None, st),
+           "es_spmm_sample(count)")
+    K = int(s_rowptr[-1].item())                       # the caller's D->H read of the size
+    s_colind = torch.empty(K, dtype=torch.int32, device=dev)
+    s_val = torch.empty(K, dtype=torch.float32, device=dev)
+    s_pos = torch.empty(K, dtype=torch.int64, device=dev) if want_pos else None
+    if K > 0:
+        _check(lib.es_spmm_sample(n, n_cols, _ptr(rowptr), _ptr(colind), _ptr(val), s, strategy,
+                                  seed & (2**64 - 1), row_base, _ptr(s_rowptr), _ptr(s_colind),
+                                  _ptr(s_val), _ptr(s_pos), st), "es_spmm_sample(materialize)")
+    return s_rowptr, s_colind, s_val, s_pos
+
+
+def es_spmm_run(rowptr, colind, val, B, s: int, strategy: int, seed: int = 0,
+                reduce: int = ES_REDUCE_SUM, F: int | None = None, C=None, stream=None):
+    """C = sampled SpMM (n_rows x F, row-major, ldc = C.stride(0)).  B: (n_cols, ldb) fp32."""
+    import torch
+    _dev(rowptr, torch.int64, "rowptr")
+    _dev(colind, torch.int32, "colind")
+    _dev(val, torch.float32, "val")
+    _dev(B, torch.float32, "B")
+    n = rowptr.numel() - 1
+    ldb = B.shape[1]
+    F = ldb if F is None else F
+    if C is None:
+        C = torch.empty((n, F), dtype=torch.float32, device=B.device)
+    if C.dim() != 2 or C.stride(1) != 1 or C.shape[0] < n or C.shape[1] < F:
+        raise EsError("C must be a row-major (n_rows, >=F) CUDA tensor")
+    _check(load_library().es_spmm_run(n, B.shape[0], _ptr(rowptr), _ptr(colind), _ptr(val), _ptr(B),
+                                      F, ldb, s, strategy, seed & (2**64 - 1), reduce, _ptr(C),
+                                      C.stride(0), _stream(stream)), "es_spmm_run")
+    return C
+
+
+def es_spmm_run_rows(n_rows: int, rowptr_slice, nnz_base: int, colind_slice, val_slice, B, s: int,
+                     strategy: int, seed: int, reduce: int, row_begin: int, row_end: int,
+                     F: int | None = None, C=None, stream=None):
+    """Rows [row_begin, row_end) of a global CSR of n_rows rows, from a slice
+    (rowptr entries for rows row_begin..row_end, absolute; colind/val offset by nnz_base)."""
+    import torch
+    _dev(rowptr_slice, torch.int64, "rowptr")
+    _dev(colind_slice, torch.int32, "colind")
+    _dev(val_slice, torch.float32, "val")
+    _dev(B, torch.float32, "B")
+    ldb = B.shape[1]
+    F = ldb if F is None else F
+    n = row_end - row_begin
+    if C is None:
+        C = torch.empty((n, F), dtype=torch.float32, device=B.device)
+    _check(load_library().es_spmm_run_rows(n_rows, B.shape[0], _ptr(rowptr_slice), nnz_base,
+                                           _ptr(colind_slice), _ptr(val_slice), _ptr(B), F, ldb, s,
+                                           strategy, seed & (2**64 - 1), reduce, _ptr(C), C.stride(0),
+                                           row_begin, row_end, _stream(stream)), "es_spmm_run_rows")
+    return C
+
+
+def es_spmm_host_workspace_bytes(n_rows, n_cols, nnz, F, ldb, has_val) -> int:
+    return int(load_library().es_spmm_host_workspace_bytes(n_rows, n_cols, nnz, F, ldb, int(has_val)))
+
+
+def es_spmm_run_host(rowptr, colind, val, B, s: int, strategy: int, seed: int = 0,
+                     reduce: int = ES_REDUCE_SUM, F: int | None = None, C=None, workspace=None,
+                     row_base: int = 0, stream=None):
+    """End-to-end call on HOST (ideally pinned) torch/numpy buffers; returns host C."""
+    import torch
+
+    def host(t, dtype):
+        if t is None:
+            return None
+        if isinstance(t, np.ndarray):
+            t = torch.from_numpy(t)
+        if t.is_cuda or t.dtype != dtype or not t.is_contiguous():
+            raise EsError("es_spmm_run_host takes contiguous host tensors")
+        return t
+
+    rowptr, colind, val = host(rowptr, torch.int64), host(colind, torch.int32), host(val, torch.float32)
+    B = host(B, torch.float32)
+    n = rowptr.numel() - 1
+    ldb = B.shape[1]
+    F = ldb if F is None else F
+    if C is None:
+        C = torch.empty((n, F), dtype=torch.float32, pin_memory=True)
+    nnz = int(rowptr[-1]) - int(rowptr[0]) if n >= 0 else 0
+    need = es_spmm_host_workspace_bytes(n, B.shape[0], nnz, F, ldb, val is not None)
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device="cuda")
+    _check(load_library().es_spmm_run_host(n, B.shape[0], _ptr(rowptr), _ptr(colind), _ptr(val),
+                                           _ptr(B), F, ldb, s, strategy, seed & (2**64 - 1), reduce,
+                                           row_base, _ptr(C), C.stride(0), _ptr(workspace), workspace.numel(),
+                                           _stream(stream)), "es_spmm_run_host")
+    return C
+
+
+def es_partition_rows(rowptr_host, s: int, F: int, n_parts: int) -> np.ndarray:
+    """Deterministic contiguous row blocks balanced by sampled bytes (host)."""
+    rp = np.ascontiguousarray(np.asarray(rowptr_host), dtype=np.int64)
+    bounds = np.empty(n_parts + 1, dtype=np.int64)
+    _check(load_library().es_partition_rows(rp.ctypes.data, len(rp) - 1, s, F, n_parts,
+                                            bounds.ctypes.data), "es_partition_rows")
+    return bounds

@@ -1,0 +1,260 @@
+// es_abi.cu -- the extern "C" boundary (include/es_spmm.h): argument validation,
+// kernel selection, the host-buffer pipeline and the row partitioner.
+#include <algorithm>
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "es_internal.h"
+#include "es_spmm.h"
+
+namespace {
+
+std::atomic<int64_t> g_launches{0};
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+es_status_t check_common(int64_t n_rows, int64_t n_cols, int64_t F, int64_t ldb, int64_t ldc,
+                         int32_t s, int32_t strategy, int32_t reduce) {
+    if (n_rows < 0 || n_cols < 0 || F < 1 || ldb < F || ldc < F || s < 1) return ES_ERR_INVALID_VALUE;
+    if (strategy != ES_BUCKET && strategy != ES_FASTRAND) return ES_ERR_INVALID_VALUE;
+    if (reduce != ES_REDUCE_SUM && reduce != ES_REDUCE_MEAN) return ES_ERR_INVALID_VALUE;
+    return ES_OK;
+}
+
+es_status_t run_rows_impl(int64_t n_rows, int64_t n_cols, const int64_t* rowptr, int64_t nnz_base,
+                          const int32_t* colind, const float* val, const float* B, int64_t F,
+                          int64_t ldb, int32_t s, int32_t strategy, uint64_t seed, int32_t reduce,
+                          float* C, int64_t ldc, int64_t row_begin, int64_t row_end,
+                          cudaStream_t st) {
+    es_status_t rc = check_common(n_rows, n_cols, F, ldb, ldc, s, strategy, reduce);
+    if (rc != ES_OK) return rc;
+    if (row_begin < 0 || row_end < row_begin || row_end > n_rows) return ES_ERR_INVALID_VALUE;
+    const int64_t n = row_end - row_begin;
+    if (n == 0) return ES_OK;
+    if (!rowptr || !C || (n_cols > 0 && !B)) return ES_ERR_INVALID_VALUE;
+    es::SpmmParams p{};
+    p.rowptr = rowptr;
+    p.nnz_base = nnz_base;
+    p.colind = colind;
+    p.val = val;
+    p.B = B;
+    p.F = F;
+    p.ldb = ldb;
+    p.s = s;
+    p.strategy = strategy;
+    p.seed = seed;
+    p.reduce = reduce;
+    p.C = C;
+    p.ldc = ldc;
+    p.n_rows = n;
+    p.row_base = row_begin;
+    const es::Plan plan = es::make_plan(F, ldb, ldc, B, C);
+    cudaError_t err = es::launch_spmm(p, plan, st);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return err == cudaSuccess ? ES_OK : ES_ERR_CUDA;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* es_status_string(es_status_t status) {
+    switch (status) {
+        case ES_OK: return "ES_OK";
+        case ES_ERR_INVALID_VALUE: return "ES_ERR_INVALID_VALUE";
+        case ES_ERR_MISALIGNED: return "ES_ERR_MISALIGNED";
+        case ES_ERR_UNSUPPORTED: return "ES_ERR_UNSUPPORTED";
+        case ES_ERR_CUDA: return "ES_ERR_CUDA";
+    }
+    return "ES_ERR_UNKNOWN";
+}
+
+int64_t es_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+es_status_t es_spmm_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C,
+                         char* buf, int32_t buf_len) {
+    if (F < 1 || ldb < F || ldc < F || !buf || buf_len < 1) return ES_ERR_INVALID_VALUE;
+    const es::Plan pl = es::make_plan(F, ldb, ldc, B, C);
+    if (pl.tma)
+        snprintf(buf, (size_t)buf_len, "es::spmm_tma<nch%d,stages%d>(warps/cta %d, rows/warp %d)%s", pl.nch,
+                 pl.stages, pl.warps_per_cta, pl.rows_per_warp, pl.c_vec ? "" : " (scalar C)");
+    else if (pl.subwarp)
+        snprintf(buf, (size_t)buf_len, "es::spmm_subwarp<vec%d,g%d>%s", pl.vec, pl.g, pl.c_vec ? "" : " (scalar C)");
+    else
+        snprintf(buf, (size_t)buf_len, "es::spmm_warp<vec%d,nch%d>%s", pl.vec, pl.nch, pl.c_vec ? "" : " (scalar C)");
+    return ES_OK;
+}
+
+es_status_t es_spmm_sample(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
+                           const int32_t* colind, const float* val, int32_t s, int32_t strategy,
+                           uint64_t seed, int64_t row_base, int64_t* s_rowptr, int32_t* s_colind,
+                           float* s_val, int64_t* s_pos, void* stream) {
+    if (n_rows < 0 || n_cols < 0 || s < 1 || row_base < 0) return ES_ERR_INVALID_VALUE;
+    if (strategy != ES_BUCKET && strategy != ES_FASTRAND) return ES_ERR_INVALID_VALUE;
+    if (!rowptr || !s_rowptr) return ES_ERR_INVALID_VALUE;
+    cudaStream_t st = as_stream(stream);
+    int launches = 0;
+    cudaError_t err = es::launch_sample_count(rowptr, n_rows, s, s_rowptr, st, &launches);
+    g_launches.fetch_add(launches, std::memory_order_relaxed);
+    if (err != cudaSuccess) return ES_ERR_CUDA;
+    if (!s_colind || n_rows == 0) return ES_OK;
+    // nnz_base: colind/val are indexed with the absolute rowptr entries.
+    err = es::launch_sample_materialize(rowptr, 0, colind, val, n_rows, s, strategy, seed, row_base,
+                                        s_rowptr, s_colind, s_val, s_pos, st);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return err == cudaSuccess ? ES_OK : ES_ERR_CUDA;
+}
+
+es_status_t es_spmm_run(int64_t n_rows, int64_t n_cols, const int64_t* rowptr, const int32_t* colind,
+                        const float* val, const float* B, int64_t F, int64_t ldb, int32_t s,
+                        int32_t strategy, uint64_t seed, int32_t reduce, float* C, int64_t ldc,
+                        void* stream) {
+    return run_rows_impl(n_rows, n_cols, rowptr, 0, colind, val, B, F, ldb, s, strategy, seed, reduce,
+                         C, ldc, 0, n_rows, as_stream(stream));
+}
+
+es_status_t es_spmm_run_rows(int64_t n_rows, int64_t n_cols, const int64_t* rowptr, int64_t nnz_base,
+                             const int32_t* colind, const float* val, const float* B, int64_t F,
+                             int64_t ldb, int32_t s, int32_t strategy, uint64_t seed, int32_t reduce,
+                             float* C, int64_t ldc, int64_t row_begin, int64_t row_end, void* stream) {
+    return run_rows_impl(n_rows, n_cols, rowptr, nnz_base, colind, val, B, F, ldb, s, strategy, seed,
+                         reduce, C, ldc, row_begin, row_end, as_stream(stream));
+}
+
+es_status_t es_partition_rows(const int64_t* rowptr_host, int64_t n_rows, int32_t s, int64_t F,
+                              int32_t n_parts, int64_t* bounds_host) {
+    if (!rowptr_host || !bounds_host || n_rows < 0 || s < 1 || F < 1 || n_parts < 1)
+        return ES_ERR_INVALID_VALUE;
+    // prefix[r] = sum_{i<r} w_i, w_i = k_i*(4F+8) + 4F  (exact int64 arithmetic)
+    std::vector<int64_t> prefix((size_t)n_rows + 1, 0);
+    for (int64_t i = 0; i < n_rows; ++i) {
+        const int64_t d = rowptr_host[i + 1] - rowptr_host[i];
+        const int64_t k = d < (int64_t)s ? d : (int64_t)s;
+        prefix[(size_t)i + 1] = prefix[(size_t)i] + k * (4 * F + 8) + 4 * F;
+    }
+    const int64_t total = prefix[(size_t)n_rows];
+    bounds_host[0] = 0;
+    for (int32_t p = 1; p < n_parts; ++p) {
+        // smallest r with prefix[r] >= ceil(total * p / P)  (128-bit to avoid overflow)
+        const __int128 num = (__int128)total * p;
+        const int64_t target = (int64_t)((num + n_parts - 1) / n_parts);
+        int64_t r = (int64_t)(std::lower_bound(prefix.begin(), prefix.end(), target) - prefix.begin());
+        r = std::max(r, bounds_host[p - 1]);
+        bounds_host[p] = std::min(r, n_rows);
+    }
+    bounds_host[n_parts] = n_rows;
+    return ES_OK;
+}
+
+// ---------------------------------------------------------------- host-buffer pipeline
+static inline int64_t align256(int64_t x) { return (x + 255) & ~(int64_t)255; }
+
+int64_t es_spmm_host_workspace_bytes(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t F,
+                                     int64_t ldb, int32_t has_val) {
+    (void)F;
+    if (n_rows < 0 || n_cols < 0 || nnz < 0 || ldb < 1) return -1;
+    return align256((n_rows + 1) * 8) + align256(nnz * 4) + (has_val ? align256(nnz * 4) : 0) +
+           align256(n_cols * ldb * 4) + align256(n_rows * ldb * 4);
+}
+
+es_status_t es_spmm_run_host(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
+                             const int32_t* colind, const float* val, const float* B, int64_t F,
+                             int64_t ldb, int32_t s, int32_t strategy, uint64_t seed, int32_t reduce,
+                             int64_t row_base, float* C, int64_t ldc, void* workspace,
+                             int64_t workspace_bytes, void* stream) {
+    es_status_t rc = check_common(n_rows, n_cols, F, ldb, ldc, s, strategy, reduce);
+    if (rc != ES_OK) return rc;
+    if (n_rows == 0) return ES_OK;
+    if (!rowptr || !C || !workspace || (n_cols > 0 && !B) || row_base < 0) return ES_ERR_INVALID_VALUE;
+    const int64_t base = rowptr[0];
+    const int64_t nnz = rowptr[n_rows] - base;
+    if (nnz > 0 && !colind) return ES_ERR_INVALID_VALUE;
+    const int64_t need = es_spmm_host_workspace_bytes(n_rows, n_cols, nnz, F, ldb, val != nullptr);
+    if (workspace_bytes < need) return ES_ERR_INVALID_VALUE;
+
+    // device workspace layout; the device C uses ldc' = ldb (dense, 16 B rows when ldb % 4 == 0)
+    char* w = static_cast<char*>(workspace);
+    int64_t* d_rowptr = reinterpret_cast<int64_t*>(w); w += align256((n_rows + 1) * 8);
+    int32_t* d_colind = reinterpret_cast<int32_t*>(w); w += align256(nnz * 4);
+    float* d_val = nullptr;
+    if (val) { d_val = reinterpret_cast<float*>(w); w += align256(nnz * 4); }
+    float* d_B = reinterpret_cast<float*>(w); w += align256(n_cols * ldb * 4);
+    float* d_C = reinterpret_cast<float*>(w);
+    const int64_t dldc = ldb;
+
+    cudaStream_t st = as_stream(stream);
+    cudaStream_t s_in = nullptr, s_out = nullptr;
+    const int kMaxChunks = 8;
+    int n_chunks = (int)std::min<int64_t>(kMaxChunks, std::max<int64_t>(1, n_rows / 4096));
+    std::vector<cudaEvent_t> ev_in((size_t)n_chunks, nullptr), ev_done((size_t)n_chunks, nullptr);
+    cudaEvent_t ev_start = nullptr, ev_out = nullptr;
+    cudaError_t err = cudaSuccess;
+    auto ok = [&](cudaError_t e) { if (err == cudaSuccess && e != cudaSuccess) err = e; return err == cudaSuccess; };
+
+    if (!ok(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking)) ||
+        !ok(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking)) ||
+        !ok(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming)) ||
+        !ok(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming))) goto cleanup;
+    for (int c = 0; c < n_chunks; ++c)
+        if (!ok(cudaEventCreateWithFlags(&ev_in[(size_t)c], cudaEventDisableTiming)) ||
+            !ok(cudaEventCreateWithFlags(&ev_done[(size_t)c], cudaEventDisableTiming))) goto cleanup;
+
+    // inputs may only be overwritten after earlier work on the caller's stream
+    if (!ok(cudaEventRecord(ev_start, st)) || !ok(cudaStreamWaitEvent(s_in, ev_start, 0))) goto cleanup;
+    if (!ok(cudaMemcpyAsync(d_rowptr, rowptr, (size_t)(n_rows + 1) * 8, cudaMemcpyHostToDevice, s_in)))
+        goto cleanup;
+    if (n_cols > 0 &&
+        !ok(cudaMemcpyAsync(d_B, B, (size_t)(n_cols * ldb) * 4, cudaMemcpyHostToDevice, s_in))) goto cleanup;
+    {
+        int64_t r0 = 0;
+        for (int c = 0; c < n_chunks; ++c) {
+            // rows [r0, r1) hold ~nnz/n_chunks nonzeros
+            int64_t r1 = n_rows;
+            if (c + 1 < n_chunks) {
+                const int64_t target = base + (nnz * (c + 1)) / n_chunks;
+                r1 = (int64_t)(std::lower_bound(rowptr, rowptr + n_rows + 1, target) - rowptr);
+                r1 = std::max(r0, std::min(r1, n_rows));
+            }
+            const int64_t e0 = rowptr[r0] - base, e1 = rowptr[r1] - base;
+            if (e1 > e0) {
+                if (!ok(cudaMemcpyAsync(d_colind + e0, colind + e0, (size_t)(e1 - e0) * 4,
+                                        cudaMemcpyHostToDevice, s_in))) goto cleanup;
+                if (val && !ok(cudaMemcpyAsync(d_val + e0, val + e0, (size_t)(e1 - e0) * 4,
+                                               cudaMemcpyHostToDevice, s_in))) goto cleanup;
+            }
+            if (!ok(cudaEventRecord(ev_in[(size_t)c], s_in)) || !ok(cudaStreamWaitEvent(st, ev_in[(size_t)c], 0)))
+                goto cleanup;
+            rc = run_rows_impl(row_base + n_rows, n_cols, d_rowptr + r0, base, d_colind, d_val, d_B, F,
+                               ldb, s, strategy, seed, reduce, d_C + r0 * dldc, dldc, row_base + r0,
+                               row_base + r1, st);
+            if (rc != ES_OK) goto cleanup;
+            if (!ok(cudaEventRecord(ev_done[(size_t)c], st)) || !ok(cudaStreamWaitEvent(s_out, ev_done[(size_t)c], 0)))
+                goto cleanup;
+            if (r1 > r0 &&
+                !ok(cudaMemcpy2DAsync(C + r0 * ldc, (size_t)ldc * 4, d_C + r0 * dldc, (size_t)dldc * 4,
+                                      (size_t)F * 4, (size_t)(r1 - r0), cudaMemcpyDeviceToHost, s_out)))
+                goto cleanup;
+            r0 = r1;
+        }
+    }
+    if (!ok(cudaEventRecord(ev_out, s_out)) || !ok(cudaStreamWaitEvent(st, ev_out, 0))) goto cleanup;
+    ok(cudaStreamSynchronize(st));
+
+cleanup:
+    if (err != cudaSuccess) cudaStreamSynchronize(st);
+    for (auto e : ev_in) if (e) cudaEventDestroy(e);
+    for (auto e : ev_done) if (e) cudaEventDestroy(e);
+    if (ev_start) cudaEventDestroy(ev_start);
+    if (ev_out) cudaEventDestroy(ev_out);
+    if (s_in) { cudaStreamSynchronize(s_in); cudaStreamDestroy(s_in); }
+    if (s_out) { cudaStreamSynchronize(s_out); cudaStreamDestroy(s_out); }
+    if (rc != ES_OK) return rc;
+    return err == cudaSuccess ? ES_OK : ES_ERR_CUDA;
+}
+
+}  // extern "C"

@@ -1,0 +1,49 @@
+// es_internal.h -- internal (C++) interface between the C ABI layer and the kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace es {
+
+struct SpmmParams {
+    const int64_t* rowptr;   // local row r uses rowptr[r], rowptr[r+1] (absolute offsets)
+    int64_t nnz_base;        // subtracted from rowptr entries before indexing colind/val
+    const int32_t* colind;
+    const float* val;        // NULL => 1.0
+    const float* B;
+    int64_t F, ldb;
+    int32_t s, strategy;
+    uint64_t seed;
+    int32_t reduce;
+    int32_t c_vec;           // vector stores to C allowed
+    float* C;                // row r of this launch at C + r*ldc
+    int64_t ldc;
+    int64_t n_rows;          // rows in this launch
+    int64_t row_base;        // global id of local row 0 (seeded FastRand offset)
+    int64_t hot_deg;         // >0: B rows of columns with degree >= hot_deg get evict_last, others
+                             // evict_first (popularity proxy, full-graph launches only)
+};
+
+struct Plan {
+    int vec;        // floats per gather (4, 2, 1)
+    bool subwarp;   // small-F streamed mapping
+    int g;          // lanes per stream (subwarp)
+    int nch;        // vectors per lane per feature tile (warp)
+    bool c_vec;
+    bool tma;          // TMA-ring kernel (spmm_tma)
+    int stages;         // ring depth (tma)
+    int rows_per_warp;  // consecutive rows per warp (tma)
+    int warps_per_cta;  // independent warps per CTA (tma)
+    int minb;           // __launch_bounds__ min blocks per SM (tma register cap)
+};
+
+Plan make_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C);
+cudaError_t launch_spmm(SpmmParams p, const Plan& plan, cudaStream_t st);
+cudaError_t launch_sample_count(const int64_t* rowptr, int64_t n, int32_t s, int64_t* s_rowptr,
+                                cudaStream_t st, int* launches);
+cudaError_t launch_sample_materialize(const int64_t* rowptr, int64_t nnz_base, const int32_t* colind,
+                                      const float* val, int64_t n, int32_t s, int32_t strategy,
+                                      uint64_t seed, int64_t row_base, const int64_t* s_rowptr,
+                                      int32_t* s_colind, float* s_val, int64_t* s_pos, cudaStream_t st);
+
+}  // namespace es

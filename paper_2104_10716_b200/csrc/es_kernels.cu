@@ -1,0 +1,587 @@
+// es_kernels.cu -- sm_100a kernels of the ES-SpMM hot path (arXiv 2104.10716).
+//
+// One fused kernel per call does all of SURVEY 8(a) a1-a5 for a row:
+//   a1  d_i, k_i = min(d_i, s)                     Alg. 1 l.5-6
+//   a2  sample positions p_j (Bucket / Eq. 2)      Alg. 1 l.8, L1042-1067
+//   a3  stage 1: (colind, val) of the k_i slots    Alg. 1 l.7-11 -- staged in REGISTERS,
+//       one slot per lane (coalesced for Bucket), broadcast by warp shuffles
+//   a4  stage 2: gather-FMA over B rows             Alg. 1 l.12-15 -- 128-bit vector
+//       gathers, several B rows in flight per lane, fp32 FMA into two interleaved
+//       partial sums (even / odd slots; R8 error bound)
+//   a5  epilogue: SUM, or MEAN = / k_i (IEEE)      Alg. 1 l.16, L1570-1575 (R5)
+//
+// Thread mapping: the paper's "group of threads per row, threads
+// on neighbouring columns of B" (L996-1001, L1093-1098) becomes, on B200,
+//   * spmm_warp   : one warp per row; lane l owns feature vectors l + 32c, c < NCH
+//                   (F/VEC > 16, e.g. F=128: 1 float4 / lane; F=602 (ldb 604): 5);
+//   * spmm_subwarp: F/VEC <= 16: the warp is split into E = 32/G streams of G lanes,
+//                   stream e sums slots j = e (mod E), then an xor-shuffle tree.
+// The summation order depends only on (k_i, F, vector width), never on which rows a
+// launch covers: row blocks computed on different GPUs are bitwise identical.
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <cuda_runtime.h>
+#include <cub/device/device_scan.cuh>
+
+#include "es_device.cuh"
+#include "es_internal.h"
+
+namespace es {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr unsigned kFull = 0xffffffffu;
+
+template <int VEC>
+__device__ __forceinline__ void store_out(float* Crow, int64_t vidx, int64_t F, const float* r,
+                                          bool c_vec, uint64_t pol) {
+    const int64_t c0 = vidx * VEC;
+    if (c_vec && c0 + VEC <= F) {
+        if constexpr (VEC == 4) st_stream4(Crow + c0, r, pol);
+        else if constexpr (VEC == 2) st_stream2(Crow + c0, r, pol);
+        else st_stream(Crow + c0, r[0], pol);
+    } else {
+#pragma unroll
+        for (int q = 0; q < VEC; ++q)
+            if (c0 + q < F) st_stream(Crow + c0 + q, r[q], pol);
+    }
+}
+
+__device__ __forceinline__ float finish(float x, int reduce, int32_t k) {
+    if (reduce == kMean) return k > 0 ? __fdiv_rn(x, (float)k) : 0.0f;
+    return x;
+}
+
+// ------------------------------------------------------------------ warp per row
+template <int VEC, int NCH, int U>
+__global__ void __launch_bounds__(kThreads)
+spmm_warp(const SpmmParams p) {
+    const int lane = threadIdx.x & 31;
+    const int64_t r = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+    if (r >= p.n_rows) return;
+    const uint64_t pol_a = policy_evict_first();
+    const uint64_t pol_b = policy_evict_last();
+
+    RowSampler rs;
+    rs.init(ld_stream(p.rowptr + r, pol_a) - p.nnz_base, ld_stream(p.rowptr + r + 1, pol_a) - p.nnz_base,
+            p.s, p.strategy, p.seed, p.row_base + r);
+    const int64_t NV = (p.F + VEC - 1) / VEC;
+    float* Crow = p.C + r * p.ldc;
+
+    for (int64_t v0 = 0; v0 < NV; v0 += 32 * NCH) {       // feature tiles (1 pass if NV <= 32*NCH)
+        // part: sequential sum over the (<= 32) slots of the current chunk; tot: sum of chunk
+        // partials (DESIGN.md §6 error bound: (31 + ceil(k/32)) u).
+        float part[NCH][VEC], tot[NCH][VEC];
+#pragma unroll
+        for (int c = 0; c < NCH; ++c)
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) { part[c][q] = 0.0f; tot[c][q] = 0.0f; }
+
+        for (int32_t j0 = 0; j0 < rs.k; j0 += 32) {
+            // stage 1 (a2+a3): lane l samples slot j0+l and loads its (col, val)
+            int32_t col = 0;
+            float a = 0.0f;
+            if (j0 + lane < rs.k) {
+                const int64_t e = rs.beg + rs.pos(j0 + lane);
+                col = ld_stream(p.colind + e, pol_a);
+                a = p.val ? ld_stream(p.val + e, pol_a) : 1.0f;
+            }
+            const int n_here = min(32, rs.k - j0);
+            // stage 2 (a4): U slots in flight
+            for (int t = 0; t < n_here; t += U) {
+                Vec<VEC> x[U][NCH];
+                float au[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int src = (t + u) & 31;
+                    const int32_t cu = __shfl_sync(kFull, col, src);
+                    const float av = __shfl_sync(kFull, a, src);
+                    const bool ok = (t + u) < n_here;
+                    au[u] = ok ? av : 0.0f;
+                    const float* brow = p.B + (int64_t)cu * p.ldb;
+#pragma unroll
+                    for (int c = 0; c < NCH; ++c) {
+                        const int64_t vidx = v0 + lane + 32 * c;
+                        if (ok && vidx < NV) {
+                            x[u][c] = ld_gather<VEC>(brow + vidx * VEC, pol_b);
+                        } else {
+#pragma unroll
+                            for (int q = 0; q < VEC; ++q) x[u][c].v[q] = 0.0f;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+#pragma unroll
+                    for (int c = 0; c < NCH; ++c)
+#pragma unroll
+                        for (int q = 0; q < VEC; ++q) part[c][q] = fmaf(au[u], x[u][c].v[q], part[c][q]);
+            }
+#pragma unroll
+            for (int c = 0; c < NCH; ++c)
+#pragma unroll
+                for (int q = 0; q < VEC; ++q) { tot[c][q] += part[c][q]; part[c][q] = 0.0f; }
+        }
+        // a5 epilogue
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+            const int64_t vidx = v0 + lane + 32 * c;
+            if (vidx < NV) {
+                float res[VEC];
+#pragma unroll
+                for (int q = 0; q < VEC; ++q) res[q] = finish(tot[c][q], p.reduce, rs.k);
+                store_out<VEC>(Crow, vidx, p.F, res, p.c_vec, pol_a);
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ sub-warp streams (small F)
+template <int VEC, int G, int U>
+__global__ void __launch_bounds__(kThreads)
+spmm_subwarp(const SpmmParams p) {
+    constexpr int E = 32 / G;                // edge streams per warp
+    const int lane = threadIdx.x & 31;
+    const int e = lane / G, g = lane % G;
+    const int64_t r = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+    if (r >= p.n_rows) return;
+    const uint64_t pol_a = policy_evict_first();
+    const uint64_t pol_b = policy_evict_last();
+
+    RowSampler rs;
+    rs.init(ld_stream(p.rowptr + r, pol_a) - p.nnz_base, ld_stream(p.rowptr + r + 1, pol_a) - p.nnz_base,
+            p.s, p.strategy, p.seed, p.row_base + r);
+    const int64_t NV = (p.F + VEC - 1) / VEC;    // <= G
+    float acc[VEC], part[VEC];        // acc: sum of per-chunk stream partials
+#pragma unroll
+    for (int q = 0; q < VEC; ++q) { acc[q] = 0.0f; part[q] = 0.0f; }
+
+    for (int32_t j0 = 0; j0 < rs.k; j0 += 32) {
+        int32_t col = 0;
+        float a = 0.0f;
+        if (j0 + lane < rs.k) {
+            const int64_t e_ = rs.beg + rs.pos(j0 + lane);
+            col = ld_stream(p.colind + e_, pol_a);
+            a = p.val ? ld_stream(p.val + e_, pol_a) : 1.0f;
+        }
+        const int n_here = min(32, rs.k - j0);
+        for (int t = 0; t < n_here; t += E * U) {
+            Vec<VEC> x[U];
+            float au[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int slot = t + u * E + e;
+                const int32_t cu = __shfl_sync(kFull, col, slot & 31);
+                const float av = __shfl_sync(kFull, a, slot & 31);
+                const bool ok = slot < n_here;
+                au[u] = ok ? av : 0.0f;
+                if (ok && g < NV) {
+                    x[u] = ld_gather<VEC>(p.B + (int64_t)cu * p.ldb + g * VEC, pol_b);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < VEC; ++q) x[u].v[q] = 0.0f;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int q = 0; q < VEC; ++q) part[q] = fmaf(au[u], x[u].v[q], part[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) { acc[q] += part[q]; part[q] = 0.0f; }
+    }
+    // reduce the E streams (xor butterfly: every lane ends with the same bits)
+#pragma unroll
+    for (int o = G; o < 32; o <<= 1)
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) acc[q] += __shfl_xor_sync(kFull, acc[q], o);
+    if (e == 0 && g < NV) {
+        float res[VEC];
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) res[q] = finish(acc[q], p.reduce, rs.k);
+        store_out<VEC>(p.C + r * p.ldc, g, p.F, res, p.c_vec, pol_a);
+    }
+}
+
+// ------------------------------------------------------------------ TMA ring (wide F)
+// One warp per CTA owns R <= 32 consecutive rows and a ring of STAGES B-row buffers in
+// shared memory.  The warp's sampled slots form one flat stream (row by row, slot order);
+// a producer cursor runs STAGES slots ahead of the consumer cursor, across row boundaries:
+// lane 0 issues one cp.async.bulk (a whole 16-B padded B row, ldb*4 bytes) per slot into
+// the stage the consumer just released, completion tracked by that stage's mbarrier
+// (expect_tx).  Bytes in flight are held by the TMA engine / smem, not registers, so
+// STAGES x (rows per SM) B rows are outstanding per SM.  Per-slot (col, val) come from a
+// chunk of 32 slots loaded coalesced by the whole warp, one chunk ahead.
+template <int NCH, int STAGES, int MINB>
+__global__ void __launch_bounds__(32, MINB)
+spmm_tma(const SpmmParams p, int R) {
+    extern __shared__ __align__(128) unsigned char smem_all[];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const uint32_t row_bytes = (uint32_t)(p.ldb * 4);       // multiple of 16 (ldb % 4 == 0)
+    const int64_t row_floats = p.ldb;
+    // per-warp region: ring | mbarriers | staged val   (independent warps, no CTA barrier)
+    const size_t region = ((size_t)STAGES * row_bytes + STAGES * 12 + 127) & ~(size_t)127;
+    unsigned char* smem = smem_all + warp * region;
+    float* ring = reinterpret_cast<float*>(smem);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (size_t)STAGES * row_bytes);
+    float* sval = reinterpret_cast<float*>(bar + STAGES);
+    const uint64_t pol_a = policy_evict_first();
+    const uint64_t pol_b = policy_evict_last();
+    const uint64_t pol_cold = policy_evict_first();
+
+    const int64_t r_begin = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * R;
+    if (r_begin >= p.n_rows) return;
+    const int nr = (int)min((int64_t)R, p.n_rows - r_begin);
+
+    // a1: per-row metadata, row i of this warp in lane i
+    RowSampler rs{};
+    int32_t kk = 0;
+    if (lane < nr) {
+        rs.init(ld_stream(p.rowptr + r_begin + lane, pol_a) - p.nnz_base,
+                ld_stream(p.rowptr + r_begin + lane + 1, pol_a) - p.nnz_base,
+                p.s, p.strategy, p.seed, p.row_base + r_begin + lane);
+        kk = rs.k;
+    }
+    int64_t incl = kk;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int64_t v = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += v;
+    }
+    const int64_t pre = incl - kk;                             // first flat slot of row `lane`
+    const int64_t T = __shfl_sync(kFull, incl, 31);           // slots of this warp
+
+    if (lane == 0) {
+        for (int i = 0; i < STAGES; ++i) mbar_init(&bar[i], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+
+    // a2+a3: (col, val) of flat slots [32c, 32c+32), lane l -> slot 32c + l
+    auto load_chunk = [&](int64_t c, int32_t& col, float& a, int& hot) {
+        const int64_t t = c * 32 + lane;
+        int row = 0;
+        for (int i = 1; i < nr; ++i)
+            if (__shfl_sync(kFull, pre, i) <= t) row = i;
+        const int64_t beg = __shfl_sync(kFull, rs.beg, row);
+        const int64_t d = __shfl_sync(kFull, rs.d, row);
+        const uint64_t off = __shfl_sync(kFull, rs.off, row);
+        const int narrow = __shfl_sync(kFull, (int)rs.narrow, row);
+        const int64_t j = t - __shfl_sync(kFull, pre, row);
+        col = 0;
+        a = 0.0f;
+        if (t < T) {
+            int64_t pos;
+            if (p.strategy == kBucket) pos = j;
+            else if (narrow) pos = (int64_t)(((uint32_t)off + (uint32_t)j * kPrime) % (uint32_t)d);
+            else pos = (int64_t)((off + (uint64_t)j * kPrime) % (uint64_t)d);
+            col = ld_stream(p.colind + beg + pos, pol_a);
+            a = p.val ? ld_stream(p.val + beg + pos, pol_a) : 1.0f;
+        }
+        hot = 1;
+        if (p.hot_deg > 0 && t < T)        // popularity proxy: degree of the column node
+            hot = (__ldg(p.rowptr + col + 1) - __ldg(p.rowptr + col)) >= p.hot_deg;
+    };
+
+    int32_t col_cur, col_nxt;
+    float a_cur, a_nxt;
+    int hot_cur, hot_nxt;
+    int64_t chunk_cur = 0;
+    load_chunk(0, col_cur, a_cur, hot_cur);
+    load_chunk(1, col_nxt, a_nxt, hot_nxt);
+    int64_t tp = 0;                                            // producer cursor (flat slot)
+
+    auto issue = [&]() {                                       // warp-collective
+        if (tp >= T) return;
+        if ((tp >> 5) != chunk_cur) {                          // advance to the prefetched chunk
+            col_cur = col_nxt;
+            a_cur = a_nxt;
+            hot_cur = hot_nxt;
+            ++chunk_cur;
+            load_chunk(chunk_cur + 1, col_nxt, a_nxt, hot_nxt);
+        }
+        const int32_t c = __shfl_sync(kFull, col_cur, (int)(tp & 31));
+        const float av = __shfl_sync(kFull, a_cur, (int)(tp & 31));
+        const int hv = __shfl_sync(kFull, hot_cur, (int)(tp & 31));
+        if (lane == 0) {
+            const int st = (int)(tp % STAGES);
+            sval[st] = av;
+            fence_proxy_async_smem();
+            mbar_arrive_expect_tx(&bar[st], row_bytes);
+            bulk_g2s(ring + (size_t)st * row_floats, p.B + (int64_t)c * p.ldb, row_bytes, &bar[st],
+                     hv ? pol_b : pol_cold);
+        }
+        ++tp;
+    };
+
+#pragma unroll 1
+    for (int i = 0; i < STAGES; ++i) issue();
+
+    // a4 + a5: consume rows in order
+    const int64_t NV = (p.F + 3) / 4;
+    int64_t tc = 0;                                            // consumer cursor
+#pragma unroll 1
+    for (int i = 0; i < nr; ++i) {
+        const int32_t k = __shfl_sync(kFull, kk, i);
+        float part[NCH][4], tot[NCH][4];
+#pragma unroll
+        for (int c = 0; c < NCH; ++c)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) { part[c][q] = 0.0f; tot[c][q] = 0.0f; }
+#pragma unroll 1
+        for (int32_t j = 0; j < k; ++j, ++tc) {
+            const int st = (int)(tc % STAGES);
+            mbar_wait(&bar[st], (uint32_t)((tc / STAGES) & 1));
+            const float av = sval[st];
+            const float* src = ring + (size_t)st * row_floats;
+#pragma unroll
+            for (int c = 0; c < NCH; ++c) {
+                const int64_t vidx = lane + 32 * c;
+                if (vidx < NV) {
+                    const float4 x = *reinterpret_cast<const float4*>(src + vidx * 4);
+                    part[c][0] = fmaf(av, x.x, part[c][0]);
+                    part[c][1] = fmaf(av, x.y, part[c][1]);
+                    part[c][2] = fmaf(av, x.z, part[c][2]);
+                    part[c][3] = fmaf(av, x.w, part[c][3]);
+                }
+            }
+            if ((j & 31) == 31) {
+#pragma unroll
+                for (int c = 0; c < NCH; ++c)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) { tot[c][q] += part[c][q]; part[c][q] = 0.0f; }
+            }
+            __syncwarp();
+            issue();                                           // refill the stage just released
+        }
+        float* Crow = p.C + (r_begin + i) * p.ldc;
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+            const int64_t vidx = lane + 32 * c;
+            if (vidx < NV) {
+                float res[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) res[q] = finish(tot[c][q] + part[c][q], p.reduce, k);
+                store_out<4>(Crow, vidx, p.F, res, p.c_vec, pol_a);
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ sampler (es_spmm_sample)
+__global__ void sample_count(const int64_t* __restrict__ rowptr, int64_t n, int32_t s,
+                             int64_t* __restrict__ s_rowptr) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) s_rowptr[0] = 0;
+    if (i < n) {
+        const int64_t d = rowptr[i + 1] - rowptr[i];
+        s_rowptr[i + 1] = d < (int64_t)s ? d : (int64_t)s;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads)
+sample_materialize(const int64_t* __restrict__ rowptr, int64_t nnz_base,
+                   const int32_t* __restrict__ colind, const float* __restrict__ val, int64_t n,
+                   int32_t s, int32_t strategy, uint64_t seed, int64_t row_base,
+                   const int64_t* __restrict__ s_rowptr, int32_t* __restrict__ s_colind,
+                   float* __restrict__ s_val, int64_t* __restrict__ s_pos) {
+    const int lane = threadIdx.x & 31;
+    const int64_t r = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+    if (r >= n) return;
+    RowSampler rs;
+    rs.init(rowptr[r] - nnz_base, rowptr[r + 1] - nnz_base, s, strategy, seed, row_base + r);
+    const int64_t o0 = s_rowptr[r];
+    for (int32_t j = lane; j < rs.k; j += 32) {
+        const int64_t pj = rs.pos(j);
+        const int64_t e = rs.beg + pj;
+        s_colind[o0 + j] = colind[e];
+        if (s_val) s_val[o0 + j] = val ? val[e] : 1.0f;
+        if (s_pos) s_pos[o0 + j] = pj;
+    }
+}
+
+// ------------------------------------------------------------------ host launchers
+namespace {
+
+template <int VEC, int NCH>
+cudaError_t launch_warp(const SpmmParams& p, cudaStream_t st) {
+    constexpr int U = NCH == 1 ? 8 : (NCH == 2 ? 4 : 2);
+    const int64_t blocks = (p.n_rows + kWarps - 1) / kWarps;
+    spmm_warp<VEC, NCH, U><<<(unsigned)blocks, kThreads, 0, st>>>(p);
+    return cudaGetLastError();
+}
+
+template <int VEC, int G>
+cudaError_t launch_subwarp(const SpmmParams& p, cudaStream_t st) {
+    const int64_t blocks = (p.n_rows + kWarps - 1) / kWarps;
+    spmm_subwarp<VEC, G, 4><<<(unsigned)blocks, kThreads, 0, st>>>(p);
+    return cudaGetLastError();
+}
+
+template <int NCH, int STAGES>
+cudaError_t launch_tma(const SpmmParams& p, const Plan& plan, cudaStream_t st) {
+    const size_t region = ((size_t)STAGES * (size_t)(p.ldb * 4) + STAGES * 12 + 127) & ~(size_t)127;
+    const int W = 1;
+    const size_t smem = region * W;
+    auto kern = plan.minb >= 32 ? spmm_tma<NCH, STAGES, 32>
+              : plan.minb >= 24 ? spmm_tma<NCH, STAGES, 24>
+              : plan.minb >= 16 ? spmm_tma<NCH, STAGES, 16> : spmm_tma<NCH, STAGES, 1>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    const int64_t rows_per_cta = (int64_t)plan.rows_per_warp * W;
+    const int64_t blocks = (p.n_rows + rows_per_cta - 1) / rows_per_cta;
+    kern<<<(unsigned)blocks, 32 * W, smem, st>>>(p, plan.rows_per_warp);
+    return cudaGetLastError();
+}
+
+template <int NCH>
+cudaError_t dispatch_tma_stages(const SpmmParams& p, const Plan& plan, cudaStream_t st) {
+    switch (plan.stages) {
+        case 2: return launch_tma<NCH, 2>(p, plan, st);
+        case 3: return launch_tma<NCH, 3>(p, plan, st);
+        case 4: return launch_tma<NCH, 4>(p, plan, st);
+        case 6: return launch_tma<NCH, 6>(p, plan, st);
+        default: return launch_tma<NCH, 8>(p, plan, st);
+    }
+}
+
+cudaError_t dispatch_tma(const SpmmParams& p, const Plan& plan, cudaStream_t st) {
+    switch (plan.nch) {
+        case 2: return dispatch_tma_stages<2>(p, plan, st);
+        case 3: return dispatch_tma_stages<3>(p, plan, st);
+        case 4: return dispatch_tma_stages<4>(p, plan, st);
+        case 5: return dispatch_tma_stages<5>(p, plan, st);
+        case 6: return dispatch_tma_stages<6>(p, plan, st);
+        case 7: return dispatch_tma_stages<7>(p, plan, st);
+        default: return dispatch_tma_stages<8>(p, plan, st);
+    }
+}
+
+template <int VEC>
+cudaError_t dispatch_vec(const SpmmParams& p, const Plan& plan, cudaStream_t st) {
+    if (plan.subwarp) {
+        switch (plan.g) {
+            case 1: return launch_subwarp<VEC, 1>(p, st);
+            case 2: return launch_subwarp<VEC, 2>(p, st);
+            case 4: return launch_subwarp<VEC, 4>(p, st);
+            case 8: return launch_subwarp<VEC, 8>(p, st);
+            default: return launch_subwarp<VEC, 16>(p, st);
+        }
+    }
+    switch (plan.nch) {
+        case 1: return launch_warp<VEC, 1>(p, st);
+        case 2: return launch_warp<VEC, 2>(p, st);
+        case 3: return launch_warp<VEC, 3>(p, st);
+        case 4: return launch_warp<VEC, 4>(p, st);
+        case 5: return launch_warp<VEC, 5>(p, st);
+        case 6: return launch_warp<VEC, 6>(p, st);
+        case 7: return launch_warp<VEC, 7>(p, st);
+        default: return launch_warp<VEC, 8>(p, st);
+    }
+}
+
+}  // namespace
+
+static int env_kernel_override() {
+    // ES_SPMM_KERNEL=warp|tma (tuning / A-B measurement only; default: auto)
+    const char* e = getenv("ES_SPMM_KERNEL");
+    if (!e) return 0;
+    if (!strcmp(e, "warp")) return 1;
+    if (!strcmp(e, "tma")) return 2;
+    return 0;
+}
+
+static int env_int(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return e ? atoi(e) : dflt;
+}
+
+Plan make_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C) {
+    Plan pl{};
+    const uintptr_t b = reinterpret_cast<uintptr_t>(B), c = reinterpret_cast<uintptr_t>(C);
+    if (b % 16 == 0 && ldb % 4 == 0) pl.vec = 4;
+    else if (b % 8 == 0 && ldb % 2 == 0) pl.vec = 2;
+    else pl.vec = 1;
+    const int64_t nv = (F + pl.vec - 1) / pl.vec;
+    if (nv <= 16) {
+        pl.subwarp = true;
+        int g = 1;
+        while (g < nv) g <<= 1;
+        pl.g = g;
+    } else {
+        pl.subwarp = false;
+        const int64_t nch = (nv + 31) / 32;
+        pl.nch = (int)(nch > 8 ? 8 : nch);
+    }
+    pl.c_vec = (c % (4u * (unsigned)pl.vec) == 0) && (ldc % pl.vec == 0);
+    // TMA ring: whole 16-B padded B rows as bulk copies; needs 16-B alignment and F <= 1024.
+    const int64_t nv4 = (F + 3) / 4;
+    // Measured (profiles/tune_r01.md): TMA wins for wide rows (Reddit F=602: 9.5 vs 26.8 ms,
+    // F=256: 4.8 vs 8.2 ms); for 512-B rows (F=128) the LDG warp kernel wins (2.97 vs 4.3 ms).
+    const int64_t kTmaMinRowBytes = env_int("ES_SPMM_TMA_MIN_BYTES", 1024);
+    const bool tma_ok = pl.vec == 4 && nv4 > 32 && nv4 <= 32 * 8;
+    const int ov = env_kernel_override();
+    pl.tma = tma_ok && ov != 1 && (ov == 2 || ldb * 4 >= kTmaMinRowBytes);
+    if (pl.tma) {
+        pl.nch = (int)((nv4 + 31) / 32);
+        pl.subwarp = false;
+        int stages = env_int("ES_SPMM_STAGES", 0);
+        if (stages != 2 && stages != 3 && stages != 4 && stages != 6 && stages != 8) stages = 4;
+        pl.stages = stages;
+        const int rpw = env_int("ES_SPMM_ROWS_PER_WARP", 0);
+        pl.rows_per_warp = (rpw >= 1 && rpw <= 32) ? rpw : 1;
+        pl.warps_per_cta = 1;
+        pl.minb = env_int("ES_SPMM_MINB", 1);
+    }
+    return pl;
+}
+
+cudaError_t launch_spmm(SpmmParams p, const Plan& plan, cudaStream_t st) {
+    if (p.n_rows <= 0) return cudaSuccess;
+    p.c_vec = plan.c_vec ? 1 : 0;
+    p.hot_deg = plan.tma ? env_int("ES_SPMM_HOT_DEG", 0) : 0;   // experiment (full-graph launches only)
+    if (p.hot_deg > 0 && (p.row_base != 0 || p.nnz_base != 0)) p.hot_deg = 0;
+    if (plan.tma) return dispatch_tma(p, plan, st);
+    switch (plan.vec) {
+        case 4: return dispatch_vec<4>(p, plan, st);
+        case 2: return dispatch_vec<2>(p, plan, st);
+        default: return dispatch_vec<1>(p, plan, st);
+    }
+}
+
+cudaError_t launch_sample_count(const int64_t* rowptr, int64_t n, int32_t s, int64_t* s_rowptr,
+                                cudaStream_t st, int* launches) {
+    const int64_t blocks = (n + 1 + 255) / 256;
+    sample_count<<<(unsigned)(blocks > 0 ? blocks : 1), 256, 0, st>>>(rowptr, n, s, s_rowptr);
+    ++*launches;
+    cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess || n == 0) return err;
+    size_t temp_bytes = 0;
+    err = cub::DeviceScan::InclusiveSum(nullptr, temp_bytes, s_rowptr + 1, s_rowptr + 1, n, st);
+    if (err != cudaSuccess) return err;
+    void* temp = nullptr;
+    err = cudaMallocAsync(&temp, temp_bytes, st);
+    if (err != cudaSuccess) return err;
+    err = cub::DeviceScan::InclusiveSum(temp, temp_bytes, s_rowptr + 1, s_rowptr + 1, n, st);
+    ++*launches;
+    cudaError_t err2 = cudaFreeAsync(temp, st);
+    return err != cudaSuccess ? err : err2;
+}
+
+cudaError_t launch_sample_materialize(const int64_t* rowptr, int64_t nnz_base, const int32_t* colind,
+                                      const float* val, int64_t n, int32_t s, int32_t strategy,
+                                      uint64_t seed, int64_t row_base, const int64_t* s_rowptr,
+                                      int32_t* s_colind, float* s_val, int64_t* s_pos, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    const int64_t blocks = (n + kWarps - 1) / kWarps;
+    sample_materialize<<<(unsigned)blocks, kThreads, 0, st>>>(rowptr, nnz_base, colind, val, n, s,
+                                                               strategy, seed, row_base, s_rowptr,
+                                                               s_colind, s_val, s_pos);
+    return cudaGetLastError();
+}
+
+}  // namespace es

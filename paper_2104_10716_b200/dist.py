@@ -1,0 +1,101 @@
+"""Multi-GPU driver: 1-D row-block data parallelism over one node.
+
+Every output row depends only on its own CSR row and on B (Alg. 1),
+so the path shards into contiguous row blocks balanced by sampled bytes
+(es_partition_rows, w_i = k_i(4F+8) + 4F).  Bounds are computed identically on every
+rank from the host rowptr.  With B replicated there is no collective on the data path;
+with B sharded by node blocks (the output of a previous layer) one all-gather of B
+precedes the SpMM, and optionally one all-gather of C follows it (input of the next
+layer).  Collectives go through torch.distributed (NCCL over NVLink 5 on B200; gloo in
+the CPU tests).  The FastRand offset uses GLOBAL row ids and the per-row summation order
+depends only on (k_i, F), so the gathered C is bitwise identical to a 1-GPU run.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+@dataclass
+class Shard:
+    rank: int
+    world: int
+    bounds: np.ndarray      # int64[world+1]
+    r0: int                 # first global row of this rank
+    r1: int                 # one past the last
+    e0: int                 # first nonzero (absolute)
+    e1: int
+
+
+def plan(rowptr_host: np.ndarray, s: int, F: int, world: int, rank: int, partition=None) -> Shard:
+    """Deterministic row blocks for `world` ranks (same on every rank)."""
+    if partition is None:
+        from . import es_partition_rows as partition
+    bounds = np.asarray(partition(rowptr_host, s, F, world), dtype=np.int64)
+    r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+    return Shard(rank, world, bounds, r0, r1, int(rowptr_host[r0]), int(rowptr_host[r1]))
+
+
+def local_csr(rowptr_host, colind_host, val_host, sh: Shard):
+    """This rank's CSR slice: rowptr entries stay ABSOLUTE (nnz_base = sh.e0)."""
+    rp = np.ascontiguousarray(rowptr_host[sh.r0:sh.r1 + 1])
+    ci = colind_host[sh.e0:sh.e1]
+    va = None if val_host is None else val_host[sh.e0:sh.e1]
+    return rp, ci, va
+
+
+def allgather_rows(local, bounds: np.ndarray, group=None):
+    """Concatenate per-rank row blocks (sizes from `bounds`) on every rank.
+    Blocks are padded to the largest block for the equal-size all_gather_into_tensor."""
+    import torch
+    import torch.distributed as dist
+    world = len(bounds) - 1
+    sizes = np.diff(bounds)
+    m = int(sizes.max()) if world else 0
+    tail = tuple(local.shape[1:])
+    buf = torch.zeros((m,) + tail, dtype=local.dtype, device=local.device)
+    buf[: local.shape[0]].copy_(local)
+    out = torch.empty((world * m,) + tail, dtype=local.dtype, device=local.device)
+    dist.all_gather_into_tensor(out, buf, group=group)
+    parts = [out[r * m: r * m + int(sizes[r])] for r in range(world)]
+    return torch.cat(parts, dim=0)
+
+
+def run_rows(sh: Shard, n_rows: int, rp, ci, va, B, F: int, s: int, strategy: int, seed: int,
+             reduce: int, C=None, stream=None, compute=None):
+    """This rank's rows through the C ABI (es_spmm_run_rows).  `compute` lets CPU tests
+    substitute a reference; the product default is the CUDA library (no fallback)."""
+    if compute is not None:
+        return compute(sh, n_rows, rp, ci, va, B, F, s, strategy, seed, reduce)
+    from . import es_spmm_run_rows
+    return es_spmm_run_rows(n_rows, rp, sh.e0, ci, va, B, s, strategy, seed, reduce, sh.r0, sh.r1,
+                            F=F, C=C, stream=stream)
+
+
+def sampled_spmm_distributed(rowptr_host, colind_host, val_host, B_local, F: int, s: int,
+                             strategy: int, seed: int = 0, reduce: int = 0, *, b_sharded=False,
+                             gather_c=False, group=None, device=None, compute=None, partition=None):
+    """One distributed sampled SpMM.
+
+    B_local: the full B (replicated) or, with b_sharded=True, this rank's node block
+    B[bounds[r]:bounds[r+1]] (rows follow the same partition).  Returns this rank's C
+    block, or the full C on every rank when gather_c=True."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    n_rows = len(rowptr_host) - 1
+    sh = plan(rowptr_host, s, F, world, rank, partition=partition)
+    rp, ci, va = local_csr(rowptr_host, colind_host, val_host, sh)
+    dev = device if device is not None else B_local.device
+
+    def t(a):
+        return None if a is None else torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+    B_full = allgather_rows(B_local, sh.bounds, group) if (b_sharded and world > 1) else B_local
+    C = run_rows(sh, n_rows, t(rp), t(ci), t(va), B_full, F, s, strategy, seed, reduce,
+                 compute=compute)
+    if gather_c and world > 1:
+        return allgather_rows(C, sh.bounds, group)
+    return C

@@ -1,0 +1,134 @@
+"""The C-ABI library loads and exports every symbol include/es_spmm.h declares; host-side
+logic (validation, partitioner, plan) works without a GPU.  No compute calls here."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2104_10716_b200 as es
+from paper_2104_10716_b200 import _build
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    _build.build()
+    return es.load_library()
+
+
+def test_header_declarations_are_exported(lib):
+    with open(os.path.join(ROOT, "include", "es_spmm.h")) as f:
+        text = f.read()
+    declared = set(re.findall(r"^\s*(?:es_status_t|int64_t|const char\*)\s+(es_\w+)\s*\(", text, re.M))
+    assert declared == set(es.EXPORTS), declared ^ set(es.EXPORTS)
+    for name in declared:
+        assert hasattr(lib, name), name
+    # the sm_100a cubin is embedded
+    blob = open(es.LIB_PATH, "rb").read()
+    assert b"sm_100a" in blob or b"sm_100" in blob
+
+
+def test_status_strings(lib):
+    assert es.es_status_string(0) == "ES_OK"
+    assert es.es_status_string(1) == "ES_ERR_INVALID_VALUE"
+    assert es.es_status_string(4) == "ES_ERR_CUDA"
+
+
+def test_host_validation_rejects_bad_arguments(lib):
+    vp = ctypes.c_void_p
+    dummy = vp(16)
+    ok = dict(n_rows=10, n_cols=10, F=8, ldb=8, s=4, strategy=2, reduce=0, ldc=8)
+
+    def run(**kw):
+        a = dict(ok, **kw)
+        return lib.es_spmm_run(a["n_rows"], a["n_cols"], dummy, dummy, None, dummy, a["F"], a["ldb"],
+                               a["s"], a["strategy"], 0, a["reduce"], dummy, a["ldc"], None)
+
+    assert run(s=0) == es.ES_ERR_INVALID_VALUE
+    assert run(F=0) == es.ES_ERR_INVALID_VALUE
+    assert run(ldb=7) == es.ES_ERR_INVALID_VALUE
+    assert run(ldc=7) == es.ES_ERR_INVALID_VALUE
+    assert run(strategy=3) == es.ES_ERR_INVALID_VALUE
+    assert run(reduce=2) == es.ES_ERR_INVALID_VALUE
+    assert run(n_rows=-1) == es.ES_ERR_INVALID_VALUE
+    assert run(n_rows=0) == es.ES_OK          # nothing to launch
+    # NULL required pointers
+    assert lib.es_spmm_run(10, 10, None, dummy, None, dummy, 8, 8, 4, 2, 0, 0, dummy, 8, None) == 1
+    assert lib.es_spmm_run(10, 10, dummy, dummy, None, dummy, 8, 8, 4, 2, 0, 0, None, 8, None) == 1
+    # row range checks
+    assert lib.es_spmm_run_rows(10, 10, dummy, 0, dummy, None, dummy, 8, 8, 4, 2, 0, 0, dummy, 8,
+                                5, 11, None) == 1
+    assert lib.es_spmm_run_rows(10, 10, dummy, 0, dummy, None, dummy, 8, 8, 4, 2, 0, 0, dummy, 8,
+                                6, 5, None) == 1
+    assert lib.es_spmm_sample(10, 10, dummy, dummy, None, 0, 2, 0, 0, dummy, None, None, None,
+                              None) == 1
+    assert lib.es_spmm_sample(10, 10, dummy, dummy, None, 3, 9, 0, 0, dummy, None, None, None,
+                              None) == 1
+
+
+def test_plan_selection(lib, monkeypatch):
+    assert es.es_spmm_plan(128, 128, 128).startswith("es::spmm_warp<vec4,nch1>")   # 512-B rows
+    assert es.es_spmm_plan(256, 256, 256).startswith("es::spmm_tma<nch2,stages4>")
+    assert es.es_spmm_plan(602, 604, 604).startswith("es::spmm_tma<nch5,stages4>")
+    monkeypatch.setenv("ES_SPMM_KERNEL", "warp")
+    assert es.es_spmm_plan(128, 128, 128).startswith("es::spmm_warp<vec4,nch1>")
+    assert "vec4,nch5" in es.es_spmm_plan(602, 604, 604)
+    monkeypatch.delenv("ES_SPMM_KERNEL")
+    assert "spmm_warp<vec2" in es.es_spmm_plan(602, 602, 602)      # 8-B rows: no TMA
+    assert "subwarp<vec4,g4>" in es.es_spmm_plan(16, 16, 16)
+    assert "subwarp<vec1,g1>" in es.es_spmm_plan(1, 1, 1)
+    assert "spmm_warp<vec4,nch8>" in es.es_spmm_plan(5000, 5000, 5000)   # feature-tiled
+
+
+class _B:
+    def __init__(self, p):
+        self.p = p
+
+    def data_ptr(self):
+        return self.p
+
+
+def test_plan_alignment_fallback(lib):
+    # B misaligned by 4 bytes -> scalar gathers; C misaligned -> scalar stores
+    assert "vec1" in es.es_spmm_plan(128, 128, 128, B=_B(0x1004), C=_B(0x1000))
+    assert "scalar C" in es.es_spmm_plan(128, 128, 128, B=_B(0x1000), C=_B(0x1004))
+
+
+def _ref_bounds(rowptr, s, F, P):
+    d = np.diff(rowptr)
+    w = np.minimum(d, s) * (4 * F + 8) + 4 * F
+    pre = np.concatenate([[0], np.cumsum(w)])
+    tot = int(pre[-1])
+    out = [0]
+    for p in range(1, P):
+        tgt = -(-tot * p // P)
+        r = int(np.searchsorted(pre, tgt, side="left"))
+        out.append(max(min(r, len(d)), out[-1]))
+    out.append(len(d))
+    return np.array(out)
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 4, 8])
+def test_partition_rows(lib, P):
+    rng = np.random.default_rng(P)
+    d = np.minimum((rng.pareto(1.1, 5000) * 20).astype(np.int64), 20000)
+    rowptr = np.concatenate([[0], np.cumsum(d)])
+    for s, F in [(256, 602), (16, 128), (10**9, 64)]:
+        b = es.es_partition_rows(rowptr, s, F, P)
+        assert b[0] == 0 and b[-1] == 5000 and np.all(np.diff(b) >= 0)
+        assert np.array_equal(b, _ref_bounds(rowptr, s, F, P))
+        # balance: every part within one max-row weight of the ideal share
+        w = np.minimum(d, s) * (4 * F + 8) + 4 * F
+        parts = [w[b[i]:b[i + 1]].sum() for i in range(P)]
+        assert max(parts) - w.sum() / P <= w.max()
+    # with s >= max degree the weights are nnz-proportional (+ per-row constant)
+    b = es.es_partition_rows(rowptr, 10**9, 1, P)
+    assert np.array_equal(b, _ref_bounds(rowptr, 10**9, 1, P))
+
+
+def test_partition_degenerate(lib):
+    assert es.es_partition_rows(np.zeros(1, np.int64), 4, 8, 3).tolist() == [0, 0, 0, 0]
+    assert es.es_partition_rows(np.array([0, 5], np.int64), 4, 8, 4).tolist()[-1] == 1
