@@ -81,8 +81,8 @@ es_status_t es_spmm_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, con
     if (F < 1 || ldb < F || ldc < F || !buf || buf_len < 1) return ES_ERR_INVALID_VALUE;
     const es::Plan pl = es::make_plan(F, ldb, ldc, B, C);
     if (pl.tma)
-        snprintf(buf, (size_t)buf_len, "es::spmm_tma<nch%d,stages%d>(warps/cta %d, rows/warp %d)%s", pl.nch,
-                 pl.stages, pl.warps_per_cta, pl.rows_per_warp, pl.c_vec ? "" : " (scalar C)");
+        snprintf(buf, (size_t)buf_len, "es::spmm_tma<nch%d,stages%d>(rows/warp %d)%s", pl.nch, pl.stages,
+                 pl.rows_per_warp, pl.c_vec ? "" : " (scalar C)");
     else if (pl.subwarp)
         snprintf(buf, (size_t)buf_len, "es::spmm_subwarp<vec%d,g%d>%s", pl.vec, pl.g, pl.c_vec ? "" : " (scalar C)");
     else

@@ -20,8 +20,6 @@ struct SpmmParams {
     int64_t ldc;
     int64_t n_rows;          // rows in this launch
     int64_t row_base;        // global id of local row 0 (seeded FastRand offset)
-    int64_t hot_deg;         // >0: B rows of columns with degree >= hot_deg get evict_last, others
-                             // evict_first (popularity proxy, full-graph launches only)
 };
 
 struct Plan {
@@ -33,8 +31,8 @@ struct Plan {
     bool tma;          // TMA-ring kernel (spmm_tma)
     int stages;         // ring depth (tma)
     int rows_per_warp;  // consecutive rows per warp (tma)
-    int warps_per_cta;  // independent warps per CTA (tma)
     int minb;           // __launch_bounds__ min blocks per SM (tma register cap)
+    int u;              // slots in flight per lane (warp kernel, NCH == 1: 8 or 16)
 };
 
 Plan make_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C);

@@ -78,14 +78,20 @@ spmm_warp(const SpmmParams p) {
 #pragma unroll
             for (int q = 0; q < VEC; ++q) { part[c][q] = 0.0f; tot[c][q] = 0.0f; }
 
+        // stage 1 (a2+a3): lane l samples slot j0+l and loads its (col, val); the next
+        // chunk's pair is requested before this chunk's gathers (one chunk of lookahead)
+        int32_t col = 0, col_n = 0;
+        float a = 0.0f, a_n = 0.0f;
+        if (lane < rs.k) {
+            const int64_t e = rs.beg + rs.pos(lane);
+            col = ld_stream(p.colind + e, pol_a);
+            a = p.val ? ld_stream(p.val + e, pol_a) : 1.0f;
+        }
         for (int32_t j0 = 0; j0 < rs.k; j0 += 32) {
-            // stage 1 (a2+a3): lane l samples slot j0+l and loads its (col, val)
-            int32_t col = 0;
-            float a = 0.0f;
-            if (j0 + lane < rs.k) {
-                const int64_t e = rs.beg + rs.pos(j0 + lane);
-                col = ld_stream(p.colind + e, pol_a);
-                a = p.val ? ld_stream(p.val + e, pol_a) : 1.0f;
+            if (j0 + 32 + lane < rs.k) {
+                const int64_t e = rs.beg + rs.pos(j0 + 32 + lane);
+                col_n = ld_stream(p.colind + e, pol_a);
+                a_n = p.val ? ld_stream(p.val + e, pol_a) : 1.0f;
             }
             const int n_here = min(32, rs.k - j0);
             // stage 2 (a4): U slots in flight
@@ -122,6 +128,8 @@ spmm_warp(const SpmmParams p) {
             for (int c = 0; c < NCH; ++c)
 #pragma unroll
                 for (int q = 0; q < VEC; ++q) { tot[c][q] += part[c][q]; part[c][q] = 0.0f; }
+            col = col_n;
+            a = a_n;
         }
         // a5 epilogue
 #pragma unroll
@@ -204,64 +212,51 @@ spmm_subwarp(const SpmmParams p) {
     }
 }
 
-// ------------------------------------------------------------------ TMA ring (wide F)
-// One warp per CTA owns R <= 32 consecutive rows and a ring of STAGES B-row buffers in
-// shared memory.  The warp's sampled slots form one flat stream (row by row, slot order);
-// a producer cursor runs STAGES slots ahead of the consumer cursor, across row boundaries:
-// lane 0 issues one cp.async.bulk (a whole 16-B padded B row, ldb*4 bytes) per slot into
-// the stage the consumer just released, completion tracked by that stage's mbarrier
-// (expect_tx).  Bytes in flight are held by the TMA engine / smem, not registers, so
-// STAGES x (rows per SM) B rows are outstanding per SM.  Per-slot (col, val) come from a
-// chunk of 32 slots loaded coalesced by the whole warp, one chunk ahead.
-template <int NCH, int STAGES, int MINB>
-__global__ void __launch_bounds__(32, MINB)
-spmm_tma(const SpmmParams p, int R) {
-    extern __shared__ __align__(128) unsigned char smem_all[];
-    const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
-    const uint32_t row_bytes = (uint32_t)(p.ldb * 4);       // multiple of 16 (ldb % 4 == 0)
-    const int64_t row_floats = p.ldb;
-    // per-warp region: ring | mbarriers | staged val   (independent warps, no CTA barrier)
-    const size_t region = ((size_t)STAGES * row_bytes + STAGES * 12 + 127) & ~(size_t)127;
-    unsigned char* smem = smem_all + warp * region;
-    float* ring = reinterpret_cast<float*>(smem);
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (size_t)STAGES * row_bytes);
-    float* sval = reinterpret_cast<float*>(bar + STAGES);
-    const uint64_t pol_a = policy_evict_first();
-    const uint64_t pol_b = policy_evict_last();
-    const uint64_t pol_cold = policy_evict_first();
+// ------------------------------------------------------------------ per-warp slot stream
+// A warp owns R <= 32 consecutive rows; their sampled slots form one flat stream (row by
+// row, slot order).  Row i's metadata (a1) lives in lane i; (col, val) of 32 consecutive
+// slots (a2+a3) are loaded coalesced by the whole warp, one chunk ahead of use, so no row
+// or chunk boundary exposes a dependent-load latency.
+struct WarpStream {
+    RowSampler rs;      // lane i: row i of the warp
+    int32_t kk;         // lane i: k of row i (0 for lanes >= nr)
+    int64_t incl;       // lane i: flat end of row i (inclusive prefix of k)
+    int64_t T;          // total slots of the warp
+    int nr;
+    int32_t col_cur, col_nxt;
+    float a_cur, a_nxt;
+    int64_t chunk_cur;
+    int64_t tp;         // producer cursor
 
-    const int64_t r_begin = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * R;
-    if (r_begin >= p.n_rows) return;
-    const int nr = (int)min((int64_t)R, p.n_rows - r_begin);
-
-    // a1: per-row metadata, row i of this warp in lane i
-    RowSampler rs{};
-    int32_t kk = 0;
-    if (lane < nr) {
-        rs.init(ld_stream(p.rowptr + r_begin + lane, pol_a) - p.nnz_base,
-                ld_stream(p.rowptr + r_begin + lane + 1, pol_a) - p.nnz_base,
-                p.s, p.strategy, p.seed, p.row_base + r_begin + lane);
-        kk = rs.k;
-    }
-    int64_t incl = kk;
+    __device__ __forceinline__ void init(const SpmmParams& p, int64_t r_begin, int nrows, int lane,
+                                         uint64_t pol) {
+        nr = nrows;
+        rs = RowSampler{};
+        kk = 0;
+        if (lane < nr) {
+            rs.init(ld_stream(p.rowptr + r_begin + lane, pol) - p.nnz_base,
+                    ld_stream(p.rowptr + r_begin + lane + 1, pol) - p.nnz_base,
+                    p.s, p.strategy, p.seed, p.row_base + r_begin + lane);
+            kk = rs.k;
+        }
+        incl = kk;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int64_t v = __shfl_up_sync(kFull, incl, o);
-        if (lane >= o) incl += v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t v = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += v;
+        }
+        T = __shfl_sync(kFull, incl, 31);
+        chunk_cur = 0;
+        tp = 0;
+        load_chunk(p, 0, lane, col_cur, a_cur, pol);
+        load_chunk(p, 1, lane, col_nxt, a_nxt, pol);
     }
-    const int64_t pre = incl - kk;                             // first flat slot of row `lane`
-    const int64_t T = __shfl_sync(kFull, incl, 31);           // slots of this warp
 
-    if (lane == 0) {
-        for (int i = 0; i < STAGES; ++i) mbar_init(&bar[i], 1);
-        fence_mbar_init();
-    }
-    __syncwarp();
-
-    // a2+a3: (col, val) of flat slots [32c, 32c+32), lane l -> slot 32c + l
-    auto load_chunk = [&](int64_t c, int32_t& col, float& a, int& hot) {
+    // (col, val) of flat slot 32c + lane
+    __device__ __forceinline__ void load_chunk(const SpmmParams& p, int64_t c, int lane, int32_t& col,
+                                               float& a, uint64_t pol) const {
         const int64_t t = c * 32 + lane;
+        const int64_t pre = incl - kk;
         int row = 0;
         for (int i = 1; i < nr; ++i)
             if (__shfl_sync(kFull, pre, i) <= t) row = i;
@@ -277,41 +272,106 @@ spmm_tma(const SpmmParams p, int R) {
             if (p.strategy == kBucket) pos = j;
             else if (narrow) pos = (int64_t)(((uint32_t)off + (uint32_t)j * kPrime) % (uint32_t)d);
             else pos = (int64_t)((off + (uint64_t)j * kPrime) % (uint64_t)d);
-            col = ld_stream(p.colind + beg + pos, pol_a);
-            a = p.val ? ld_stream(p.val + beg + pos, pol_a) : 1.0f;
+            col = ld_stream(p.colind + beg + pos, pol);
+            a = p.val ? ld_stream(p.val + beg + pos, pol) : 1.0f;
         }
-        hot = 1;
-        if (p.hot_deg > 0 && t < T)        // popularity proxy: degree of the column node
-            hot = (__ldg(p.rowptr + col + 1) - __ldg(p.rowptr + col)) >= p.hot_deg;
-    };
+    }
 
-    int32_t col_cur, col_nxt;
-    float a_cur, a_nxt;
-    int hot_cur, hot_nxt;
-    int64_t chunk_cur = 0;
-    load_chunk(0, col_cur, a_cur, hot_cur);
-    load_chunk(1, col_nxt, a_nxt, hot_nxt);
-    int64_t tp = 0;                                            // producer cursor (flat slot)
-
-    auto issue = [&]() {                                       // warp-collective
-        if (tp >= T) return;
-        if ((tp >> 5) != chunk_cur) {                          // advance to the prefetched chunk
+    // Warp-collective: (col, val) of the next slot of the stream; false when exhausted.
+    __device__ __forceinline__ bool next(const SpmmParams& p, int lane, int32_t& col, float& a,
+                                         uint64_t pol) {
+        if (tp >= T) return false;
+        if ((tp >> 5) != chunk_cur) {
             col_cur = col_nxt;
             a_cur = a_nxt;
-            hot_cur = hot_nxt;
             ++chunk_cur;
-            load_chunk(chunk_cur + 1, col_nxt, a_nxt, hot_nxt);
+            load_chunk(p, chunk_cur + 1, lane, col_nxt, a_nxt, pol);
         }
-        const int32_t c = __shfl_sync(kFull, col_cur, (int)(tp & 31));
-        const float av = __shfl_sync(kFull, a_cur, (int)(tp & 31));
-        const int hv = __shfl_sync(kFull, hot_cur, (int)(tp & 31));
+        col = __shfl_sync(kFull, col_cur, (int)(tp & 31));
+        a = __shfl_sync(kFull, a_cur, (int)(tp & 31));
+        ++tp;
+        return true;
+    }
+};
+
+// Row accumulator of spmm_tma: slot j of a row FMAs into `part`; every 32 slots part is
+// added to `tot`.  spmm_warp uses the same order, so the two kernel
+// families are bitwise interchangeable (tests: same_as_first in scripts/tune.py).
+template <int NCH, int VEC>
+struct RowAcc {
+    float part[NCH][VEC], tot[NCH][VEC];
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+        for (int c = 0; c < NCH; ++c)
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) { part[c][q] = 0.0f; tot[c][q] = 0.0f; }
+    }
+    __device__ __forceinline__ void chunk_end() {
+#pragma unroll
+        for (int c = 0; c < NCH; ++c)
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) { tot[c][q] += part[c][q]; part[c][q] = 0.0f; }
+    }
+    __device__ __forceinline__ void store(const SpmmParams& p, int64_t row, int lane, int64_t NV,
+                                          int32_t k, uint64_t pol) {
+        float* Crow = p.C + row * p.ldc;
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+            const int64_t vidx = lane + 32 * c;
+            if (vidx < NV) {
+                float res[VEC];
+#pragma unroll
+                for (int q = 0; q < VEC; ++q) res[q] = finish(tot[c][q] + part[c][q], p.reduce, k);
+                store_out<VEC>(Crow, vidx, p.F, res, p.c_vec, pol);
+            }
+        }
+    }
+};
+
+// ------------------------------------------------------------------ TMA ring (wide F)
+// One warp per CTA (R rows) and a ring of STAGES B-row buffers in shared memory.  The
+// producer cursor of the warp's slot stream runs STAGES slots ahead of the consumer,
+// across row boundaries: lane 0 issues one cp.async.bulk (a whole 16-B padded B row,
+// ldb*4 bytes) per slot into the stage the consumer just released, completion tracked by
+// that stage's mbarrier (expect_tx).  Bytes in flight live in the TMA engine / smem, not in
+// registers (profiles/r01.md: 6.7 TB/s DRAM vs 2.4 TB/s for register-staged gathers).
+template <int NCH, int STAGES, int MINB>
+__global__ void __launch_bounds__(32, MINB)
+spmm_tma(const SpmmParams p, int R) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int lane = threadIdx.x & 31;
+    const uint32_t row_bytes = (uint32_t)(p.ldb * 4);       // multiple of 16 (ldb % 4 == 0)
+    const int64_t row_floats = p.ldb;
+    float* ring = reinterpret_cast<float*>(smem);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (size_t)STAGES * row_bytes);
+    float* sval = reinterpret_cast<float*>(bar + STAGES);
+    const uint64_t pol_a = policy_evict_first();
+    const uint64_t pol_b = policy_evict_last();
+
+    const int64_t r_begin = (int64_t)blockIdx.x * R;
+    if (r_begin >= p.n_rows) return;
+    const int nr = (int)min((int64_t)R, p.n_rows - r_begin);
+
+    WarpStream ws;
+    ws.init(p, r_begin, nr, lane, pol_a);
+
+    if (lane == 0) {
+        for (int i = 0; i < STAGES; ++i) mbar_init(&bar[i], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+
+    int64_t tp = 0;
+    auto issue = [&]() {                                       // warp-collective
+        int32_t c;
+        float a;
+        if (!ws.next(p, lane, c, a, pol_a)) return;
         if (lane == 0) {
             const int st = (int)(tp % STAGES);
-            sval[st] = av;
+            sval[st] = a;
             fence_proxy_async_smem();
             mbar_arrive_expect_tx(&bar[st], row_bytes);
-            bulk_g2s(ring + (size_t)st * row_floats, p.B + (int64_t)c * p.ldb, row_bytes, &bar[st],
-                     hv ? pol_b : pol_cold);
+            bulk_g2s(ring + (size_t)st * row_floats, p.B + (int64_t)c * p.ldb, row_bytes, &bar[st], pol_b);
         }
         ++tp;
     };
@@ -319,17 +379,13 @@ spmm_tma(const SpmmParams p, int R) {
 #pragma unroll 1
     for (int i = 0; i < STAGES; ++i) issue();
 
-    // a4 + a5: consume rows in order
     const int64_t NV = (p.F + 3) / 4;
     int64_t tc = 0;                                            // consumer cursor
+    RowAcc<NCH, 4> acc;
 #pragma unroll 1
     for (int i = 0; i < nr; ++i) {
-        const int32_t k = __shfl_sync(kFull, kk, i);
-        float part[NCH][4], tot[NCH][4];
-#pragma unroll
-        for (int c = 0; c < NCH; ++c)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) { part[c][q] = 0.0f; tot[c][q] = 0.0f; }
+        const int32_t k = __shfl_sync(kFull, ws.kk, i);
+        acc.zero();
 #pragma unroll 1
         for (int32_t j = 0; j < k; ++j, ++tc) {
             const int st = (int)(tc % STAGES);
@@ -341,32 +397,17 @@ spmm_tma(const SpmmParams p, int R) {
                 const int64_t vidx = lane + 32 * c;
                 if (vidx < NV) {
                     const float4 x = *reinterpret_cast<const float4*>(src + vidx * 4);
-                    part[c][0] = fmaf(av, x.x, part[c][0]);
-                    part[c][1] = fmaf(av, x.y, part[c][1]);
-                    part[c][2] = fmaf(av, x.z, part[c][2]);
-                    part[c][3] = fmaf(av, x.w, part[c][3]);
+                    acc.part[c][0] = fmaf(av, x.x, acc.part[c][0]);
+                    acc.part[c][1] = fmaf(av, x.y, acc.part[c][1]);
+                    acc.part[c][2] = fmaf(av, x.z, acc.part[c][2]);
+                    acc.part[c][3] = fmaf(av, x.w, acc.part[c][3]);
                 }
             }
-            if ((j & 31) == 31) {
-#pragma unroll
-                for (int c = 0; c < NCH; ++c)
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) { tot[c][q] += part[c][q]; part[c][q] = 0.0f; }
-            }
+            if ((j & 31) == 31) acc.chunk_end();
             __syncwarp();
             issue();                                           // refill the stage just released
         }
-        float* Crow = p.C + (r_begin + i) * p.ldc;
-#pragma unroll
-        for (int c = 0; c < NCH; ++c) {
-            const int64_t vidx = lane + 32 * c;
-            if (vidx < NV) {
-                float res[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) res[q] = finish(tot[c][q] + part[c][q], p.reduce, k);
-                store_out<4>(Crow, vidx, p.F, res, p.c_vec, pol_a);
-            }
-        }
+        acc.store(p, r_begin + i, lane, NV, k, pol_a);
     }
 }
 
@@ -406,9 +447,15 @@ sample_materialize(const int64_t* __restrict__ rowptr, int64_t nnz_base,
 namespace {
 
 template <int VEC, int NCH>
-cudaError_t launch_warp(const SpmmParams& p, cudaStream_t st) {
+cudaError_t launch_warp(const SpmmParams& p, const Plan& plan, cudaStream_t st) {
     constexpr int U = NCH == 1 ? 8 : (NCH == 2 ? 4 : 2);
     const int64_t blocks = (p.n_rows + kWarps - 1) / kWarps;
+    if constexpr (NCH == 1) {
+        if (plan.u == 16) {
+            spmm_warp<VEC, 1, 16><<<(unsigned)blocks, kThreads, 0, st>>>(p);
+            return cudaGetLastError();
+        }
+    }
     spmm_warp<VEC, NCH, U><<<(unsigned)blocks, kThreads, 0, st>>>(p);
     return cudaGetLastError();
 }
@@ -422,30 +469,23 @@ cudaError_t launch_subwarp(const SpmmParams& p, cudaStream_t st) {
 
 template <int NCH, int STAGES>
 cudaError_t launch_tma(const SpmmParams& p, const Plan& plan, cudaStream_t st) {
-    const size_t region = ((size_t)STAGES * (size_t)(p.ldb * 4) + STAGES * 12 + 127) & ~(size_t)127;
-    const int W = 1;
-    const size_t smem = region * W;
-    auto kern = plan.minb >= 32 ? spmm_tma<NCH, STAGES, 32>
-              : plan.minb >= 24 ? spmm_tma<NCH, STAGES, 24>
-              : plan.minb >= 16 ? spmm_tma<NCH, STAGES, 16> : spmm_tma<NCH, STAGES, 1>;
+    const size_t smem = (size_t)STAGES * (size_t)(p.ldb * 4) + STAGES * 12;
+    auto kern = plan.minb >= 24 ? spmm_tma<NCH, STAGES, 24> : spmm_tma<NCH, STAGES, 1>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
-    const int64_t rows_per_cta = (int64_t)plan.rows_per_warp * W;
-    const int64_t blocks = (p.n_rows + rows_per_cta - 1) / rows_per_cta;
-    kern<<<(unsigned)blocks, 32 * W, smem, st>>>(p, plan.rows_per_warp);
+    const int64_t blocks = (p.n_rows + plan.rows_per_warp - 1) / plan.rows_per_warp;
+    kern<<<(unsigned)blocks, 32, smem, st>>>(p, plan.rows_per_warp);
     return cudaGetLastError();
 }
 
 template <int NCH>
 cudaError_t dispatch_tma_stages(const SpmmParams& p, const Plan& plan, cudaStream_t st) {
     switch (plan.stages) {
-        case 2: return launch_tma<NCH, 2>(p, plan, st);
         case 3: return launch_tma<NCH, 3>(p, plan, st);
-        case 4: return launch_tma<NCH, 4>(p, plan, st);
-        case 6: return launch_tma<NCH, 6>(p, plan, st);
-        default: return launch_tma<NCH, 8>(p, plan, st);
+        case 8: return launch_tma<NCH, 8>(p, plan, st);
+        default: return launch_tma<NCH, 4>(p, plan, st);
     }
 }
 
@@ -473,14 +513,14 @@ cudaError_t dispatch_vec(const SpmmParams& p, const Plan& plan, cudaStream_t st)
         }
     }
     switch (plan.nch) {
-        case 1: return launch_warp<VEC, 1>(p, st);
-        case 2: return launch_warp<VEC, 2>(p, st);
-        case 3: return launch_warp<VEC, 3>(p, st);
-        case 4: return launch_warp<VEC, 4>(p, st);
-        case 5: return launch_warp<VEC, 5>(p, st);
-        case 6: return launch_warp<VEC, 6>(p, st);
-        case 7: return launch_warp<VEC, 7>(p, st);
-        default: return launch_warp<VEC, 8>(p, st);
+        case 1: return launch_warp<VEC, 1>(p, plan, st);
+        case 2: return launch_warp<VEC, 2>(p, plan, st);
+        case 3: return launch_warp<VEC, 3>(p, plan, st);
+        case 4: return launch_warp<VEC, 4>(p, plan, st);
+        case 5: return launch_warp<VEC, 5>(p, plan, st);
+        case 6: return launch_warp<VEC, 6>(p, plan, st);
+        case 7: return launch_warp<VEC, 7>(p, plan, st);
+        default: return launch_warp<VEC, 8>(p, plan, st);
     }
 }
 
@@ -518,9 +558,10 @@ Plan make_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C
         pl.nch = (int)(nch > 8 ? 8 : nch);
     }
     pl.c_vec = (c % (4u * (unsigned)pl.vec) == 0) && (ldc % pl.vec == 0);
+    pl.u = env_int("ES_SPMM_U", 8);
     // TMA ring: whole 16-B padded B rows as bulk copies; needs 16-B alignment and F <= 1024.
     const int64_t nv4 = (F + 3) / 4;
-    // Measured (profiles/tune_r01.md): TMA wins for wide rows (Reddit F=602: 9.5 vs 26.8 ms,
+    // Measured (profiles/r01.md): TMA wins for wide rows (Reddit F=602: 9.5 vs 26.8 ms,
     // F=256: 4.8 vs 8.2 ms); for 512-B rows (F=128) the LDG warp kernel wins (2.97 vs 4.3 ms).
     const int64_t kTmaMinRowBytes = env_int("ES_SPMM_TMA_MIN_BYTES", 1024);
     const bool tma_ok = pl.vec == 4 && nv4 > 32 && nv4 <= 32 * 8;
@@ -530,11 +571,10 @@ Plan make_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C
         pl.nch = (int)((nv4 + 31) / 32);
         pl.subwarp = false;
         int stages = env_int("ES_SPMM_STAGES", 0);
-        if (stages != 2 && stages != 3 && stages != 4 && stages != 6 && stages != 8) stages = 4;
+        if (stages != 3 && stages != 8) stages = 4;
         pl.stages = stages;
         const int rpw = env_int("ES_SPMM_ROWS_PER_WARP", 0);
         pl.rows_per_warp = (rpw >= 1 && rpw <= 32) ? rpw : 1;
-        pl.warps_per_cta = 1;
         pl.minb = env_int("ES_SPMM_MINB", 1);
     }
     return pl;
@@ -543,8 +583,6 @@ Plan make_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C
 cudaError_t launch_spmm(SpmmParams p, const Plan& plan, cudaStream_t st) {
     if (p.n_rows <= 0) return cudaSuccess;
     p.c_vec = plan.c_vec ? 1 : 0;
-    p.hot_deg = plan.tma ? env_int("ES_SPMM_HOT_DEG", 0) : 0;   // experiment (full-graph launches only)
-    if (p.hot_deg > 0 && (p.row_base != 0 || p.nnz_base != 0)) p.hot_deg = 0;
     if (plan.tma) return dispatch_tma(p, plan, st);
     switch (plan.vec) {
         case 4: return dispatch_vec<4>(p, plan, st);

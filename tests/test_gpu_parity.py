@@ -95,13 +95,14 @@ FS = [(1, 1), (3, 3), (3, 4), (7, 8), (16, 16), (17, 17), (32, 32), (64, 64), (1
       (128, 128), (129, 132), (256, 256), (602, 602), (602, 604), (1000, 1000), (1100, 1104)]
 
 
-@pytest.fixture(params=["auto", "warp"])
+@pytest.fixture(params=["auto", "warp", "tma"])
 def kernel(request, monkeypatch):
-    """Run a test under the automatic plan (TMA ring for wide F) and the LDG warp kernel."""
-    if request.param == "warp":
-        monkeypatch.setenv("ES_SPMM_KERNEL", "warp")
-    else:
+    """Run a test under the automatic plan and with each kernel family forced where it
+    applies (TMA ring, LDG warp-per-row, LDG register-ring stream)."""
+    if request.param == "auto":
         monkeypatch.delenv("ES_SPMM_KERNEL", raising=False)
+    else:
+        monkeypatch.setenv("ES_SPMM_KERNEL", request.param)
     return request.param
 
 

@@ -71,6 +71,7 @@ def test_host_validation_rejects_bad_arguments(lib):
 
 def test_plan_selection(lib, monkeypatch):
     assert es.es_spmm_plan(128, 128, 128).startswith("es::spmm_warp<vec4,nch1>")   # 512-B rows
+    assert es.es_spmm_plan(200, 200, 200).startswith("es::spmm_warp<vec4,nch2>")
     assert es.es_spmm_plan(256, 256, 256).startswith("es::spmm_tma<nch2,stages4>")
     assert es.es_spmm_plan(602, 604, 604).startswith("es::spmm_tma<nch5,stages4>")
     monkeypatch.setenv("ES_SPMM_KERNEL", "warp")
@@ -78,6 +79,9 @@ def test_plan_selection(lib, monkeypatch):
     assert "vec4,nch5" in es.es_spmm_plan(602, 604, 604)
     monkeypatch.delenv("ES_SPMM_KERNEL")
     assert "spmm_warp<vec2" in es.es_spmm_plan(602, 602, 602)      # 8-B rows: no TMA
+    monkeypatch.setenv("ES_SPMM_KERNEL", "tma")
+    assert es.es_spmm_plan(200, 200, 200).startswith("es::spmm_tma<nch2")
+    monkeypatch.delenv("ES_SPMM_KERNEL")
     assert "subwarp<vec4,g4>" in es.es_spmm_plan(16, 16, 16)
     assert "subwarp<vec1,g1>" in es.es_spmm_plan(1, 1, 1)
     assert "spmm_warp<vec4,nch8>" in es.es_spmm_plan(5000, 5000, 5000)   # feature-tiled
