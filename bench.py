@@ -197,10 +197,16 @@ def main():
     import paper_2104_10716_b200 as es
 
     es.load_library()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # one process per GPU; ES_BENCH_BACKEND=gloo lets a 1-GPU box exercise the multi-rank
+    # flow (ranks then share cuda:0 -- validation only, never a reported scaling number)
+    backend = os.environ.get("ES_BENCH_BACKEND", "nccl")
+    dev = torch.device("cuda", local % torch.cuda.device_count())
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     # ---------------- inputs (seeded, synthetic)
     rowptr, colind = synth.graph(a.config)
@@ -262,7 +268,7 @@ def main():
     t_rank = float(per_step.sum())
     t_max = t_rank
     if world > 1:
-        tt = torch.tensor([t_rank], dtype=torch.float64, device=dev)
+        tt = torch.tensor([t_rank], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_max = float(tt.item())
     ms_per_step = 1e3 * t_max / a.steps
@@ -296,7 +302,7 @@ def main():
     e2e = None
     if not a.no_e2e:
         e2e = run_e2e(a, es, torch, dev, stream, rowptr, colind, val, B, r0, r1, e0, e1, F, ldb,
-                      strat_id, red_id, flops_all, world, dist)
+                      strat_id, red_id, flops_all, world, dist, backend)
 
     # ---------------- CPU baseline: the oracle as it stands, rank 0 at N=1 only
     cpu = None
@@ -321,7 +327,8 @@ def main():
                        "sampling_rate": round(K_all / nnz, 4), "F": F, "ldb": ldb, "s": a.s,
                        "strategy": a.strategy, "reduce": a.reduce, "seed": a.seed,
                        "l2": "no flush (warm)" if a.no_flush else "flushed between timed steps (256 MiB write)",
-                       "parallelism": f"row-partitioned x{world} (sampled-byte balanced), B replicated",
+                       "parallelism": f"row-partitioned x{world} (sampled-byte balanced), B replicated"
+                                      + ("" if backend == "nccl" else f" [{backend} validation run]"),
                        "timing": "sum of per-step CUDA-event times on the launch stream, max over ranks"},
             "roofline": roofline,
             "cpu_baseline": cpu,
@@ -342,7 +349,7 @@ def main():
 
 
 def run_e2e(a, es, torch, dev, stream, rowptr, colind, val, B, r0, r1, e0, e1, F, ldb, strat_id, red_id,
-            flops_all, world, dist):
+            flops_all, world, dist, backend):
     """Same metric through es_spmm_run_host: every step copies this rank's CSR slice and the
     replicated B from pinned host memory and reads C back (inside the timed region)."""
     rp_h = torch.from_numpy(rowptr[r0:r1 + 1].copy()).pin_memory()
@@ -372,7 +379,7 @@ def run_e2e(a, es, torch, dev, stream, rowptr, colind, val, B, r0, r1, e0, e1, F
     torch.cuda.synchronize(dev)
     t = ev0.elapsed_time(ev1) / 1e3
     if world > 1:
-        tt = torch.tensor([t], dtype=torch.float64, device=dev)
+        tt = torch.tensor([t], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t = float(tt.item())
     h2d = (rp_h.numel() * 8 + ci_h.numel() * 4 + va_h.numel() * 4 + B_h.numel() * 4)

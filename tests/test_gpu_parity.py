@@ -264,9 +264,16 @@ def _full(name, F, ldb, s, strat, seed, reduce, n_check=1500):
     o = oracle.spmm(rowptr, colind, val, B, s, strat, seed=seed, reduce=reduce, F=F, rows=rows)
     ok, msg = rel_ok(g, o)
     assert ok, (name, msg)
-    # sampled counts for all rows: B == 1 trick is too big here; check the sampler instead
-    srp, _, _, _ = es.es_spmm_sample(rp, ci, v, s, strat, seed, want_pos=False)
-    assert np.array_equal(np.diff(srp.cpu().numpy()), np.minimum(d, s))
+    # sampler at full size: k_i of every row, and the bit-exact slot positions / columns of the
+    # checked rows against the brute-force Eq. 2 positions
+    srp, sc, _, spos = es.es_spmm_sample(rp, ci, v, s, strat, seed, want_pos=True)
+    srp = srp.cpu().numpy()
+    assert np.array_equal(np.diff(srp), np.minimum(d, s))
+    for r in rows[:400]:
+        a, b = int(srp[r]), int(srp[r + 1])
+        want = oracle.brute.positions(strat, int(d[r]), s, seed, int(r))
+        assert spos[a:b].cpu().tolist() == want
+        assert np.array_equal(sc[a:b].cpu().numpy(), colind[rowptr[r] + np.asarray(want, np.int64)])
     return msg
 
 
@@ -294,3 +301,10 @@ def test_full_proteins():
 @pytest.mark.parametrize("strat", STRATS)
 def test_full_reddit(F, ldb, strat, kernel):
     _full("reddit", F, ldb, 256, strat, 0, ES_REDUCE_MEAN)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("strat", [ES_FASTRAND])
+def test_full_scaled(strat):
+    """Config 5: 10M nodes, 1.0B edges, F=256, s=128 (bench launch configuration, 1 GPU)."""
+    _full("scaled", 256, 256, 128, strat, 0, ES_REDUCE_SUM, n_check=1000)
