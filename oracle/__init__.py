@@ -8,7 +8,8 @@ Two independent implementations live here:
 
 * ``es_oracle.c`` (loaded through ctypes): the sampled SpMM of Alg. 1
   with Bucket (L1042-1047) and FastRand Eq. 2 (L1064-1067, P'=577 L1058), fp64
-  accumulation in slot order rounded once to fp32, mean by k_i (L1570-1575, reading R5).
+  accumulation in slot order rounded once to fp32, mean by k_i (L1570-1575, reading R5);
+  and its backward w.r.t. B, dB = A_s^T dC over the same slots (NEXT-2, §6.2).
 * ``brute``: a pure-Python/numpy brute force for tiny graphs -- builds the dense
   sampled adjacency A_s (fp64) slot by slot with Python integers and multiplies it by B.
 
@@ -59,6 +60,9 @@ def _L():
         lib.oracle_spmm.restype = ctypes.c_int
         lib.oracle_spmm.argtypes = [i64, vp, vp, vp, vp, i64, i64, i64, i32, u64, i32, i64,
                                     vp, i64, vp, i64]
+        lib.oracle_spmm_backward.restype = ctypes.c_int
+        lib.oracle_spmm_backward.argtypes = [i64, vp, vp, vp, vp, i64, i64, i64, i32, u64, i32, i64,
+                                             i64, vp, i64]
         lib.oracle_max_threads.restype = ctypes.c_int
         lib.oracle_max_threads.argtypes = []
         _lib = lib
@@ -137,6 +141,24 @@ def spmm(rowptr, colind, val, B, s: int, strategy: int, seed: int = 0, reduce: i
     if rc != 0:
         raise MemoryError("oracle_spmm: allocation failed")
     return C
+
+
+def spmm_backward(rowptr, colind, val, dC, n_cols: int, s: int, strategy: int, seed: int = 0,
+                  reduce: int = SUM, F: int | None = None, row_base: int = 0) -> np.ndarray:
+    """dB = A_s^T dC over the forward's sampled slots (MEAN: rows of A_s scaled by 1/k_i);
+    returns a fresh (n_cols, F) fp32 array."""
+    rowptr, colind, val = _csr(rowptr, colind, val)
+    dC = np.ascontiguousarray(dC, dtype=np.float32)
+    F = dC.shape[1] if F is None else F
+    dB = np.zeros((n_cols, F), dtype=np.float32)
+    if n_cols == 0 or F == 0:
+        return dB
+    rc = _L().oracle_spmm_backward(len(rowptr) - 1, rowptr.ctypes.data, colind.ctypes.data, _p(val),
+                                   dC.ctypes.data, F, dC.shape[1], s, strategy, seed & (2**64 - 1),
+                                   reduce, row_base, n_cols, dB.ctypes.data, F)
+    if rc != 0:
+        raise MemoryError("oracle_spmm_backward: allocation failed")
+    return dB
 
 
 def max_threads() -> int:

@@ -59,3 +59,12 @@ def spmm(rowptr, colind, val, B, s: int, strategy: int, seed: int = 0, reduce: i
         kk = np.maximum(k, 1).astype(np.float32)[:, None]
         C = np.where(k[:, None] > 0, C / kk, np.float32(0.0)).astype(np.float32)
     return C
+
+
+def spmm_backward(rowptr, colind, val, dC, n_cols: int, s: int, strategy: int, seed: int = 0,
+                  reduce: int = SUM):
+    """dB = A_s^T dC with the dense sampled matrix (rows scaled by 1/k_i for MEAN), fp64."""
+    A, k = sampled_dense(rowptr, colind, val, n_cols, s, strategy, seed)
+    if reduce == MEAN:
+        A = A / np.maximum(k, 1)[:, None]
+    return (A.T @ np.asarray(dC, dtype=np.float64)).astype(np.float32)

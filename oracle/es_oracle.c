@@ -154,6 +154,38 @@ int oracle_spmm(int64_t n_rows, const int64_t* rowptr, const int32_t* colind, co
     return bad ? -1 : 0;
 }
 
+/* Backward of the sampled SpMM w.r.t. B -- the training variant the paper leaves to future
+ * work (§6.2: dynamic sampling "could accelerate GNN training").
+ * Over the SAME sampled slots as the forward (Alg. 1 positions, Eq. 2, R6 rotation):
+ *   dB[col_ij, c] += w_ij * dC[i, c],   w_ij = val[e_ij] (SUM)  or  val[e_ij] / k_i (MEAN)
+ * i.e. dB = A_s^T dC with A_s the (row-scaled for MEAN) sampled matrix.  Rows in order,
+ * slots in order, fp64 accumulation, rounded once to fp32 and ADDED to dB (n_cols x ldb).
+ * Single-threaded on purpose (one obvious summation order).  Returns -1 on OOM. */
+int oracle_spmm_backward(int64_t n_rows, const int64_t* rowptr, const int32_t* colind,
+                         const float* val, const float* dC, int64_t F, int64_t ldc, int64_t s,
+                         int32_t strategy, uint64_t seed, int32_t reduce, int64_t row_base,
+                         int64_t n_cols, float* dB, int64_t ldb) {
+    double* acc = (double*)calloc((size_t)(n_cols > 0 ? n_cols : 1) * (size_t)(F > 0 ? F : 1),
+                                  sizeof(double));
+    if (!acc) return -1;
+    for (int64_t i = 0; i < n_rows; ++i) {
+        int64_t d = rowptr[i + 1] - rowptr[i];
+        int64_t k = oracle_k(d, s);
+        int64_t off = strategy == ORACLE_FASTRAND ? oracle_offset(seed, row_base + i, d) : 0;
+        for (int64_t j = 0; j < k; ++j) {
+            int64_t e = rowptr[i] + oracle_position(strategy, j, d, off);
+            double w = val ? (double)val[e] : 1.0;
+            if (reduce == ORACLE_MEAN) w /= (double)k;
+            double* row = acc + (int64_t)colind[e] * F;
+            for (int64_t c = 0; c < F; ++c) row[c] += w * (double)dC[i * ldc + c];
+        }
+    }
+    for (int64_t r = 0; r < n_cols; ++r)
+        for (int64_t c = 0; c < F; ++c) dB[r * ldb + c] += (float)acc[r * F + c];
+    free(acc);
+    return 0;
+}
+
 int oracle_max_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

@@ -3,7 +3,8 @@
 Each test names what it pins and why a plausible oracle bug (dropped term, wrong
 sign/index, transposed operand, wrong divisor, wrong row id in the seeded offset)
 would fail it.  Oracle functions pinned here: mix64/offset, position, rate, sample,
-spmm (SUM/MEAN, Bucket/FastRand, seeded, row subsets, row_base) and brute.
+spmm (SUM/MEAN, Bucket/FastRand, seeded, row subsets, row_base), spmm_backward (adjoint
+identity, dense brute force, column-hit counts) and brute.
 """
 import math
 
@@ -302,3 +303,41 @@ def test_empty_inputs():
     assert C.shape == (0, 3)
     C = oracle.spmm(np.zeros(4, np.int64), np.zeros(0, np.int32), None, B, 4, FASTRAND, reduce=MEAN)
     assert C.shape == (3, 3) and np.all(C == 0)
+
+
+# ----------------------------------------------------------------- backward (NEXT-2)
+@pytest.mark.parametrize("strat", [BUCKET, FASTRAND])
+@pytest.mark.parametrize("reduce", [SUM, MEAN])
+def test_backward_adjoint_identity(strat, reduce):
+    """<A_s B, dC> = <B, A_s^T dC>: the backward is the adjoint of the forward over the same
+    sampled slots (a wrong index, a transposed operand or a missing 1/k breaks it)."""
+    rowptr, colind, val = synth.random_csr(250, 400, seed=8, max_deg=120, special=(577, 1154 // 3))
+    B = synth.dense(400, 11, seed=2)
+    dC = synth.dense(250, 11, seed=3)
+    C = oracle.spmm(rowptr, colind, val, B, 24, strat, seed=5, reduce=reduce)
+    dB = oracle.spmm_backward(rowptr, colind, val, dC, 400, 24, strat, seed=5, reduce=reduce)
+    lhs = float(np.sum(C.astype(np.float64) * dC))
+    rhs = float(np.sum(B.astype(np.float64) * dB))
+    assert abs(lhs - rhs) <= 1e-6 * abs(lhs)
+
+
+@pytest.mark.parametrize("strat", [BUCKET, FASTRAND])
+@pytest.mark.parametrize("reduce", [SUM, MEAN])
+def test_backward_against_dense_brute_force(strat, reduce):
+    rowptr, colind, val = synth.random_csr(70, 1300, seed=12, max_deg=40, special=(577, 1154, 600))
+    dC = synth.dense(70, 6, seed=4)
+    for s in (1, 5, 40, 2000):
+        want = oracle.brute.spmm_backward(rowptr, colind, val, dC, 1300, s, strat, 7, reduce)
+        got = oracle.spmm_backward(rowptr, colind, val, dC, 1300, s, strat, seed=7, reduce=reduce)
+        assert _ulp_close(got, want, ulps=2)
+
+
+def test_backward_ones_count_column_hits():
+    """dC == 1, val == 1, SUM: dB[c, :] = number of sampled slots pointing at column c."""
+    rowptr, colind, _ = synth.random_csr(300, 500, seed=1, max_deg=300, special=(577, 1154))
+    for s in (1, 10, 1000):
+        srp, sc, _, _ = oracle.sample(rowptr, colind, None, s, FASTRAND, seed=2)
+        dB = oracle.spmm_backward(rowptr, colind, None, np.ones((300, 3), np.float32), 500, s,
+                                  FASTRAND, seed=2)
+        hits = np.bincount(sc, minlength=500).astype(np.float32)
+        assert np.array_equal(dB, np.repeat(hits[:, None], 3, 1))
