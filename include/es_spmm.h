@@ -109,6 +109,23 @@ es_status_t es_spmm_run_rows(int64_t n_rows, int64_t n_cols,
                              float* C /*[dev]*/, int64_t ldc,
                              int64_t row_begin, int64_t row_end, void* stream);
 
+/* Backward w.r.t. B of es_spmm_run_rows (training variant; the paper leaves training with
+ * dynamic sampling to future work, §6.2):
+ *   dB[col_ij, 0:F] += w_ij * dC[i, 0:F]  over the SAME sampled slots (same s, strategy, seed),
+ *   w_ij = val[e_ij] (SUM) or val[e_ij] / k_i (MEAN), i.e. dB += A_s^T dC.
+ * Arguments as es_spmm_run_rows; dC [dev] points at row row_begin's gradient (rows x ldc, the
+ * allocation holds rows*ldc floats), dB [dev] is the full n_cols x ldb gradient, ACCUMULATED
+ * into (the caller zeroes it; several row blocks / ranks may add into one dB).  Uses fp32
+ * vector reductions (red.global.add.v4.f32): the order of additions across rows is not
+ * deterministic; per-element error <= (n_c + 1) u sum|terms| for n_c contributions. */
+es_status_t es_spmm_backward(int64_t n_rows, int64_t n_cols,
+                             const int64_t* rowptr /*[dev]*/, int64_t nnz_base,
+                             const int32_t* colind /*[dev]*/, const float* val /*[dev] or NULL*/,
+                             const float* dC /*[dev]*/, int64_t F, int64_t ldc,
+                             int32_t s, int32_t strategy, uint64_t seed, int32_t reduce,
+                             float* dB /*[dev] n_cols x ldb*/, int64_t ldb,
+                             int64_t row_begin, int64_t row_end, void* stream);
+
 /* End-to-end variant with HOST inputs and output (the call a user with host data makes):
  * copies rowptr/colind/val/B host->device, runs the fused kernel and copies C back,
  * rowptr entries are absolute offsets with colind[0] holding nonzero rowptr[0];

@@ -19,7 +19,8 @@ ES_REDUCE_SUM, ES_REDUCE_MEAN = 0, 1
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libesspmm.so")
-EXPORTS = ("es_spmm_sample", "es_spmm_run", "es_spmm_run_rows", "es_spmm_host_workspace_bytes",
+EXPORTS = ("es_spmm_sample", "es_spmm_run", "es_spmm_run_rows", "es_spmm_backward",
+           "es_spmm_host_workspace_bytes",
            "es_spmm_run_host", "es_partition_rows", "es_spmm_plan", "es_launch_count",
            "es_status_string")
 
@@ -51,6 +52,9 @@ def load_library(path: str = LIB_PATH):
     lib.es_spmm_run_rows.restype = st
     lib.es_spmm_run_rows.argtypes = [i64, i64, vp, i64, vp, vp, vp, i64, i64, i32, i32, u64, i32, vp,
                                      i64, i64, i64, vp]
+    lib.es_spmm_backward.restype = st
+    lib.es_spmm_backward.argtypes = [i64, i64, vp, i64, vp, vp, vp, i64, i64, i32, i32, u64, i32, vp, i64,
+                                     i64, i64, vp]
     lib.es_spmm_host_workspace_bytes.restype = i64
     lib.es_spmm_host_workspace_bytes.argtypes = [i64, i64, i64, i64, i64, i32]
     lib.es_spmm_run_host.restype = st
@@ -178,6 +182,33 @@ def es_spmm_run_rows(n_rows: int, rowptr_slice, nnz_base: int, colind_slice, val
                                            strategy, seed & (2**64 - 1), reduce, _ptr(C), C.stride(0),
                                            row_begin, row_end, _stream(stream)), "es_spmm_run_rows")
     return C
+
+
+def es_spmm_backward(rowptr, colind, val, dC, n_cols: int, s: int, strategy: int, seed: int = 0,
+                     reduce: int = ES_REDUCE_SUM, F: int | None = None, dB=None, ldb: int | None = None,
+                     row_begin: int = 0, row_end: int | None = None, n_rows: int | None = None,
+                     nnz_base: int = 0, stream=None):
+    """dB += A_s^T dC over the forward's sampled slots (same s, strategy, seed).  Defaults: the
+    full CSR (rowptr has n_rows+1 entries); for a row block pass the slice like es_spmm_run_rows.
+    Returns dB (allocated zeroed as (n_cols, ldb) if not given)."""
+    import torch
+    _dev(rowptr, torch.int64, "rowptr")
+    _dev(colind, torch.int32, "colind")
+    _dev(val, torch.float32, "val")
+    if dC.dim() != 2 or dC.stride(1) != 1 or not dC.is_cuda or dC.dtype != torch.float32:
+        raise EsError("dC must be a row-major fp32 CUDA matrix")
+    F = dC.shape[1] if F is None else F
+    if row_end is None:
+        row_end = row_begin + rowptr.numel() - 1
+    if n_rows is None:
+        n_rows = row_end
+    if dB is None:
+        dB = torch.zeros((n_cols, F if ldb is None else ldb), dtype=torch.float32, device=dC.device)
+    _check(load_library().es_spmm_backward(n_rows, n_cols, _ptr(rowptr), nnz_base, _ptr(colind), _ptr(val),
+                                           _ptr(dC), F, dC.stride(0), s, strategy, seed & (2**64 - 1), reduce,
+                                           _ptr(dB), dB.stride(0), row_begin, row_end, _stream(stream)),
+           "es_spmm_backward")
+    return dB
 
 
 def es_spmm_host_workspace_bytes(n_rows, n_cols, nnz, F, ldb, has_val) -> int:

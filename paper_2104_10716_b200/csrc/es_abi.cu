@@ -126,6 +126,41 @@ es_status_t es_spmm_run_rows(int64_t n_rows, int64_t n_cols, const int64_t* rowp
                          reduce, C, ldc, row_begin, row_end, as_stream(stream));
 }
 
+es_status_t es_spmm_backward(int64_t n_rows, int64_t n_cols, const int64_t* rowptr, int64_t nnz_base,
+                             const int32_t* colind, const float* val, const float* dC, int64_t F,
+                             int64_t ldc, int32_t s, int32_t strategy, uint64_t seed, int32_t reduce,
+                             float* dB, int64_t ldb, int64_t row_begin, int64_t row_end, void* stream) {
+    es_status_t rc = check_common(n_rows, n_cols, F, ldb, ldc, s, strategy, reduce);
+    if (rc != ES_OK) return rc;
+    if (row_begin < 0 || row_end < row_begin || row_end > n_rows) return ES_ERR_INVALID_VALUE;
+    const int64_t n = row_end - row_begin;
+    if (n == 0) return ES_OK;
+    if (!rowptr || !dC || (n_cols > 0 && !dB)) return ES_ERR_INVALID_VALUE;
+    es::BwdParams p{};
+    p.rowptr = rowptr;
+    p.nnz_base = nnz_base;
+    p.colind = colind;
+    p.val = val;
+    p.dC = dC;
+    p.F = F;
+    p.ldc = ldc;
+    p.s = s;
+    p.strategy = strategy;
+    p.seed = seed;
+    p.reduce = reduce;
+    p.dB = dB;
+    p.ldb = ldb;
+    p.n_rows = n;
+    p.row_base = row_begin;
+    const uintptr_t a = reinterpret_cast<uintptr_t>(dC), b = reinterpret_cast<uintptr_t>(dB);
+    if (a % 16 == 0 && b % 16 == 0 && ldc % 4 == 0 && ldb % 4 == 0) p.vec = 4;
+    else if (a % 8 == 0 && b % 8 == 0 && ldc % 2 == 0 && ldb % 2 == 0) p.vec = 2;
+    else p.vec = 1;
+    cudaError_t err = es::launch_backward(p, as_stream(stream));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return err == cudaSuccess ? ES_OK : ES_ERR_CUDA;
+}
+
 es_status_t es_partition_rows(const int64_t* rowptr_host, int64_t n_rows, int32_t s, int64_t F,
                               int32_t n_parts, int64_t* bounds_host) {
     if (!rowptr_host || !bounds_host || n_rows < 0 || s < 1 || F < 1 || n_parts < 1)

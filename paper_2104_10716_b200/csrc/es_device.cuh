@@ -117,6 +117,18 @@ __device__ __forceinline__ void st_stream2(float* p, const float* a, uint64_t po
                  :: "l"(p), "f"(a[0]), "f"(a[1]), "l"(pol) : "memory");
 }
 
+// Vector reductions into global memory (SASS REDG.E.ADD.F32x4): relaxed, gpu scope.  Note the
+// hardware add flushes fp32 denormals to zero (FTZ), unlike the FMA path.
+__device__ __forceinline__ void red_add4(float* p, float a, float b, float c, float d) {
+    asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1,%2,%3,%4};"
+                 :: "l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+__device__ __forceinline__ void red_add2(float* p, float a, float b) {
+    asm volatile("red.relaxed.gpu.global.add.v2.f32 [%0], {%1,%2};" :: "l"(p), "f"(a), "f"(b) : "memory");
+}
+__device__ __forceinline__ void red_add1(float* p, float a) {
+    asm volatile("red.relaxed.gpu.global.add.f32 [%0], %1;" :: "l"(p), "f"(a) : "memory");
+}
 
 // ---- mbarrier + TMA bulk copy (cp.async.bulk, SASS UBLKCP) helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

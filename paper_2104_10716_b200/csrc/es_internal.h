@@ -35,6 +35,25 @@ struct Plan {
     int u;              // slots in flight per lane (warp kernel, NCH == 1: 8 or 16)
 };
 
+// Backward w.r.t. B: dB[col_ij] += w_ij * dC[i]  (w = val, or val / k_i for MEAN)
+struct BwdParams {
+    const int64_t* rowptr;   // local row r uses rowptr[r], rowptr[r+1] (absolute offsets)
+    int64_t nnz_base;
+    const int32_t* colind;
+    const float* val;
+    const float* dC;         // row r of this launch at dC + r*ldc
+    int64_t F, ldc;
+    int32_t s, strategy;
+    uint64_t seed;
+    int32_t reduce;
+    float* dB;               // n_cols x ldb, accumulated
+    int64_t ldb;
+    int64_t n_rows, row_base;
+    int32_t vec;             // 4, 2, 1 (alignment of dC, dB, ldc, ldb)
+};
+
+cudaError_t launch_backward(const BwdParams& p, cudaStream_t st);
+
 Plan make_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C);
 cudaError_t launch_spmm(SpmmParams p, const Plan& plan, cudaStream_t st);
 cudaError_t launch_sample_count(const int64_t* rowptr, int64_t n, int32_t s, int64_t* s_rowptr,

@@ -411,6 +411,93 @@ spmm_tma(const SpmmParams p, int R) {
     }
 }
 
+// ------------------------------------------------------------------ backward w.r.t. B (NEXT-2)
+// The training variant (§6.2, future work there): over the SAME sampled
+// slots as the forward, dB[col_ij, :] += w_ij * dC[i, :] with w = val (SUM) or val/k_i (MEAN).
+// One warp per row: the dC row is read once into registers (MEAN: divided by k_i with IEEE
+// division), then every sampled slot scatters w * dC_row into its B row with 128-bit vector
+// reductions (red.global.add.v4.f32).  Summation order across rows is not deterministic.
+template <int VEC, int NCH>
+__global__ void __launch_bounds__(kThreads)
+spmm_bwd_warp(const BwdParams p) {
+    const int lane = threadIdx.x & 31;
+    const int64_t r = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+    if (r >= p.n_rows) return;
+    const uint64_t pol_a = policy_evict_first();
+    RowSampler rs;
+    rs.init(ld_stream(p.rowptr + r, pol_a) - p.nnz_base, ld_stream(p.rowptr + r + 1, pol_a) - p.nnz_base,
+            p.s, p.strategy, p.seed, p.row_base + r);
+    if (rs.k == 0) return;
+    const int64_t NV = (p.F + VEC - 1) / VEC;
+    const float* dCrow = p.dC + r * p.ldc;
+    for (int64_t v0 = 0; v0 < NV; v0 += 32 * NCH) {
+        float x[NCH][VEC];
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+            const int64_t vidx = v0 + lane + 32 * c;
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) {
+                const int64_t col = vidx * VEC + q;
+                float v = (vidx < NV && col < p.F) ? ld_stream(dCrow + col, pol_a) : 0.0f;
+                x[c][q] = p.reduce == kMean ? __fdiv_rn(v, (float)rs.k) : v;
+            }
+        }
+        for (int32_t j0 = 0; j0 < rs.k; j0 += 32) {
+            int32_t colj = 0;
+            float a = 0.0f;
+            if (j0 + lane < rs.k) {
+                const int64_t e = rs.beg + rs.pos(j0 + lane);
+                colj = ld_stream(p.colind + e, pol_a);
+                a = p.val ? ld_stream(p.val + e, pol_a) : 1.0f;
+            }
+            const int n_here = min(32, rs.k - j0);
+            for (int t = 0; t < n_here; ++t) {
+                const int32_t cu = __shfl_sync(kFull, colj, t);
+                const float av = __shfl_sync(kFull, a, t);
+                float* brow = p.dB + (int64_t)cu * p.ldb;
+#pragma unroll
+                for (int c = 0; c < NCH; ++c) {
+                    const int64_t vidx = v0 + lane + 32 * c;
+                    if (vidx >= NV) continue;
+                    const int64_t c0 = vidx * VEC;
+                    if (c0 + VEC <= p.F) {
+                        if constexpr (VEC == 4) red_add4(brow + c0, av * x[c][0], av * x[c][1], av * x[c][2], av * x[c][3]);
+                        else if constexpr (VEC == 2) red_add2(brow + c0, av * x[c][0], av * x[c][1]);
+                        else red_add1(brow + c0, av * x[c][0]);
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < VEC; ++q)
+                            if (c0 + q < p.F) red_add1(brow + c0 + q, av * x[c][q]);
+                    }
+                }
+            }
+        }
+    }
+}
+
+namespace {
+template <int VEC>
+cudaError_t launch_bwd_vec(const BwdParams& p, cudaStream_t st) {
+    const int64_t NV = (p.F + VEC - 1) / VEC;
+    const int64_t nch = (NV + 31) / 32;
+    const int64_t blocks = (p.n_rows + kWarps - 1) / kWarps;
+    if (nch <= 1) spmm_bwd_warp<VEC, 1><<<(unsigned)blocks, kThreads, 0, st>>>(p);
+    else if (nch <= 2) spmm_bwd_warp<VEC, 2><<<(unsigned)blocks, kThreads, 0, st>>>(p);
+    else if (nch <= 4) spmm_bwd_warp<VEC, 4><<<(unsigned)blocks, kThreads, 0, st>>>(p);
+    else spmm_bwd_warp<VEC, 8><<<(unsigned)blocks, kThreads, 0, st>>>(p);
+    return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t launch_backward(const BwdParams& p, cudaStream_t st) {
+    if (p.n_rows <= 0) return cudaSuccess;
+    switch (p.vec) {
+        case 4: return launch_bwd_vec<4>(p, st);
+        case 2: return launch_bwd_vec<2>(p, st);
+        default: return launch_bwd_vec<1>(p, st);
+    }
+}
+
 // ------------------------------------------------------------------ sampler (es_spmm_sample)
 __global__ void sample_count(const int64_t* __restrict__ rowptr, int64_t n, int32_t s,
                              int64_t* __restrict__ s_rowptr) {

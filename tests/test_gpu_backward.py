@@ -1,0 +1,104 @@
+"""GPU parity of the backward w.r.t. B (NEXT-2) against the oracle.
+
+The GPU adds contributions with fp32 vector reductions in nondeterministic order, so the bar is
+the order-independent bound |g - o| <= (n_c + 2) u sum|terms| (n_c = contributions to that
+element, u = 2^-24), computed from the oracle on |val|, |dC|; integer-valued cases are exact."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2104_10716_b200 as es  # noqa: E402
+from paper_2104_10716_b200.autograd import sampled_spmm  # noqa: E402
+
+DEV = "cuda:0"
+U = 2.0 ** -24
+
+
+def t(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+@pytest.fixture(scope="module")
+def graph():
+    return synth.random_csr(900, 1100, seed=21, max_deg=250, special=(577, 1154, 1000))
+
+
+def bound_ok(g, rowptr, colind, val, dC, n_cols, s, strat, seed, reduce):
+    o = oracle.spmm_backward(rowptr, colind, val, dC, n_cols, s, strat, seed=seed, reduce=reduce)
+    mag = oracle.spmm_backward(rowptr, colind, None if val is None else np.abs(val), np.abs(dC), n_cols, s,
+                               strat, seed=seed, reduce=reduce).astype(np.float64)
+    _, sc, _, _ = oracle.sample(rowptr, colind, val, s, strat, seed)
+    nc = np.bincount(sc, minlength=n_cols).astype(np.float64)[:, None]
+    tol = (nc + 2) * U * mag + 1e-30
+    err = np.abs(g.astype(np.float64) - o)
+    return bool(np.all(err <= tol)), float(np.max(err / np.maximum(mag, 1e-30)))
+
+
+@pytest.mark.parametrize("F,ld", [(1, 1), (16, 16), (41, 41), (128, 128), (602, 604), (602, 602), (1100, 1100)])
+@pytest.mark.parametrize("strat", [1, 2])
+@pytest.mark.parametrize("reduce", [0, 1])
+def test_backward_parity(graph, F, ld, strat, reduce):
+    rowptr, colind, val = graph
+    dC = synth.dense(900, F, seed=F + 1, ld=ld)
+    dB = es.es_spmm_backward(t(rowptr), t(colind), t(val), t(dC), 1100, 64, strat, 9, reduce, F=F, ldb=ld)
+    torch.cuda.synchronize()
+    g = dB.cpu().numpy()
+    ok, worst = bound_ok(g[:, :F], rowptr, colind, val, dC[:, :F], 1100, 64, strat, 9, reduce)
+    assert ok, worst
+    if ld > F:
+        assert np.all(g[:, F:] == 0)          # padding columns never touched
+
+
+def test_backward_ones_exact(graph):
+    rowptr, colind, _ = graph
+    for s in (1, 32, 3000):
+        dB = es.es_spmm_backward(t(rowptr), t(colind), None, torch.ones((900, 8), device=DEV), 1100, s, 2, 4)
+        _, sc, _, _ = oracle.sample(rowptr, colind, None, s, 2, 4)
+        hits = np.bincount(sc, minlength=1100).astype(np.float32)
+        assert np.array_equal(dB.cpu().numpy(), np.repeat(hits[:, None], 8, 1))
+
+
+def test_adjoint_identity_gpu(graph):
+    rowptr, colind, val = graph
+    B = synth.dense(1100, 96, seed=3)
+    dC = synth.dense(900, 96, seed=4)
+    for reduce in (0, 1):
+        C = es.es_spmm_run(t(rowptr), t(colind), t(val), t(B), 50, 2, 7, reduce)
+        dB = es.es_spmm_backward(t(rowptr), t(colind), t(val), t(dC), 1100, 50, 2, 7, reduce)
+        lhs = float(torch.sum(C.double() * t(dC).double()))
+        rhs = float(torch.sum(t(B).double() * dB.double()))
+        assert abs(lhs - rhs) <= 1e-5 * abs(lhs)
+
+
+def test_row_blocks_accumulate_into_one_dB(graph):
+    rowptr, colind, val = graph
+    dC = synth.dense(900, 64, seed=5)
+    full = es.es_spmm_backward(t(rowptr), t(colind), t(val), t(dC), 1100, 40, 2, 3, 1)
+    dB = torch.zeros((1100, 64), device=DEV)
+    bounds = es.es_partition_rows(rowptr, 40, 64, 3)
+    for a, b in zip(bounds[:-1], bounds[1:]):
+        e0, e1 = rowptr[a], rowptr[b]
+        es.es_spmm_backward(t(rowptr[a:b + 1]), t(colind[e0:e1]), t(val[e0:e1]), t(dC[a:b]), 1100, 40, 2, 3, 1,
+                            dB=dB, row_begin=int(a), row_end=int(b), n_rows=900, nnz_base=int(e0))
+    assert torch.allclose(dB, full, rtol=1e-5, atol=1e-6)
+
+
+def test_autograd_gradient(graph):
+    rowptr, colind, val = graph
+    B = t(synth.dense(1100, 32, seed=8)).requires_grad_(True)
+    W = t(synth.dense(900, 32, seed=9))
+    for seed in (1, 2):                     # a new sampled subset per "iteration"
+        C = sampled_spmm(B, t(rowptr), t(colind), t(val), 24, 2, seed, 1)
+        loss = (C * W).sum()
+        B.grad = None
+        loss.backward()
+        g = B.grad.cpu().numpy()
+        ok, worst = bound_ok(g, rowptr, colind, val, W.cpu().numpy(), 1100, 24, 2, seed, 1)
+        assert ok, worst
