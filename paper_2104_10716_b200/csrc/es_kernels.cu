@@ -54,8 +54,8 @@ __device__ __forceinline__ float finish(float x, int reduce, int32_t k) {
 }
 
 // ------------------------------------------------------------------ warp per row
-template <int VEC, int NCH, int U>
-__global__ void __launch_bounds__(kThreads)
+template <int VEC, int NCH, int U, int MINB = 1>
+__global__ void __launch_bounds__(kThreads, MINB)
 spmm_warp(const SpmmParams p) {
     const int lane = threadIdx.x & 31;
     const int64_t r = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
@@ -537,14 +537,19 @@ template <int VEC, int NCH>
 cudaError_t launch_warp(const SpmmParams& p, const Plan& plan, cudaStream_t st) {
     constexpr int U = NCH == 1 ? 8 : (NCH == 2 ? 4 : 2);
     const int64_t blocks = (p.n_rows + kWarps - 1) / kWarps;
-    if constexpr (NCH == 1) {
-        if (plan.u == 16) {
-            spmm_warp<VEC, 1, 16><<<(unsigned)blocks, kThreads, 0, st>>>(p);
-            return cudaGetLastError();
-        }
+    if constexpr (NCH == 1 && VEC == 4) {      // tuning variants (ES_SPMM_U / ES_SPMM_MINB)
+        auto k = spmm_warp<VEC, 1, 4, 4>;
+        if (plan.u == 2) k = plan.minb >= 6 ? spmm_warp<VEC, 1, 2, 6> : plan.minb >= 5 ? spmm_warp<VEC, 1, 2, 5>
+                                                                            : spmm_warp<VEC, 1, 2, 4>;
+        else if (plan.u == 4) k = plan.minb >= 6 ? spmm_warp<VEC, 1, 4, 6> : plan.minb >= 5 ? spmm_warp<VEC, 1, 4, 5>
+                                                                               : spmm_warp<VEC, 1, 4, 4>;
+        else if (plan.u == 8) k = plan.minb >= 4 ? spmm_warp<VEC, 1, 8, 4> : spmm_warp<VEC, 1, 8, 3>;
+        k<<<(unsigned)blocks, kThreads, 0, st>>>(p);
+        return cudaGetLastError();
+    } else {
+        spmm_warp<VEC, NCH, U><<<(unsigned)blocks, kThreads, 0, st>>>(p);
+        return cudaGetLastError();
     }
-    spmm_warp<VEC, NCH, U><<<(unsigned)blocks, kThreads, 0, st>>>(p);
-    return cudaGetLastError();
 }
 
 template <int VEC, int G>
@@ -645,7 +650,8 @@ Plan make_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C
         pl.nch = (int)(nch > 8 ? 8 : nch);
     }
     pl.c_vec = (c % (4u * (unsigned)pl.vec) == 0) && (ldc % pl.vec == 0);
-    pl.u = env_int("ES_SPMM_U", 8);
+    pl.u = env_int("ES_SPMM_U", 4);
+    pl.minb = env_int("ES_SPMM_MINB", 4);
     // TMA ring: whole 16-B padded B rows as bulk copies; needs 16-B alignment and F <= 1024.
     const int64_t nv4 = (F + 3) / 4;
     // Measured (profiles/r01.md): TMA wins for wide rows (Reddit F=602: 9.5 vs 26.8 ms,
