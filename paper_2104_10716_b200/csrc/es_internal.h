@@ -29,6 +29,7 @@ struct Plan {
     int nch;        // vectors per lane per feature tile (warp)
     bool c_vec;
     bool tma;          // TMA-ring kernel (spmm_tma)
+    bool cpasync;      // cp.async ring kernel (spmm_cpasync)
     int stages;         // ring depth (tma)
     int rows_per_warp;  // consecutive rows per warp (tma)
     int minb;           // __launch_bounds__ min blocks per SM (tma register cap)

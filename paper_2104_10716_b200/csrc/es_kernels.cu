@@ -212,6 +212,117 @@ spmm_subwarp(const SpmmParams p) {
     }
 }
 
+// ------------------------------------------------------------------ cp.async ring
+// One warp per row; lane l owns feature vectors l + 32c, c < NCH (F <= 128*NCH).  Each lane
+// streams ITS OWN 16-B pieces of every gathered B row into a private D-deep shared-memory
+// ring with cp.async (SASS LDGSTS): bytes in flight live in smem, not registers (D slots per
+// warp at ~40 registers/thread -> 48 warps/SM for F=128), and since a lane only ever reads
+// what it copied, no warp or CTA synchronisation is needed.  Same per-element order as
+// spmm_warp / spmm_tma (32-slot partials), so results are bitwise interchangeable.
+template <int NCH, int D, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
+spmm_cpasync(const SpmmParams p) {
+    static_assert(D >= 1 && D <= 32, "ring depth");
+    extern __shared__ __align__(16) float4 ring_smem[];          // [kWarps][D][NCH*32]
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int64_t r = (int64_t)blockIdx.x * kWarps + warp;
+    if (r >= p.n_rows) return;
+    const uint64_t pol_a = policy_evict_first();
+    const uint64_t pol_b = policy_evict_last();
+    RowSampler rs;
+    rs.init(ld_stream(p.rowptr + r, pol_a) - p.nnz_base, ld_stream(p.rowptr + r + 1, pol_a) - p.nnz_base,
+            p.s, p.strategy, p.seed, p.row_base + r);
+    const int NV = (int)((p.F + 3) / 4);
+    const int32_t k = rs.k;
+    constexpr int kStage = NCH * 32;                             // float4 per stage
+    float4* my = ring_smem + (size_t)warp * D * kStage + lane;
+    const float* bl = p.B + lane * 4;
+
+    auto copy_slot = [&](int stage, int32_t c) {
+        const float* src = bl + (int64_t)c * p.ldb;
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch)
+            if (lane + 32 * ch < NV) cp_async16(my + stage * kStage + 32 * ch, src + 128 * ch, pol_b);
+    };
+
+    // (col, val) of the chunk holding the consumer slot (c0, a0) and of the next chunk (c1, a1)
+    int32_t c0 = 0, c1 = 0;
+    float a0 = 0.0f, a1 = 0.0f;
+    if (lane < k) {
+        const int64_t e = rs.beg + rs.pos(lane);
+        c0 = ld_stream(p.colind + e, pol_a);
+        a0 = p.val ? ld_stream(p.val + e, pol_a) : 1.0f;
+    }
+    if (32 + lane < k) {
+        const int64_t e = rs.beg + rs.pos(32 + lane);
+        c1 = ld_stream(p.colind + e, pol_a);
+        a1 = p.val ? ld_stream(p.val + e, pol_a) : 1.0f;
+    }
+    // prologue: slots 0 .. D-1 (all in chunk 0 since D <= 32)
+#pragma unroll
+    for (int t = 0; t < D; ++t) {
+        const int32_t c = __shfl_sync(kFull, c0, t);
+        if (t < k) copy_slot(t, c);
+        cp_async_commit();
+    }
+    float part[NCH][4], tot[NCH][4];
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) { part[ch][q] = 0.0f; tot[ch][q] = 0.0f; }
+    for (int32_t j0 = 0; j0 < k; j0 += 32) {
+        const int n_here = min(32, k - j0);
+#pragma unroll 4
+        for (int u = 0; u < 32; ++u) {
+            if (u >= n_here) break;
+            const int st = (j0 + u) % D;
+            cp_async_wait<D - 1>();                               // slot j0+u has landed
+            const float av = __shfl_sync(kFull, a0, u);
+#pragma unroll
+            for (int ch = 0; ch < NCH; ++ch) {
+                if (lane + 32 * ch < NV) {
+                    const float4 x = my[st * kStage + 32 * ch];
+                    part[ch][0] = fmaf(av, x.x, part[ch][0]);
+                    part[ch][1] = fmaf(av, x.y, part[ch][1]);
+                    part[ch][2] = fmaf(av, x.z, part[ch][2]);
+                    part[ch][3] = fmaf(av, x.w, part[ch][3]);
+                }
+            }
+            // refill this stage with slot j0 + u + D (current chunk or the next)
+            const int tn = u + D;
+            const int32_t cc = __shfl_sync(kFull, c0, tn & 31);
+            const int32_t cn = __shfl_sync(kFull, c1, tn & 31);
+            if (j0 + tn < k) copy_slot(st, tn < 32 ? cc : cn);
+            cp_async_commit();
+        }
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) { tot[ch][q] += part[ch][q]; part[ch][q] = 0.0f; }
+        // advance the chunk window; the chunk after next is requested now (used >= 32 - D slots later)
+        c0 = c1;
+        a0 = a1;
+        c1 = 0;
+        a1 = 0.0f;
+        if (j0 + 64 + lane < k) {
+            const int64_t e = rs.beg + rs.pos(j0 + 64 + lane);
+            c1 = ld_stream(p.colind + e, pol_a);
+            a1 = p.val ? ld_stream(p.val + e, pol_a) : 1.0f;
+        }
+    }
+    cp_async_wait<0>();
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) {
+        if (lane + 32 * ch < NV) {
+            float res[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) res[q] = finish(tot[ch][q], p.reduce, k);
+            store_out<4>(p.C + r * p.ldc, lane + 32 * ch, p.F, res, p.c_vec, pol_a);
+        }
+    }
+}
+
 // ------------------------------------------------------------------ per-warp slot stream
 // A warp owns R <= 32 consecutive rows; their sampled slots form one flat stream (row by
 // row, slot order).  Row i's metadata (a1) lives in lane i; (col, val) of 32 consecutive
@@ -533,6 +644,50 @@ sample_materialize(const int64_t* __restrict__ rowptr, int64_t nnz_base,
 // ------------------------------------------------------------------ host launchers
 namespace {
 
+template <int NCH, int D, int MINB>
+cudaError_t launch_cpasync_k(const SpmmParams& p, cudaStream_t st) {
+    const int64_t blocks = (p.n_rows + kWarps - 1) / kWarps;
+    auto k = spmm_cpasync<NCH, D, MINB>;
+    const size_t smem = (size_t)kWarps * D * NCH * 32 * 16;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    k<<<(unsigned)blocks, kThreads, smem, st>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cpasync(const SpmmParams& p, const Plan& plan, cudaStream_t st) {
+    // (MINB = 8 -- 32 registers -- made ptxas emit code that traps with an illegal instruction
+    //  on B200; 6 is the tested ceiling)
+    if (plan.nch == 1) {
+        const bool m4 = plan.minb <= 4;
+        switch (plan.stages) {
+            case 2: return m4 ? launch_cpasync_k<1, 2, 4>(p, st) : launch_cpasync_k<1, 2, 6>(p, st);
+            case 3: return m4 ? launch_cpasync_k<1, 3, 4>(p, st) : launch_cpasync_k<1, 3, 6>(p, st);
+            case 8: return m4 ? launch_cpasync_k<1, 8, 4>(p, st) : launch_cpasync_k<1, 8, 6>(p, st);
+            default: return m4 ? launch_cpasync_k<1, 4, 4>(p, st) : launch_cpasync_k<1, 4, 6>(p, st);
+        }
+    }
+    const bool d2 = plan.stages == 2;
+    if (plan.nch == 2) {
+        const bool m4 = plan.minb >= 4;
+        switch (plan.stages) {
+            case 2: return m4 ? launch_cpasync_k<2, 2, 4>(p, st) : launch_cpasync_k<2, 2, 1>(p, st);
+            case 8: return m4 ? launch_cpasync_k<2, 8, 4>(p, st) : launch_cpasync_k<2, 8, 1>(p, st);
+            default: return m4 ? launch_cpasync_k<2, 4, 4>(p, st) : launch_cpasync_k<2, 4, 1>(p, st);
+        }
+    }
+    switch (plan.nch) {
+        case 3: return d2 ? launch_cpasync_k<3, 2, 1>(p, st) : launch_cpasync_k<3, 4, 1>(p, st);
+        case 4: return d2 ? launch_cpasync_k<4, 2, 1>(p, st) : launch_cpasync_k<4, 4, 1>(p, st);
+        case 5: return d2 ? launch_cpasync_k<5, 2, 1>(p, st) : launch_cpasync_k<5, 4, 1>(p, st);
+        case 6: return d2 ? launch_cpasync_k<6, 2, 1>(p, st) : launch_cpasync_k<6, 4, 1>(p, st);
+        case 7: return d2 ? launch_cpasync_k<7, 2, 1>(p, st) : launch_cpasync_k<7, 4, 1>(p, st);
+        default: return d2 ? launch_cpasync_k<8, 2, 1>(p, st) : launch_cpasync_k<8, 4, 1>(p, st);
+    }
+}
+
 template <int VEC, int NCH>
 cudaError_t launch_warp(const SpmmParams& p, const Plan& plan, cudaStream_t st) {
     constexpr int U = NCH == 1 ? 8 : (NCH == 2 ? 4 : 2);
@@ -624,6 +779,7 @@ static int env_kernel_override() {
     if (!e) return 0;
     if (!strcmp(e, "warp")) return 1;
     if (!strcmp(e, "tma")) return 2;
+    if (!strcmp(e, "cpasync")) return 3;
     return 0;
 }
 
@@ -656,10 +812,21 @@ Plan make_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C
     const int64_t nv4 = (F + 3) / 4;
     // Measured (profiles/r01.md): TMA wins for wide rows (Reddit F=602: 9.5 vs 26.8 ms,
     // F=256: 4.8 vs 8.2 ms); for 512-B rows (F=128) the LDG warp kernel wins (2.97 vs 4.3 ms).
-    const int64_t kTmaMinRowBytes = env_int("ES_SPMM_TMA_MIN_BYTES", 1024);
+    const int64_t kTmaMinRowBytes = env_int("ES_SPMM_TMA_MIN_BYTES", 2048);
     const bool tma_ok = pl.vec == 4 && nv4 > 32 && nv4 <= 32 * 8;
     const int ov = env_kernel_override();
     pl.tma = tma_ok && ov != 1 && (ov == 2 || ldb * 4 >= kTmaMinRowBytes);
+    // cp.async ring: 16-B aligned B, 16 < F/4 <= 128 by default (profiles/r01.md: Reddit F=128
+    // 1.95 vs 2.27 ms, F=256 3.13 vs 4.55 (TMA), F=512 7.23 vs 7.51 (TMA); F=602 TMA wins 9.4 vs
+    // 10.4); forced up to F/4 <= 256 with ES_SPMM_KERNEL=cpasync.
+    pl.cpasync = pl.vec == 4 && nv4 > 16 && nv4 <= 32 * 8 &&
+                 (ov == 3 || (ov == 0 && nv4 <= 32 * 4));
+    if (pl.cpasync) {
+        pl.tma = false;
+        pl.nch = (int)((nv4 + 31) / 32);
+        pl.stages = env_int("ES_SPMM_STAGES", 4);
+        pl.minb = env_int("ES_SPMM_MINB", pl.nch == 1 ? 6 : 1);
+    }
     if (pl.tma) {
         pl.nch = (int)((nv4 + 31) / 32);
         pl.subwarp = false;
@@ -677,6 +844,7 @@ cudaError_t launch_spmm(SpmmParams p, const Plan& plan, cudaStream_t st) {
     if (p.n_rows <= 0) return cudaSuccess;
     p.c_vec = plan.c_vec ? 1 : 0;
     if (plan.tma) return dispatch_tma(p, plan, st);
+    if (plan.cpasync) return launch_cpasync(p, plan, st);
     switch (plan.vec) {
         case 4: return dispatch_vec<4>(p, plan, st);
         case 2: return dispatch_vec<2>(p, plan, st);

@@ -95,7 +95,7 @@ FS = [(1, 1), (3, 3), (3, 4), (7, 8), (16, 16), (17, 17), (32, 32), (64, 64), (1
       (128, 128), (129, 132), (256, 256), (602, 602), (602, 604), (1000, 1000), (1100, 1104)]
 
 
-@pytest.fixture(params=["auto", "warp", "tma"])
+@pytest.fixture(params=["auto", "warp", "tma", "cpasync"])
 def kernel(request, monkeypatch):
     """Run a test under the automatic plan and with each kernel family forced where it
     applies (TMA ring, LDG warp-per-row, LDG register-ring stream)."""

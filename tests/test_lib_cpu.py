@@ -70,17 +70,22 @@ def test_host_validation_rejects_bad_arguments(lib):
 
 
 def test_plan_selection(lib, monkeypatch):
-    assert es.es_spmm_plan(128, 128, 128).startswith("es::spmm_warp<vec4,nch1>")   # 512-B rows
-    assert es.es_spmm_plan(200, 200, 200).startswith("es::spmm_warp<vec4,nch2>")
-    assert es.es_spmm_plan(256, 256, 256).startswith("es::spmm_tma<nch2,stages4>")
+    assert es.es_spmm_plan(128, 128, 128).startswith("es::spmm_cpasync<stages4>")
+    assert es.es_spmm_plan(200, 200, 200).startswith("es::spmm_cpasync<stages4>")
+    assert es.es_spmm_plan(256, 256, 256).startswith("es::spmm_cpasync<stages4>")
+    assert es.es_spmm_plan(512, 512, 512).startswith("es::spmm_cpasync<stages4>")
     assert es.es_spmm_plan(602, 604, 604).startswith("es::spmm_tma<nch5,stages4>")
+    assert es.es_spmm_plan(100, 102, 100).startswith("es::spmm_warp<vec2")      # 8-B aligned rows
     monkeypatch.setenv("ES_SPMM_KERNEL", "warp")
     assert es.es_spmm_plan(128, 128, 128).startswith("es::spmm_warp<vec4,nch1>")
+    assert es.es_spmm_plan(256, 256, 256).startswith("es::spmm_warp<vec4,nch2>")
     assert "vec4,nch5" in es.es_spmm_plan(602, 604, 604)
     monkeypatch.delenv("ES_SPMM_KERNEL")
     assert "spmm_warp<vec2" in es.es_spmm_plan(602, 602, 602)      # 8-B rows: no TMA
     monkeypatch.setenv("ES_SPMM_KERNEL", "tma")
     assert es.es_spmm_plan(200, 200, 200).startswith("es::spmm_tma<nch2")
+    monkeypatch.setenv("ES_SPMM_KERNEL", "cpasync")
+    assert es.es_spmm_plan(602, 604, 604).startswith("es::spmm_cpasync")
     monkeypatch.delenv("ES_SPMM_KERNEL")
     assert "subwarp<vec4,g4>" in es.es_spmm_plan(16, 16, 16)
     assert "subwarp<vec1,g1>" in es.es_spmm_plan(1, 1, 1)
@@ -98,6 +103,7 @@ class _B:
 def test_plan_alignment_fallback(lib):
     # B misaligned by 4 bytes -> scalar gathers; C misaligned -> scalar stores
     assert "vec1" in es.es_spmm_plan(128, 128, 128, B=_B(0x1004), C=_B(0x1000))
+    assert "vec2" in es.es_spmm_plan(128, 128, 128, B=_B(0x1008), C=_B(0x1000))
     assert "scalar C" in es.es_spmm_plan(128, 128, 128, B=_B(0x1000), C=_B(0x1004))
 
 
