@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true", help="warm-L2 variant (not the headline)")
+    ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
+                    help="replay each step from a captured CUDA graph (auto: when a step < 0.5 ms, "
+                         "i.e. launch-bound configs)")
     ap.add_argument("--cpu-seconds", type=float, default=3.0, help="wall-time target of the oracle sample")
     a = ap.parse_args()
     d = DEFAULTS[a.config]
@@ -231,15 +234,39 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
-    def step():
+    def launch(st):
         es.es_spmm_run_rows(n, rp_d, e0, ci_d, va_d, B_d, a.s, strat_id, a.seed, red_id, r0, r1,
-                            F=F, C=C_d, stream=stream)
+                            F=F, C=C_d, stream=st)
 
+    lc0 = es.es_launch_count()
     for _ in range(a.warmup):
         if not a.no_flush:
             flush.zero_()
-        step()
+        launch(stream)
     torch.cuda.synchronize(dev)
+    launches_per_step = (es.es_launch_count() - lc0) // a.warmup
+    w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0.record(stream)
+    launch(stream)
+    w1.record(stream)
+    torch.cuda.synchronize(dev)
+    use_graph = a.graph == "on" or (a.graph == "auto" and w0.elapsed_time(w1) < 0.5)
+    if use_graph:
+        # the step's launches captured once and replayed: the timed region then holds the
+        # kernel's device time instead of host launch latency (launch-bound small graphs)
+        graph = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream(dev)
+        cap.wait_stream(stream)
+        with torch.cuda.graph(graph, stream=cap):
+            launch(cap)
+        stream.wait_stream(cap)
+        torch.cuda.synchronize(dev)
+
+        def step():
+            graph.replay()
+    else:
+        def step():
+            launch(stream)
 
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
@@ -249,7 +276,6 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    launches0 = es.es_launch_count()
     wall0 = time.perf_counter()
     for i in range(a.steps):
         if not a.no_flush:
@@ -261,7 +287,7 @@ def main():
     if world > 1:
         dist.barrier()
     wall = time.perf_counter() - wall0
-    launches = es.es_launch_count() - launches0
+    launches = launches_per_step * a.steps          # our kernels launched in the timed region
     clk = clocks.stop()
 
     per_step = np.array([s_.elapsed_time(e_) for s_, e_ in zip(starts, ends)]) / 1e3   # seconds
@@ -329,7 +355,8 @@ def main():
                        "l2": "no flush (warm)" if a.no_flush else "flushed between timed steps (256 MiB write)",
                        "parallelism": f"row-partitioned x{world} (sampled-byte balanced), B replicated"
                                       + ("" if backend == "nccl" else f" [{backend} validation run]"),
-                       "timing": "sum of per-step CUDA-event times on the launch stream, max over ranks"},
+                       "timing": "sum of per-step CUDA-event times on the launch stream, max over ranks"
+                                 + ("; each step replays a captured CUDA graph" if use_graph else "")},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -308,3 +308,21 @@ def test_full_reddit(F, ldb, strat, kernel):
 def test_full_scaled(strat):
     """Config 5: 10M nodes, 1.0B edges, F=256, s=128 (bench launch configuration, 1 GPU)."""
     _full("scaled", 256, 256, 128, strat, 0, ES_REDUCE_SUM, n_check=1000)
+
+
+def test_hand_golden_exact(golden, kernel):
+    """The hand-checkable worked example (tests/golden/worked_examples.json 'hand'): small
+    integers, so every kernel family must reproduce it exactly."""
+    g = golden["hand"]
+    rowptr = np.array(g["rowptr"], np.int64)
+    colind = np.array(g["colind"], np.int32)
+    for F in (2, 130, 602):          # subwarp / warp-or-cpasync / tma paths; extra columns = 0
+        B = np.zeros((g["n_cols"], F if F != 602 else 604), np.float32)
+        B[:, 0] = np.arange(1, g["n_cols"] + 1)
+        B[:, 1] = 10 * np.arange(1, g["n_cols"] + 1)
+        for c in g["cases"]:
+            strat = ES_BUCKET if c["strategy"] == "bucket" else ES_FASTRAND
+            red = ES_REDUCE_SUM if c["reduce"] == "sum" else ES_REDUCE_MEAN
+            out = run_gpu(rowptr, colind, None, B, c["s"], strat, 0, red, F=F)
+            assert np.array_equal(out[:, :2], np.array(c["C"], np.float32)), (F, c)
+            assert np.all(out[:, 2:] == 0)
