@@ -53,16 +53,18 @@ def _L():
         lib.oracle_offset.argtypes = [u64, i64, i64]
         lib.oracle_position.restype = i64
         lib.oracle_position.argtypes = [i32, i64, i64, i64]
+        lib.oracle_position_p.restype = i64
+        lib.oracle_position_p.argtypes = [i32, i64, i64, i64, i64]
         lib.oracle_rate.restype = ctypes.c_double
         lib.oracle_rate.argtypes = [i64, vp, i64]
         lib.oracle_sample.restype = None
-        lib.oracle_sample.argtypes = [i64, vp, vp, vp, i64, i32, u64, i64, vp, vp, vp, vp]
+        lib.oracle_sample.argtypes = [i64, vp, vp, vp, i64, i32, u64, i64, i64, vp, vp, vp, vp]
         lib.oracle_spmm.restype = ctypes.c_int
-        lib.oracle_spmm.argtypes = [i64, vp, vp, vp, vp, i64, i64, i64, i32, u64, i32, i64,
+        lib.oracle_spmm.argtypes = [i64, vp, vp, vp, vp, i64, i64, i64, i32, u64, i32, i64, i64, i32,
                                     vp, i64, vp, i64]
         lib.oracle_spmm_backward.restype = ctypes.c_int
         lib.oracle_spmm_backward.argtypes = [i64, vp, vp, vp, vp, i64, i64, i64, i32, u64, i32, i64,
-                                             i64, vp, i64]
+                                             i64, i32, i64, vp, i64]
         lib.oracle_max_threads.restype = ctypes.c_int
         lib.oracle_max_threads.argtypes = []
         _lib = lib
@@ -89,9 +91,11 @@ def offset(seed: int, row: int, d: int) -> int:
     return int(_L().oracle_offset(seed & (2**64 - 1), row, d))
 
 
-def position(strategy: int, j: int, d: int, off: int = 0) -> int:
-    """Eq. 2 (FastRand) / j (Bucket)."""
-    return int(_L().oracle_position(strategy, j, d, off))
+def position(strategy: int, j: int, d: int, off: int = 0, prime: int = PRIME) -> int:
+    """Eq. 2 (FastRand) / j (Bucket); prime = P' (577, L1058)."""
+    if prime == PRIME:
+        return int(_L().oracle_position(strategy, j, d, off))
+    return int(_L().oracle_position_p(strategy, j, d, off, prime))
 
 
 def rate(rowptr, s: int) -> float:
@@ -100,28 +104,31 @@ def rate(rowptr, s: int) -> float:
     return float(_L().oracle_rate(len(rowptr) - 1, rowptr.ctypes.data, s))
 
 
-def sample(rowptr, colind, val, s: int, strategy: int, seed: int = 0, row_base: int = 0):
+def sample(rowptr, colind, val, s: int, strategy: int, seed: int = 0, row_base: int = 0,
+           prime: int = PRIME):
     """Materialised sampled CSR in slot order: (s_rowptr, s_colind, s_val, s_pos)."""
     rowptr, colind, val = _csr(rowptr, colind, val)
     n = len(rowptr) - 1
     s_rowptr = np.empty(n + 1, dtype=np.int64)
     L = _L()
     L.oracle_sample(n, rowptr.ctypes.data, colind.ctypes.data, _p(val), s, strategy,
-                    seed & (2**64 - 1), row_base, s_rowptr.ctypes.data, None, None, None)
+                    seed & (2**64 - 1), row_base, prime, s_rowptr.ctypes.data, None, None, None)
     K = int(s_rowptr[-1])
     s_colind = np.empty(K, dtype=np.int32)
     s_val = np.empty(K, dtype=np.float32)
     s_pos = np.empty(K, dtype=np.int64)
     L.oracle_sample(n, rowptr.ctypes.data, colind.ctypes.data, _p(val), s, strategy,
-                    seed & (2**64 - 1), row_base, s_rowptr.ctypes.data, s_colind.ctypes.data,
+                    seed & (2**64 - 1), row_base, prime, s_rowptr.ctypes.data, s_colind.ctypes.data,
                     s_val.ctypes.data, s_pos.ctypes.data)
     return s_rowptr, s_colind, s_val, s_pos
 
 
 def spmm(rowptr, colind, val, B, s: int, strategy: int, seed: int = 0, reduce: int = SUM,
-         F: int | None = None, rows=None, row_base: int = 0) -> np.ndarray:
+         F: int | None = None, rows=None, row_base: int = 0, prime: int = PRIME,
+         mean_by_degree: bool = False) -> np.ndarray:
     """Sampled SpMM C (fp32).  B is (n_cols, ldb) fp32; F defaults to ldb.
-    ``rows``: optional int64 row list -> returns only those rows (len(rows) x F)."""
+    ``rows``: optional int64 row list -> returns only those rows (len(rows) x F).
+    ``prime`` / ``mean_by_degree``: NEXT-4 variants (P' override; MEAN divides by d_i)."""
     rowptr, colind, val = _csr(rowptr, colind, val)
     B = np.ascontiguousarray(B, dtype=np.float32)
     ldb = B.shape[1]
@@ -136,15 +143,16 @@ def spmm(rowptr, colind, val, B, s: int, strategy: int, seed: int = 0, reduce: i
     if n_out == 0 or F == 0:
         return C
     rc = _L().oracle_spmm(n, rowptr.ctypes.data, colind.ctypes.data, _p(val), B.ctypes.data, F,
-                          ldb, s, strategy, seed & (2**64 - 1), reduce, row_base, _p(rows),
-                          n_out, C.ctypes.data, F)
+                          ldb, s, strategy, seed & (2**64 - 1), reduce, row_base, prime,
+                          int(mean_by_degree), _p(rows), n_out, C.ctypes.data, F)
     if rc != 0:
         raise MemoryError("oracle_spmm: allocation failed")
     return C
 
 
 def spmm_backward(rowptr, colind, val, dC, n_cols: int, s: int, strategy: int, seed: int = 0,
-                  reduce: int = SUM, F: int | None = None, row_base: int = 0) -> np.ndarray:
+                  reduce: int = SUM, F: int | None = None, row_base: int = 0, prime: int = PRIME,
+                  mean_by_degree: bool = False) -> np.ndarray:
     """dB = A_s^T dC over the forward's sampled slots (MEAN: rows of A_s scaled by 1/k_i);
     returns a fresh (n_cols, F) fp32 array."""
     rowptr, colind, val = _csr(rowptr, colind, val)
@@ -155,7 +163,8 @@ def spmm_backward(rowptr, colind, val, dC, n_cols: int, s: int, strategy: int, s
         return dB
     rc = _L().oracle_spmm_backward(len(rowptr) - 1, rowptr.ctypes.data, colind.ctypes.data, _p(val),
                                    dC.ctypes.data, F, dC.shape[1], s, strategy, seed & (2**64 - 1),
-                                   reduce, row_base, n_cols, dB.ctypes.data, F)
+                                   reduce, row_base, prime, int(mean_by_degree), n_cols,
+                                   dB.ctypes.data, F)
     if rc != 0:
         raise MemoryError("oracle_spmm_backward: allocation failed")
     return dB

@@ -27,23 +27,23 @@ def _splitmix(x: int) -> int:
     return x
 
 
-def positions(strategy: int, d: int, s: int, seed: int = 0, row: int = 0) -> list[int]:
+def positions(strategy: int, d: int, s: int, seed: int = 0, row: int = 0, prime: int = 577) -> list[int]:
     k = min(d, s)
     if strategy == BUCKET:
         return list(range(k))
     off = 0
     if seed and d:
         off = _splitmix(seed + 0x9E3779B97F4A7C15 * (row + 1)) % d
-    return [(off + j * 577) % d for j in range(k)]
+    return [(off + j * prime) % d for j in range(k)]
 
 
-def sampled_dense(rowptr, colind, val, n_cols: int, s: int, strategy: int, seed: int = 0):
+def sampled_dense(rowptr, colind, val, n_cols: int, s: int, strategy: int, seed: int = 0, prime: int = 577):
     n = len(rowptr) - 1
     A = np.zeros((n, n_cols), dtype=np.float64)
     k = np.zeros(n, dtype=np.int64)
     for i in range(n):
         lo, hi = int(rowptr[i]), int(rowptr[i + 1])
-        ps = positions(strategy, hi - lo, s, seed, i)
+        ps = positions(strategy, hi - lo, s, seed, i, prime)
         k[i] = len(ps)
         for p in ps:
             e = lo + p
@@ -51,13 +51,15 @@ def sampled_dense(rowptr, colind, val, n_cols: int, s: int, strategy: int, seed:
     return A, k
 
 
-def spmm(rowptr, colind, val, B, s: int, strategy: int, seed: int = 0, reduce: int = SUM):
+def spmm(rowptr, colind, val, B, s: int, strategy: int, seed: int = 0, reduce: int = SUM,
+         prime: int = 577, mean_by_degree: bool = False):
     B = np.asarray(B, dtype=np.float32)
-    A, k = sampled_dense(rowptr, colind, val, B.shape[0], s, strategy, seed)
+    A, k = sampled_dense(rowptr, colind, val, B.shape[0], s, strategy, seed, prime)
     C = (A @ B.astype(np.float64)).astype(np.float32)
     if reduce == MEAN:
-        kk = np.maximum(k, 1).astype(np.float32)[:, None]
-        C = np.where(k[:, None] > 0, C / kk, np.float32(0.0)).astype(np.float32)
+        div = np.diff(np.asarray(rowptr, np.int64)) if mean_by_degree else k
+        dd = np.maximum(div, 1).astype(np.float32)[:, None]
+        C = np.where(div[:, None] > 0, C / dd, np.float32(0.0)).astype(np.float32)
     return C
 
 

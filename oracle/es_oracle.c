@@ -57,10 +57,16 @@ int64_t oracle_offset(uint64_t seed, int64_t row, int64_t d) {
 /* Position within the row of sampled slot j (0 <= j < k <= d).
  *   Bucket:   p_j = j                                    (L1043 "first S")
  *   FastRand: p_j = (off + j * P') mod d                 (Eq. 2; off per R6)
- * 64-bit unsigned arithmetic: j*577 < 2^64 for any j < 3.2e16. */
-int64_t oracle_position(int32_t strategy, int64_t j, int64_t d, int64_t off) {
+ * P' = 577 (L1058) unless overridden (NEXT-4 sensitivity variant; prime <= 0 means 577).
+ * 64-bit unsigned arithmetic: j*P' < 2^64 for the sizes used here. */
+int64_t oracle_position_p(int32_t strategy, int64_t j, int64_t d, int64_t off, int64_t prime) {
+    uint64_t pp = prime > 0 ? (uint64_t)prime : ORACLE_PRIME;
     if (strategy == ORACLE_BUCKET) return j;
-    return (int64_t)(((uint64_t)off + (uint64_t)j * ORACLE_PRIME) % (uint64_t)d);
+    return (int64_t)(((uint64_t)off + (uint64_t)j * pp) % (uint64_t)d);
+}
+
+int64_t oracle_position(int32_t strategy, int64_t j, int64_t d, int64_t off) {
+    return oracle_position_p(strategy, j, d, off, (int64_t)ORACLE_PRIME);
 }
 
 /* k_i = min(d_i, s)   (Alg. 1 l.6, L961) */
@@ -81,8 +87,8 @@ double oracle_rate(int64_t n_rows, const int64_t* rowptr, int64_t s) {
  * rowptr entries are absolute offsets into colind/val. */
 void oracle_sample(int64_t n_rows, const int64_t* rowptr, const int32_t* colind,
                    const float* val, int64_t s, int32_t strategy, uint64_t seed,
-                   int64_t row_base, int64_t* s_rowptr, int32_t* s_colind, float* s_val,
-                   int64_t* s_pos) {
+                   int64_t row_base, int64_t prime, int64_t* s_rowptr, int32_t* s_colind,
+                   float* s_val, int64_t* s_pos) {
     s_rowptr[0] = 0;
     for (int64_t i = 0; i < n_rows; ++i)
         s_rowptr[i + 1] = s_rowptr[i] + oracle_k(rowptr[i + 1] - rowptr[i], s);
@@ -93,7 +99,7 @@ void oracle_sample(int64_t n_rows, const int64_t* rowptr, const int32_t* colind,
         int64_t k = oracle_k(d, s);
         int64_t off = strategy == ORACLE_FASTRAND ? oracle_offset(seed, row_base + i, d) : 0;
         for (int64_t j = 0; j < k; ++j) {
-            int64_t p = oracle_position(strategy, j, d, off);
+            int64_t p = oracle_position_p(strategy, j, d, off, prime);
             int64_t e = rowptr[i] + p;
             int64_t o = s_rowptr[i] + j;
             s_colind[o] = colind[e];
@@ -106,21 +112,24 @@ void oracle_sample(int64_t n_rows, const int64_t* rowptr, const int32_t* colind,
 /* One output row of the sampled SpMM (Alg. 1 l.5-16 for all col_id of a row):
  *   acc[c] = sum_{j<k} val[e_j] * B[colind[e_j], c]   in fp64, slot order
  *   SUM:  C[c] = fp32(acc[c])
- *   MEAN: C[c] = fp32(acc[c]) / fp32(k)  (IEEE fp32 division), k == 0 -> 0   (R5, R8, R9) */
+ *   MEAN: C[c] = fp32(acc[c]) / fp32(k)  (IEEE fp32 division), k == 0 -> 0   (R5, R8, R9)
+ *         (mean_by_degree: / fp32(d) instead -- the other reading of L1571, NEXT-4) */
 static void oracle_row(int64_t d, const int32_t* cols, const float* vals, const float* B,
                        int64_t F, int64_t ldb, int64_t s, int32_t strategy, int64_t off,
-                       int32_t reduce, double* acc, float* Crow) {
+                       int32_t reduce, int64_t prime, int32_t mean_by_degree, double* acc,
+                       float* Crow) {
     int64_t k = oracle_k(d, s);
+    int64_t div = mean_by_degree ? d : k;
     for (int64_t c = 0; c < F; ++c) acc[c] = 0.0;
     for (int64_t j = 0; j < k; ++j) {
-        int64_t p = oracle_position(strategy, j, d, off);
+        int64_t p = oracle_position_p(strategy, j, d, off, prime);
         double a = vals ? (double)vals[p] : 1.0;
         const float* Brow = B + (int64_t)cols[p] * ldb;
         for (int64_t c = 0; c < F; ++c) acc[c] += a * (double)Brow[c];
     }
     for (int64_t c = 0; c < F; ++c) {
         float v = (float)acc[c];
-        if (reduce == ORACLE_MEAN) v = k > 0 ? v / (float)k : 0.0f;
+        if (reduce == ORACLE_MEAN) v = div > 0 ? v / (float)div : 0.0f;
         Crow[c] = v;
     }
 }
@@ -129,8 +138,8 @@ static void oracle_row(int64_t d, const int32_t* cols, const float* vals, const 
  * rows[] (output row r of C is then global-slice row rows[r]).  Returns -1 on OOM. */
 int oracle_spmm(int64_t n_rows, const int64_t* rowptr, const int32_t* colind, const float* val,
                 const float* B, int64_t F, int64_t ldb, int64_t s, int32_t strategy,
-                uint64_t seed, int32_t reduce, int64_t row_base,
-                const int64_t* rows, int64_t n_sel, float* C, int64_t ldc) {
+                uint64_t seed, int32_t reduce, int64_t row_base, int64_t prime,
+                int32_t mean_by_degree, const int64_t* rows, int64_t n_sel, float* C, int64_t ldc) {
     int64_t n_out = rows ? n_sel : n_rows;
     int bad = 0;
 #pragma omp parallel
@@ -147,7 +156,7 @@ int oracle_spmm(int64_t n_rows, const int64_t* rowptr, const int32_t* colind, co
             int64_t d = rowptr[i + 1] - rowptr[i];
             int64_t off = strategy == ORACLE_FASTRAND ? oracle_offset(seed, row_base + i, d) : 0;
             oracle_row(d, colind + rowptr[i], val ? val + rowptr[i] : NULL, B, F, ldb, s,
-                       strategy, off, reduce, acc, C + r * ldc);
+                       strategy, off, reduce, prime, mean_by_degree, acc, C + r * ldc);
         }
         free(acc);
     }
@@ -164,7 +173,8 @@ int oracle_spmm(int64_t n_rows, const int64_t* rowptr, const int32_t* colind, co
 int oracle_spmm_backward(int64_t n_rows, const int64_t* rowptr, const int32_t* colind,
                          const float* val, const float* dC, int64_t F, int64_t ldc, int64_t s,
                          int32_t strategy, uint64_t seed, int32_t reduce, int64_t row_base,
-                         int64_t n_cols, float* dB, int64_t ldb) {
+                         int64_t prime, int32_t mean_by_degree, int64_t n_cols, float* dB,
+                         int64_t ldb) {
     double* acc = (double*)calloc((size_t)(n_cols > 0 ? n_cols : 1) * (size_t)(F > 0 ? F : 1),
                                   sizeof(double));
     if (!acc) return -1;
@@ -173,9 +183,9 @@ int oracle_spmm_backward(int64_t n_rows, const int64_t* rowptr, const int32_t* c
         int64_t k = oracle_k(d, s);
         int64_t off = strategy == ORACLE_FASTRAND ? oracle_offset(seed, row_base + i, d) : 0;
         for (int64_t j = 0; j < k; ++j) {
-            int64_t e = rowptr[i] + oracle_position(strategy, j, d, off);
+            int64_t e = rowptr[i] + oracle_position_p(strategy, j, d, off, prime);
             double w = val ? (double)val[e] : 1.0;
-            if (reduce == ORACLE_MEAN) w /= (double)k;
+            if (reduce == ORACLE_MEAN) w /= (double)(mean_by_degree ? d : k);
             double* row = acc + (int64_t)colind[e] * F;
             for (int64_t c = 0; c < F; ++c) row[c] += w * (double)dC[i * ldc + c];
         }

@@ -341,3 +341,54 @@ def test_backward_ones_count_column_hits():
                                   FASTRAND, seed=2)
         hits = np.bincount(sc, minlength=500).astype(np.float32)
         assert np.array_equal(dB, np.repeat(hits[:, None], 3, 1))
+
+
+# ----------------------------------------------------------------- NEXT-4 variants
+def test_prime_override_permutation_iff_coprime():
+    """Generalisation of Eq. 2: j -> P' j mod d is a bijection of Z_d iff gcd(P', d) = 1."""
+    for prime in (1, 2, 3, 7, 101, 577, 1009):
+        for d in range(1, 260):
+            ps = [oracle.position(FASTRAND, j, d, 0, prime) for j in range(d)]
+            assert (sorted(ps) == list(range(d))) == (math.gcd(prime, d) == 1), (prime, d)
+    # P' = 1 (and P' = 1 + d) is Bucket order
+    assert [oracle.position(FASTRAND, j, 50, 0, 1) for j in range(50)] == list(range(50))
+    assert [oracle.position(FASTRAND, j, 50, 0, 51) for j in range(50)] == list(range(50))
+
+
+@pytest.mark.parametrize("prime", [2, 7, 1009])
+def test_prime_override_against_brute_force(prime):
+    rowptr, colind, val = synth.random_csr(60, 900, seed=3, max_deg=60, special=(14, 1009))
+    B = synth.dense(900, 5, seed=1)
+    for s in (1, 7, 100):
+        want = oracle.brute.spmm(rowptr, colind, val, B, s, FASTRAND, 4, SUM, prime=prime)
+        got = oracle.spmm(rowptr, colind, val, B, s, FASTRAND, seed=4, prime=prime)
+        assert _ulp_close(got, want)
+        srp, sc, _, spos = oracle.sample(rowptr, colind, val, s, FASTRAND, 4, prime=prime)
+        d = np.diff(rowptr)
+        for i in range(60):
+            assert spos[srp[i]:srp[i + 1]].tolist() == oracle.brute.positions(FASTRAND, int(d[i]), s, 4, i, prime)
+
+
+def test_mean_by_degree_variant():
+    """MEAN by the original degree d_i (the other reading of L1571): with B == 1 every
+    non-empty row is fp32(k_i)/fp32(d_i) exactly; brute force otherwise."""
+    rowptr, colind, val = synth.random_csr(200, 800, seed=6, max_deg=150, special=(577,))
+    d = np.diff(rowptr)
+    ones = np.ones((800, 3), np.float32)
+    for s in (1, 16, 1000):
+        C = oracle.spmm(rowptr, colind, None, ones, s, FASTRAND, reduce=MEAN, mean_by_degree=True)
+        k = np.minimum(d, s)
+        want = np.where(d > 0, k.astype(np.float32) / np.maximum(d, 1).astype(np.float32), 0).astype(np.float32)
+        assert np.array_equal(C, np.repeat(want[:, None], 3, 1))
+        B = synth.dense(800, 4, seed=9)
+        got = oracle.spmm(rowptr, colind, val, B, s, BUCKET, reduce=MEAN, mean_by_degree=True)
+        exp = oracle.brute.spmm(rowptr, colind, val, B, s, BUCKET, 0, MEAN, mean_by_degree=True)
+        assert _ulp_close(got, exp, ulps=2)
+    # backward with the same divisor stays the adjoint
+    B = synth.dense(800, 6, seed=2)
+    dC = synth.dense(200, 6, seed=3)
+    C = oracle.spmm(rowptr, colind, val, B, 12, FASTRAND, seed=1, reduce=MEAN, mean_by_degree=True)
+    dB = oracle.spmm_backward(rowptr, colind, val, dC, 800, 12, FASTRAND, seed=1, reduce=MEAN,
+                              mean_by_degree=True)
+    assert abs(float(np.sum(C.astype(np.float64) * dC)) - float(np.sum(B.astype(np.float64) * dB))) \
+        <= 1e-6 * abs(float(np.sum(C.astype(np.float64) * dC)))
