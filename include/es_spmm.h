@@ -61,6 +61,24 @@ typedef enum {
 
 enum { ES_BUCKET = 1, ES_FASTRAND = 2 };          /* sampling strategy, §4.4 */
 enum { ES_REDUCE_SUM = 0, ES_REDUCE_MEAN = 1 };   /* GCN sum (Eq. 1) / GraphSage mean (L1256) */
+enum { ES_MEAN_BY_SAMPLED = 0, ES_MEAN_BY_DEGREE = 1 };
+enum { ES_DTYPE_F32 = 0, ES_DTYPE_BF16 = 1 };
+
+/* Sensitivity variants.  Zero-initialised = the defaults
+ * every non-_ex entry point uses.
+ *   prime        : P' of Eq. 2 (L1064-1067); 0 means 577 (L1058).  Any value >= 1 is accepted
+ *                  (the bijection property needs gcd(P', d_i) = 1).
+ *   mean_divisor : ES_MEAN_BY_SAMPLED divides MEAN by k_i (reading R5, default) or
+ *                  ES_MEAN_BY_DEGREE by the original d_i (the other reading of L1571).
+ *   b_dtype      : ES_DTYPE_F32, or ES_DTYPE_BF16: B holds bf16 values (2 bytes; rows 16-B
+ *                  aligned, ldb % 8 == 0, F <= 2048, else ES_ERR_UNSUPPORTED); the arithmetic
+ *                  stays fp32 (exact widening, fp32 FMA) -- only the storage of B changes. */
+typedef struct {
+    int32_t struct_size;   /* sizeof(es_spmm_options_t) (forward compatibility) */
+    int32_t prime;
+    int32_t mean_divisor;
+    int32_t b_dtype;
+} es_spmm_options_t;
 
 /* Edge sampling materialised (stage 1 of Alg. 1; the paper's "pre-sampled graph",
  * §5.6).
@@ -109,6 +127,22 @@ es_status_t es_spmm_run_rows(int64_t n_rows, int64_t n_cols,
                              float* C /*[dev]*/, int64_t ldc,
                              int64_t row_begin, int64_t row_end, void* stream);
 
+/* es_spmm_run_rows with options (NULL = defaults).  B is `const void*` typed by opt->b_dtype. */
+es_status_t es_spmm_run_ex(int64_t n_rows, int64_t n_cols,
+                           const int64_t* rowptr /*[dev]*/, int64_t nnz_base,
+                           const int32_t* colind /*[dev]*/, const float* val /*[dev] or NULL*/,
+                           const void* B /*[dev]*/, int64_t F, int64_t ldb,
+                           int32_t s, int32_t strategy, uint64_t seed, int32_t reduce,
+                           float* C /*[dev]*/, int64_t ldc, int64_t row_begin, int64_t row_end,
+                           const es_spmm_options_t* opt, void* stream);
+
+/* es_spmm_sample with options (only `prime` applies; NULL = defaults). */
+es_status_t es_spmm_sample_ex(int64_t n_rows, int64_t n_cols,
+                              const int64_t* rowptr, const int32_t* colind, const float* val,
+                              int32_t s, int32_t strategy, uint64_t seed, int64_t row_base,
+                              int64_t* s_rowptr, int32_t* s_colind, float* s_val, int64_t* s_pos,
+                              const es_spmm_options_t* opt, void* stream);
+
 /* Backward w.r.t. B of es_spmm_run_rows (training variant; the paper leaves training with
  * dynamic sampling to future work, §6.2):
  *   dB[col_ij, 0:F] += w_ij * dC[i, 0:F]  over the SAME sampled slots (same s, strategy, seed),
@@ -125,6 +159,15 @@ es_status_t es_spmm_backward(int64_t n_rows, int64_t n_cols,
                              int32_t s, int32_t strategy, uint64_t seed, int32_t reduce,
                              float* dB /*[dev] n_cols x ldb*/, int64_t ldb,
                              int64_t row_begin, int64_t row_end, void* stream);
+
+/* es_spmm_backward with options (prime, mean_divisor; b_dtype must be ES_DTYPE_F32). */
+es_status_t es_spmm_backward_ex(int64_t n_rows, int64_t n_cols,
+                                const int64_t* rowptr, int64_t nnz_base,
+                                const int32_t* colind, const float* val,
+                                const float* dC, int64_t F, int64_t ldc,
+                                int32_t s, int32_t strategy, uint64_t seed, int32_t reduce,
+                                float* dB, int64_t ldb, int64_t row_begin, int64_t row_end,
+                                const es_spmm_options_t* opt, void* stream);
 
 /* End-to-end variant with HOST inputs and output (the call a user with host data makes):
  * copies rowptr/colind/val/B host->device, runs the fused kernel and copies C back,

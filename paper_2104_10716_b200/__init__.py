@@ -16,11 +16,13 @@ import numpy as np
 ES_OK, ES_ERR_INVALID_VALUE, ES_ERR_MISALIGNED, ES_ERR_UNSUPPORTED, ES_ERR_CUDA = 0, 1, 2, 3, 4
 ES_BUCKET, ES_FASTRAND = 1, 2
 ES_REDUCE_SUM, ES_REDUCE_MEAN = 0, 1
+ES_MEAN_BY_SAMPLED, ES_MEAN_BY_DEGREE = 0, 1
+ES_DTYPE_F32, ES_DTYPE_BF16 = 0, 1
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libesspmm.so")
 EXPORTS = ("es_spmm_sample", "es_spmm_run", "es_spmm_run_rows", "es_spmm_backward",
-           "es_spmm_host_workspace_bytes",
+           "es_spmm_run_ex", "es_spmm_sample_ex", "es_spmm_backward_ex", "es_spmm_host_workspace_bytes",
            "es_spmm_run_host", "es_partition_rows", "es_spmm_plan", "es_launch_count",
            "es_status_string")
 
@@ -29,6 +31,17 @@ _lib = None
 
 class EsError(RuntimeError):
     pass
+
+
+class EsOptions(ctypes.Structure):
+    """es_spmm_options_t (include/es_spmm.h): NEXT-4 sensitivity variants."""
+    _fields_ = [("struct_size", ctypes.c_int32), ("prime", ctypes.c_int32),
+                ("mean_divisor", ctypes.c_int32), ("b_dtype", ctypes.c_int32)]
+
+    @classmethod
+    def make(cls, prime: int = 0, mean_by_degree: bool = False, bf16: bool = False):
+        return cls(ctypes.sizeof(cls), prime, ES_MEAN_BY_DEGREE if mean_by_degree else ES_MEAN_BY_SAMPLED,
+                   ES_DTYPE_BF16 if bf16 else ES_DTYPE_F32)
 
 
 def load_library(path: str = LIB_PATH):
@@ -55,6 +68,15 @@ def load_library(path: str = LIB_PATH):
     lib.es_spmm_backward.restype = st
     lib.es_spmm_backward.argtypes = [i64, i64, vp, i64, vp, vp, vp, i64, i64, i32, i32, u64, i32, vp, i64,
                                      i64, i64, vp]
+    op = ctypes.POINTER(EsOptions)
+    lib.es_spmm_run_ex.restype = st
+    lib.es_spmm_run_ex.argtypes = [i64, i64, vp, i64, vp, vp, vp, i64, i64, i32, i32, u64, i32, vp, i64,
+                                   i64, i64, op, vp]
+    lib.es_spmm_sample_ex.restype = st
+    lib.es_spmm_sample_ex.argtypes = [i64, i64, vp, vp, vp, i32, i32, u64, i64, vp, vp, vp, vp, op, vp]
+    lib.es_spmm_backward_ex.restype = st
+    lib.es_spmm_backward_ex.argtypes = [i64, i64, vp, i64, vp, vp, vp, i64, i64, i32, i32, u64, i32, vp,
+                                        i64, i64, i64, op, vp]
     lib.es_spmm_host_workspace_bytes.restype = i64
     lib.es_spmm_host_workspace_bytes.argtypes = [i64, i64, i64, i64, i64, i32]
     lib.es_spmm_run_host.restype = st
@@ -182,6 +204,80 @@ def es_spmm_run_rows(n_rows: int, rowptr_slice, nnz_base: int, colind_slice, val
                                            strategy, seed & (2**64 - 1), reduce, _ptr(C), C.stride(0),
                                            row_begin, row_end, _stream(stream)), "es_spmm_run_rows")
     return C
+
+
+def es_spmm_run_ex(rowptr, colind, val, B, s: int, strategy: int, seed: int = 0,
+                   reduce: int = ES_REDUCE_SUM, F: int | None = None, C=None, prime: int = 0,
+                   mean_by_degree: bool = False, row_begin: int = 0, row_end: int | None = None,
+                   n_rows: int | None = None, nnz_base: int = 0, stream=None):
+    """es_spmm_run_rows with the NEXT-4 options: P' override, MEAN by original degree, and bf16
+    storage of B (pass a torch.bfloat16 B; accumulation stays fp32)."""
+    import torch
+    _dev(rowptr, torch.int64, "rowptr")
+    _dev(colind, torch.int32, "colind")
+    _dev(val, torch.float32, "val")
+    if not (isinstance(B, torch.Tensor) and B.is_cuda and B.dim() == 2 and B.is_contiguous()):
+        raise EsError("B must be a contiguous 2-D CUDA tensor")
+    if B.dtype not in (torch.float32, torch.bfloat16):
+        raise EsError("B must be float32 or bfloat16")
+    ldb = B.shape[1]
+    F = ldb if F is None else F
+    if row_end is None:
+        row_end = row_begin + rowptr.numel() - 1
+    if n_rows is None:
+        n_rows = row_end
+    if C is None:
+        C = torch.empty((row_end - row_begin, F), dtype=torch.float32, device=B.device)
+    opt = EsOptions.make(prime, mean_by_degree, B.dtype == torch.bfloat16)
+    _check(load_library().es_spmm_run_ex(n_rows, B.shape[0], _ptr(rowptr), nnz_base, _ptr(colind), _ptr(val),
+                                         _ptr(B), F, ldb, s, strategy, seed & (2**64 - 1), reduce, _ptr(C),
+                                         C.stride(0), row_begin, row_end, ctypes.byref(opt), _stream(stream)),
+           "es_spmm_run_ex")
+    return C
+
+
+def es_spmm_sample_ex(rowptr, colind, val, s: int, strategy: int, seed: int = 0, row_base: int = 0,
+                      prime: int = 0, stream=None):
+    """es_spmm_sample with a P' override; returns (s_rowptr, s_colind, s_val, s_pos)."""
+    import torch
+    lib = load_library()
+    _dev(rowptr, torch.int64, "rowptr")
+    _dev(colind, torch.int32, "colind")
+    _dev(val, torch.float32, "val")
+    opt = EsOptions.make(prime)
+    n = rowptr.numel() - 1
+    dev = rowptr.device
+    s_rowptr = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    st = _stream(stream)
+    _check(lib.es_spmm_sample_ex(n, 0, _ptr(rowptr), _ptr(colind), _ptr(val), s, strategy, seed & (2**64 - 1),
+                                 row_base, _ptr(s_rowptr), None, None, None, ctypes.byref(opt), st),
+           "es_spmm_sample_ex(count)")
+    K = int(s_rowptr[-1].item())
+    s_colind = torch.empty(K, dtype=torch.int32, device=dev)
+    s_val = torch.empty(K, dtype=torch.float32, device=dev)
+    s_pos = torch.empty(K, dtype=torch.int64, device=dev)
+    if K > 0:
+        _check(lib.es_spmm_sample_ex(n, 0, _ptr(rowptr), _ptr(colind), _ptr(val), s, strategy,
+                                     seed & (2**64 - 1), row_base, _ptr(s_rowptr), _ptr(s_colind), _ptr(s_val),
+                                     _ptr(s_pos), ctypes.byref(opt), st), "es_spmm_sample_ex(materialize)")
+    return s_rowptr, s_colind, s_val, s_pos
+
+
+def es_spmm_backward_ex(rowptr, colind, val, dC, n_cols: int, s: int, strategy: int, seed: int = 0,
+                        reduce: int = ES_REDUCE_SUM, prime: int = 0, mean_by_degree: bool = False,
+                        F: int | None = None, dB=None, stream=None):
+    """Backward with the P' / MEAN-divisor options (full CSR)."""
+    import torch
+    F = dC.shape[1] if F is None else F
+    if dB is None:
+        dB = torch.zeros((n_cols, F), dtype=torch.float32, device=dC.device)
+    n = rowptr.numel() - 1
+    opt = EsOptions.make(prime, mean_by_degree)
+    _check(load_library().es_spmm_backward_ex(n, n_cols, _ptr(rowptr), 0, _ptr(colind), _ptr(val), _ptr(dC), F,
+                                              dC.stride(0), s, strategy, seed & (2**64 - 1), reduce, _ptr(dB),
+                                              dB.stride(0), 0, n, ctypes.byref(opt), _stream(stream)),
+           "es_spmm_backward_ex")
+    return dB
 
 
 def es_spmm_backward(rowptr, colind, val, dC, n_cols: int, s: int, strategy: int, seed: int = 0,

@@ -31,6 +31,41 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def _check_no_spills(ptxas_log: str, src: str) -> None:
+    """cp.async ring kernels that spill registers trapped with cudaErrorIllegalInstruction on
+    B200 (profiles/r01.md); refuse to build one."""
+    entry = None
+    for line in ptxas_log.splitlines():
+        if "Compiling entry function" in line:
+            entry = line.split("'")[1] if "'" in line else line
+        elif "spill stores" in line and entry and "spmm_cpasync" in entry:
+            stores = int(line.split("bytes spill stores")[0].split(",")[-1].strip().split()[0])
+            if stores:
+                raise RuntimeError(f"{src}: {entry} spills ({line.strip()}); lower its MINB")
+
+
+def _check_sass(lib: str) -> None:
+    """Reject a library whose SASS uses a 64-bit memory descriptor in an odd (misaligned)
+    uniform register pair, e.g. `desc[UR1]`: ptxas 12.9 emitted that for a cache-hinted
+    cp.async under register pressure and it traps (cudaErrorIllegalInstruction) on B200."""
+    import re
+    cuobjdump = os.path.join(os.path.dirname(NVCC), "cuobjdump")
+    res = subprocess.run([cuobjdump, "-sass", lib], capture_output=True, text=True)
+    if res.returncode != 0:
+        return                                   # no disassembler: nothing to check
+    fn = None
+    bad = []
+    for line in res.stdout.splitlines():
+        if "Function : " in line:
+            fn = line.split("Function : ")[1].strip()
+        for m in re.finditer(r"desc\[UR(\d+)\]", line):
+            if int(m.group(1)) % 2:
+                bad.append((fn, line.strip()))
+    if bad:
+        raise RuntimeError("misaligned 64-bit uniform descriptor in SASS (illegal instruction on B200): "
+                           + "; ".join(f"{f}: {l}" for f, l in bad[:3]))
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
@@ -45,6 +80,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             raise RuntimeError(f"nvcc failed on {src}")
         if verbose:
             sys.stderr.write(res.stderr)
+        _check_no_spills(res.stderr, src)
         objs.append(obj)
     tmp = LIB + ".tmp"
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs,
@@ -53,6 +89,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc link failed")
+    _check_sass(tmp)
     os.replace(tmp, LIB)
     for o in objs:
         os.remove(o)

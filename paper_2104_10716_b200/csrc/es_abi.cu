@@ -26,11 +26,30 @@ es_status_t check_common(int64_t n_rows, int64_t n_cols, int64_t F, int64_t ldb,
     return ES_OK;
 }
 
+struct Opts {
+    uint32_t prime = 577;
+    int32_t mean_by_degree = 0;
+    int32_t bf16 = 0;
+};
+
+es_status_t read_opts(const es_spmm_options_t* o, Opts* out) {
+    *out = Opts{};
+    if (!o) return ES_OK;
+    if (o->struct_size < (int32_t)sizeof(es_spmm_options_t)) return ES_ERR_INVALID_VALUE;
+    if (o->prime < 0) return ES_ERR_INVALID_VALUE;
+    if (o->mean_divisor != ES_MEAN_BY_SAMPLED && o->mean_divisor != ES_MEAN_BY_DEGREE) return ES_ERR_INVALID_VALUE;
+    if (o->b_dtype != ES_DTYPE_F32 && o->b_dtype != ES_DTYPE_BF16) return ES_ERR_INVALID_VALUE;
+    out->prime = o->prime == 0 ? 577u : (uint32_t)o->prime;
+    out->mean_by_degree = o->mean_divisor == ES_MEAN_BY_DEGREE;
+    out->bf16 = o->b_dtype == ES_DTYPE_BF16;
+    return ES_OK;
+}
+
 es_status_t run_rows_impl(int64_t n_rows, int64_t n_cols, const int64_t* rowptr, int64_t nnz_base,
-                          const int32_t* colind, const float* val, const float* B, int64_t F,
+                          const int32_t* colind, const float* val, const void* B, int64_t F,
                           int64_t ldb, int32_t s, int32_t strategy, uint64_t seed, int32_t reduce,
                           float* C, int64_t ldc, int64_t row_begin, int64_t row_end,
-                          cudaStream_t st) {
+                          const Opts& o, cudaStream_t st) {
     es_status_t rc = check_common(n_rows, n_cols, F, ldb, ldc, s, strategy, reduce);
     if (rc != ES_OK) return rc;
     if (row_begin < 0 || row_end < row_begin || row_end > n_rows) return ES_ERR_INVALID_VALUE;
@@ -42,7 +61,7 @@ es_status_t run_rows_impl(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
     p.nnz_base = nnz_base;
     p.colind = colind;
     p.val = val;
-    p.B = B;
+    p.B = static_cast<const float*>(B);
     p.F = F;
     p.ldb = ldb;
     p.s = s;
@@ -53,7 +72,11 @@ es_status_t run_rows_impl(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
     p.ldc = ldc;
     p.n_rows = n;
     p.row_base = row_begin;
-    const es::Plan plan = es::make_plan(F, ldb, ldc, B, C);
+    p.prime = o.prime;
+    p.mean_by_degree = o.mean_by_degree;
+    p.b_bf16 = o.bf16;
+    const es::Plan plan = o.bf16 ? es::make_plan_bf16(F, ldb, ldc, B, C) : es::make_plan(F, ldb, ldc, B, C);
+    if (plan.unsupported) return ES_ERR_UNSUPPORTED;
     cudaError_t err = es::launch_spmm(p, plan, st);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return err == cudaSuccess ? ES_OK : ES_ERR_CUDA;
@@ -96,6 +119,16 @@ es_status_t es_spmm_sample(int64_t n_rows, int64_t n_cols, const int64_t* rowptr
                            const int32_t* colind, const float* val, int32_t s, int32_t strategy,
                            uint64_t seed, int64_t row_base, int64_t* s_rowptr, int32_t* s_colind,
                            float* s_val, int64_t* s_pos, void* stream) {
+    return es_spmm_sample_ex(n_rows, n_cols, rowptr, colind, val, s, strategy, seed, row_base, s_rowptr,
+                             s_colind, s_val, s_pos, nullptr, stream);
+}
+
+es_status_t es_spmm_sample_ex(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
+                              const int32_t* colind, const float* val, int32_t s, int32_t strategy,
+                              uint64_t seed, int64_t row_base, int64_t* s_rowptr, int32_t* s_colind,
+                              float* s_val, int64_t* s_pos, const es_spmm_options_t* opt, void* stream) {
+    Opts o;
+    if (read_opts(opt, &o) != ES_OK) return ES_ERR_INVALID_VALUE;
     if (n_rows < 0 || n_cols < 0 || s < 1 || row_base < 0) return ES_ERR_INVALID_VALUE;
     if (strategy != ES_BUCKET && strategy != ES_FASTRAND) return ES_ERR_INVALID_VALUE;
     if (!rowptr || !s_rowptr) return ES_ERR_INVALID_VALUE;
@@ -107,7 +140,7 @@ es_status_t es_spmm_sample(int64_t n_rows, int64_t n_cols, const int64_t* rowptr
     if (!s_colind || n_rows == 0) return ES_OK;
     // nnz_base: colind/val are indexed with the absolute rowptr entries.
     err = es::launch_sample_materialize(rowptr, 0, colind, val, n_rows, s, strategy, seed, row_base,
-                                        s_rowptr, s_colind, s_val, s_pos, st);
+                                        o.prime, s_rowptr, s_colind, s_val, s_pos, st);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return err == cudaSuccess ? ES_OK : ES_ERR_CUDA;
 }
@@ -117,7 +150,7 @@ es_status_t es_spmm_run(int64_t n_rows, int64_t n_cols, const int64_t* rowptr, c
                         int32_t strategy, uint64_t seed, int32_t reduce, float* C, int64_t ldc,
                         void* stream) {
     return run_rows_impl(n_rows, n_cols, rowptr, 0, colind, val, B, F, ldb, s, strategy, seed, reduce,
-                         C, ldc, 0, n_rows, as_stream(stream));
+                         C, ldc, 0, n_rows, Opts{}, as_stream(stream));
 }
 
 es_status_t es_spmm_run_rows(int64_t n_rows, int64_t n_cols, const int64_t* rowptr, int64_t nnz_base,
@@ -125,13 +158,36 @@ es_status_t es_spmm_run_rows(int64_t n_rows, int64_t n_cols, const int64_t* rowp
                              int64_t ldb, int32_t s, int32_t strategy, uint64_t seed, int32_t reduce,
                              float* C, int64_t ldc, int64_t row_begin, int64_t row_end, void* stream) {
     return run_rows_impl(n_rows, n_cols, rowptr, nnz_base, colind, val, B, F, ldb, s, strategy, seed,
-                         reduce, C, ldc, row_begin, row_end, as_stream(stream));
+                         reduce, C, ldc, row_begin, row_end, Opts{}, as_stream(stream));
+}
+
+es_status_t es_spmm_run_ex(int64_t n_rows, int64_t n_cols, const int64_t* rowptr, int64_t nnz_base,
+                           const int32_t* colind, const float* val, const void* B, int64_t F,
+                           int64_t ldb, int32_t s, int32_t strategy, uint64_t seed, int32_t reduce,
+                           float* C, int64_t ldc, int64_t row_begin, int64_t row_end,
+                           const es_spmm_options_t* opt, void* stream) {
+    Opts o;
+    if (read_opts(opt, &o) != ES_OK) return ES_ERR_INVALID_VALUE;
+    return run_rows_impl(n_rows, n_cols, rowptr, nnz_base, colind, val, B, F, ldb, s, strategy, seed,
+                         reduce, C, ldc, row_begin, row_end, o, as_stream(stream));
 }
 
 es_status_t es_spmm_backward(int64_t n_rows, int64_t n_cols, const int64_t* rowptr, int64_t nnz_base,
                              const int32_t* colind, const float* val, const float* dC, int64_t F,
                              int64_t ldc, int32_t s, int32_t strategy, uint64_t seed, int32_t reduce,
                              float* dB, int64_t ldb, int64_t row_begin, int64_t row_end, void* stream) {
+    return es_spmm_backward_ex(n_rows, n_cols, rowptr, nnz_base, colind, val, dC, F, ldc, s, strategy, seed,
+                               reduce, dB, ldb, row_begin, row_end, nullptr, stream);
+}
+
+es_status_t es_spmm_backward_ex(int64_t n_rows, int64_t n_cols, const int64_t* rowptr, int64_t nnz_base,
+                                const int32_t* colind, const float* val, const float* dC, int64_t F,
+                                int64_t ldc, int32_t s, int32_t strategy, uint64_t seed, int32_t reduce,
+                                float* dB, int64_t ldb, int64_t row_begin, int64_t row_end,
+                                const es_spmm_options_t* opt, void* stream) {
+    Opts o;
+    if (read_opts(opt, &o) != ES_OK) return ES_ERR_INVALID_VALUE;
+    if (o.bf16) return ES_ERR_UNSUPPORTED;
     es_status_t rc = check_common(n_rows, n_cols, F, ldb, ldc, s, strategy, reduce);
     if (rc != ES_OK) return rc;
     if (row_begin < 0 || row_end < row_begin || row_end > n_rows) return ES_ERR_INVALID_VALUE;
@@ -154,6 +210,8 @@ es_status_t es_spmm_backward(int64_t n_rows, int64_t n_cols, const int64_t* rowp
     p.ldb = ldb;
     p.n_rows = n;
     p.row_base = row_begin;
+    p.prime = o.prime;
+    p.mean_by_degree = o.mean_by_degree;
     const uintptr_t a = reinterpret_cast<uintptr_t>(dC), b = reinterpret_cast<uintptr_t>(dB);
     if (a % 16 == 0 && b % 16 == 0 && ldc % 4 == 0 && ldb % 4 == 0) p.vec = 4;
     else if (a % 8 == 0 && b % 8 == 0 && ldc % 2 == 0 && ldb % 2 == 0) p.vec = 2;
@@ -268,7 +326,7 @@ es_status_t es_spmm_run_host(int64_t n_rows, int64_t n_cols, const int64_t* rowp
                 goto cleanup;
             rc = run_rows_impl(row_base + n_rows, n_cols, d_rowptr + r0, base, d_colind, d_val, d_B, F,
                                ldb, s, strategy, seed, reduce, d_C + r0 * dldc, dldc, row_base + r0,
-                               row_base + r1, st);
+                               row_base + r1, Opts{}, st);
             if (rc != ES_OK) goto cleanup;
             if (!ok(cudaEventRecord(ev_done[(size_t)c], st)) || !ok(cudaStreamWaitEvent(s_out, ev_done[(size_t)c], 0)))
                 goto cleanup;

@@ -26,26 +26,28 @@ struct RowSampler {
     int32_t k;        // min(d, s)
     int32_t strategy;
     uint64_t off;     // FastRand rotation, 0 for seed == 0
+    uint32_t prime;   // P' (577, L1058; NEXT-4 override)
     bool narrow;      // all positions computable in 32-bit unsigned arithmetic
 
     __device__ __forceinline__ void init(int64_t b, int64_t e, int32_t s, int32_t strat,
-                                         uint64_t seed, int64_t global_row) {
+                                         uint64_t seed, int64_t global_row, uint32_t pp) {
         beg = b;
         d = e - b;
         k = d < (int64_t)s ? (int32_t)d : s;
         strategy = strat;
+        prime = pp;
         off = (strat == kFastRand && seed != 0 && d > 0)
                   ? mix64(seed + kGolden * (uint64_t)(global_row + 1)) % (uint64_t)d : 0;
-        // off < d, j < k <= s: off + j*577 < 2^32 guarantees exact 32-bit arithmetic.
-        narrow = (uint64_t)d + (uint64_t)(k > 0 ? k - 1 : 0) * kPrime < (1ull << 32);
+        // off < d, j < k <= s: off + j*P' < 2^32 guarantees exact 32-bit arithmetic.
+        narrow = (uint64_t)d + (uint64_t)(k > 0 ? k - 1 : 0) * pp < (1ull << 32);
     }
 
     // Position within the row of slot j < k.  Bucket: j (L1043).  FastRand: Eq. 2
-    // (L1066) rotated by off (R6): (off + j*577) mod d.
+    // (L1066) rotated by off (R6): (off + j*P') mod d.
     __device__ __forceinline__ int64_t pos(int32_t j) const {
         if (strategy == kBucket) return j;
-        if (narrow) return (int64_t)(((uint32_t)off + (uint32_t)j * kPrime) % (uint32_t)d);
-        return (int64_t)((off + (uint64_t)j * kPrime) % (uint64_t)d);
+        if (narrow) return (int64_t)(((uint32_t)off + (uint32_t)j * prime) % (uint32_t)d);
+        return (int64_t)((off + (uint64_t)j * prime) % (uint64_t)d);
     }
 };
 
@@ -135,9 +137,13 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 }
 
 // ---- per-thread async copies (cp.async, SASS LDGSTS): global -> shared, 16 B, L2 only
+template <bool kHint = true>
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, uint64_t pol) {
-    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;"
-                 :: "r"(smem_u32(dst)), "l"(src), "l"(pol) : "memory");
+    if constexpr (kHint)
+        asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;"
+                     :: "r"(smem_u32(dst)), "l"(src), "l"(pol) : "memory");
+    else
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(smem_u32(dst)), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>

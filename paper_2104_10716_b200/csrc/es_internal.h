@@ -20,6 +20,9 @@ struct SpmmParams {
     int64_t ldc;
     int64_t n_rows;          // rows in this launch
     int64_t row_base;        // global id of local row 0 (seeded FastRand offset)
+    uint32_t prime;          // P' (577 unless overridden, NEXT-4)
+    int32_t mean_by_degree;  // MEAN divides by d_i instead of k_i (NEXT-4)
+    int32_t b_bf16;          // B stored as bf16 (fp32 accumulation, NEXT-4)
 };
 
 struct Plan {
@@ -30,6 +33,8 @@ struct Plan {
     bool c_vec;
     bool tma;          // TMA-ring kernel (spmm_tma)
     bool cpasync;      // cp.async ring kernel (spmm_cpasync)
+    bool bf16;         // B stored as bf16 (cp.async ring only)
+    bool unsupported;  // no kernel for this layout (bf16 with misaligned rows)
     int stages;         // ring depth (tma)
     int rows_per_warp;  // consecutive rows per warp (tma)
     int minb;           // __launch_bounds__ min blocks per SM (tma register cap)
@@ -51,17 +56,21 @@ struct BwdParams {
     int64_t ldb;
     int64_t n_rows, row_base;
     int32_t vec;             // 4, 2, 1 (alignment of dC, dB, ldc, ldb)
+    uint32_t prime;
+    int32_t mean_by_degree;
 };
 
 cudaError_t launch_backward(const BwdParams& p, cudaStream_t st);
 
 Plan make_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C);
+Plan make_plan_bf16(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C);
 cudaError_t launch_spmm(SpmmParams p, const Plan& plan, cudaStream_t st);
 cudaError_t launch_sample_count(const int64_t* rowptr, int64_t n, int32_t s, int64_t* s_rowptr,
                                 cudaStream_t st, int* launches);
 cudaError_t launch_sample_materialize(const int64_t* rowptr, int64_t nnz_base, const int32_t* colind,
                                       const float* val, int64_t n, int32_t s, int32_t strategy,
-                                      uint64_t seed, int64_t row_base, const int64_t* s_rowptr,
-                                      int32_t* s_colind, float* s_val, int64_t* s_pos, cudaStream_t st);
+                                      uint64_t seed, int64_t row_base, uint32_t prime,
+                                      const int64_t* s_rowptr, int32_t* s_colind, float* s_val,
+                                      int64_t* s_pos, cudaStream_t st);
 
 }  // namespace es

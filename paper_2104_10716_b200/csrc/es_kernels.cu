@@ -48,9 +48,13 @@ __device__ __forceinline__ void store_out(float* Crow, int64_t vidx, int64_t F, 
     }
 }
 
-__device__ __forceinline__ float finish(float x, int reduce, int32_t k) {
-    if (reduce == kMean) return k > 0 ? __fdiv_rn(x, (float)k) : 0.0f;
+// a5 epilogue: SUM, or MEAN = / div (IEEE) with div = k_i (reading R5) or d_i (NEXT-4 option)
+__device__ __forceinline__ float finish(float x, int reduce, int64_t div) {
+    if (reduce == kMean) return div > 0 ? __fdiv_rn(x, (float)div) : 0.0f;
     return x;
+}
+__device__ __forceinline__ int64_t mean_div(const SpmmParams& p, int64_t d, int32_t k) {
+    return p.mean_by_degree ? d : (int64_t)k;
 }
 
 // ------------------------------------------------------------------ warp per row
@@ -65,7 +69,7 @@ spmm_warp(const SpmmParams p) {
 
     RowSampler rs;
     rs.init(ld_stream(p.rowptr + r, pol_a) - p.nnz_base, ld_stream(p.rowptr + r + 1, pol_a) - p.nnz_base,
-            p.s, p.strategy, p.seed, p.row_base + r);
+            p.s, p.strategy, p.seed, p.row_base + r, p.prime);
     const int64_t NV = (p.F + VEC - 1) / VEC;
     float* Crow = p.C + r * p.ldc;
 
@@ -138,7 +142,7 @@ spmm_warp(const SpmmParams p) {
             if (vidx < NV) {
                 float res[VEC];
 #pragma unroll
-                for (int q = 0; q < VEC; ++q) res[q] = finish(tot[c][q], p.reduce, rs.k);
+                for (int q = 0; q < VEC; ++q) res[q] = finish(tot[c][q], p.reduce, mean_div(p, rs.d, rs.k));
                 store_out<VEC>(Crow, vidx, p.F, res, p.c_vec, pol_a);
             }
         }
@@ -159,7 +163,7 @@ spmm_subwarp(const SpmmParams p) {
 
     RowSampler rs;
     rs.init(ld_stream(p.rowptr + r, pol_a) - p.nnz_base, ld_stream(p.rowptr + r + 1, pol_a) - p.nnz_base,
-            p.s, p.strategy, p.seed, p.row_base + r);
+            p.s, p.strategy, p.seed, p.row_base + r, p.prime);
     const int64_t NV = (p.F + VEC - 1) / VEC;    // <= G
     float acc[VEC], part[VEC];        // acc: sum of per-chunk stream partials
 #pragma unroll
@@ -207,7 +211,7 @@ spmm_subwarp(const SpmmParams p) {
     if (e == 0 && g < NV) {
         float res[VEC];
 #pragma unroll
-        for (int q = 0; q < VEC; ++q) res[q] = finish(acc[q], p.reduce, rs.k);
+        for (int q = 0; q < VEC; ++q) res[q] = finish(acc[q], p.reduce, mean_div(p, rs.d, rs.k));
         store_out<VEC>(p.C + r * p.ldc, g, p.F, res, p.c_vec, pol_a);
     }
 }
@@ -219,10 +223,32 @@ spmm_subwarp(const SpmmParams p) {
 // warp at ~40 registers/thread -> 48 warps/SM for F=128), and since a lane only ever reads
 // what it copied, no warp or CTA synchronisation is needed.  Same per-element order as
 // spmm_warp / spmm_tma (32-slot partials), so results are bitwise interchangeable.
-template <int NCH, int D, int MINB>
+template <typename TB>
+struct Piece;                                   // a 16-B piece of a B row, widened to fp32
+template <> struct Piece<float> {
+    static constexpr int kElems = 4;
+    __device__ __forceinline__ static void widen(const float4& raw, float* out) {
+        out[0] = raw.x; out[1] = raw.y; out[2] = raw.z; out[3] = raw.w;
+    }
+};
+template <> struct Piece<uint16_t> {            // bf16 storage (NEXT-4): exact widening
+    static constexpr int kElems = 8;
+    __device__ __forceinline__ static void widen(const float4& raw, float* out) {
+        const uint32_t w[4] = {__float_as_uint(raw.x), __float_as_uint(raw.y), __float_as_uint(raw.z),
+                               __float_as_uint(raw.w)};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            out[2 * i] = __uint_as_float(w[i] << 16);
+            out[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+        }
+    }
+};
+
+template <typename TB, int NCH, int D, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB)
 spmm_cpasync(const SpmmParams p) {
     static_assert(D >= 1 && D <= 32, "ring depth");
+    constexpr int EPP = Piece<TB>::kElems;                       // B elements per 16-B piece
     extern __shared__ __align__(16) float4 ring_smem[];          // [kWarps][D][NCH*32]
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -232,18 +258,22 @@ spmm_cpasync(const SpmmParams p) {
     const uint64_t pol_b = policy_evict_last();
     RowSampler rs;
     rs.init(ld_stream(p.rowptr + r, pol_a) - p.nnz_base, ld_stream(p.rowptr + r + 1, pol_a) - p.nnz_base,
-            p.s, p.strategy, p.seed, p.row_base + r);
-    const int NV = (int)((p.F + 3) / 4);
+            p.s, p.strategy, p.seed, p.row_base + r, p.prime);
+    const int NV = (int)((p.F + EPP - 1) / EPP);
     const int32_t k = rs.k;
-    constexpr int kStage = NCH * 32;                             // float4 per stage
+    constexpr int kStage = NCH * 32;                             // pieces per stage
     float4* my = ring_smem + (size_t)warp * D * kStage + lane;
-    const float* bl = p.B + lane * 4;
+    const TB* bl = reinterpret_cast<const TB*>(p.B) + lane * EPP;
 
     auto copy_slot = [&](int stage, int32_t c) {
-        const float* src = bl + (int64_t)c * p.ldb;
+        const TB* src = bl + (int64_t)c * p.ldb;
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch)
-            if (lane + 32 * ch < NV) cp_async16(my + stage * kStage + 32 * ch, src + 128 * ch, pol_b);
+            // no L2 hint on the bf16 instantiations: ptxas 12.9 placed their 64-bit policy
+            // descriptor in a misaligned uniform register pair (desc[UR1]) -> illegal
+            // instruction on B200 (_build.py now scans the SASS for that pattern)
+            if (lane + 32 * ch < NV)
+                cp_async16<sizeof(TB) == 4>(my + stage * kStage + 32 * ch, src + 32 * EPP * ch, pol_b);
     };
 
     // (col, val) of the chunk holding the consumer slot (c0, a0) and of the next chunk (c1, a1)
@@ -266,11 +296,11 @@ spmm_cpasync(const SpmmParams p) {
         if (t < k) copy_slot(t, c);
         cp_async_commit();
     }
-    float part[NCH][4], tot[NCH][4];
+    float part[NCH][EPP], tot[NCH][EPP];
 #pragma unroll
     for (int ch = 0; ch < NCH; ++ch)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) { part[ch][q] = 0.0f; tot[ch][q] = 0.0f; }
+        for (int q = 0; q < EPP; ++q) { part[ch][q] = 0.0f; tot[ch][q] = 0.0f; }
     for (int32_t j0 = 0; j0 < k; j0 += 32) {
         const int n_here = min(32, k - j0);
 #pragma unroll 4
@@ -282,11 +312,10 @@ spmm_cpasync(const SpmmParams p) {
 #pragma unroll
             for (int ch = 0; ch < NCH; ++ch) {
                 if (lane + 32 * ch < NV) {
-                    const float4 x = my[st * kStage + 32 * ch];
-                    part[ch][0] = fmaf(av, x.x, part[ch][0]);
-                    part[ch][1] = fmaf(av, x.y, part[ch][1]);
-                    part[ch][2] = fmaf(av, x.z, part[ch][2]);
-                    part[ch][3] = fmaf(av, x.w, part[ch][3]);
+                    float x[EPP];
+                    Piece<TB>::widen(my[st * kStage + 32 * ch], x);
+#pragma unroll
+                    for (int q = 0; q < EPP; ++q) part[ch][q] = fmaf(av, x[q], part[ch][q]);
                 }
             }
             // refill this stage with slot j0 + u + D (current chunk or the next)
@@ -299,7 +328,7 @@ spmm_cpasync(const SpmmParams p) {
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch)
 #pragma unroll
-            for (int q = 0; q < 4; ++q) { tot[ch][q] += part[ch][q]; part[ch][q] = 0.0f; }
+            for (int q = 0; q < EPP; ++q) { tot[ch][q] += part[ch][q]; part[ch][q] = 0.0f; }
         // advance the chunk window; the chunk after next is requested now (used >= 32 - D slots later)
         c0 = c1;
         a0 = a1;
@@ -312,13 +341,21 @@ spmm_cpasync(const SpmmParams p) {
         }
     }
     cp_async_wait<0>();
+    // d_i re-read here (L2 hit) instead of kept live through the loop: the loop's register
+    // budget decides the occupancy (and spilling cp.async kernels trapped on B200, _build.py)
+    int64_t div = k;
+    if (p.reduce == kMean && p.mean_by_degree)
+        div = ld_stream(p.rowptr + r + 1, pol_a) - ld_stream(p.rowptr + r, pol_a);
 #pragma unroll
     for (int ch = 0; ch < NCH; ++ch) {
         if (lane + 32 * ch < NV) {
-            float res[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) res[q] = finish(tot[ch][q], p.reduce, k);
-            store_out<4>(p.C + r * p.ldc, lane + 32 * ch, p.F, res, p.c_vec, pol_a);
+            for (int h = 0; h < EPP / 4; ++h) {
+                float res[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) res[q] = finish(tot[ch][4 * h + q], p.reduce, div);
+                store_out<4>(p.C + r * p.ldc, (int64_t)(lane + 32 * ch) * (EPP / 4) + h, p.F, res, p.c_vec, pol_a);
+            }
         }
     }
 }
@@ -347,7 +384,7 @@ struct WarpStream {
         if (lane < nr) {
             rs.init(ld_stream(p.rowptr + r_begin + lane, pol) - p.nnz_base,
                     ld_stream(p.rowptr + r_begin + lane + 1, pol) - p.nnz_base,
-                    p.s, p.strategy, p.seed, p.row_base + r_begin + lane);
+                    p.s, p.strategy, p.seed, p.row_base + r_begin + lane, p.prime);
             kk = rs.k;
         }
         incl = kk;
@@ -381,8 +418,8 @@ struct WarpStream {
         if (t < T) {
             int64_t pos;
             if (p.strategy == kBucket) pos = j;
-            else if (narrow) pos = (int64_t)(((uint32_t)off + (uint32_t)j * kPrime) % (uint32_t)d);
-            else pos = (int64_t)((off + (uint64_t)j * kPrime) % (uint64_t)d);
+            else if (narrow) pos = (int64_t)(((uint32_t)off + (uint32_t)j * p.prime) % (uint32_t)d);
+            else pos = (int64_t)((off + (uint64_t)j * p.prime) % (uint64_t)d);
             col = ld_stream(p.colind + beg + pos, pol);
             a = p.val ? ld_stream(p.val + beg + pos, pol) : 1.0f;
         }
@@ -424,7 +461,7 @@ struct RowAcc {
             for (int q = 0; q < VEC; ++q) { tot[c][q] += part[c][q]; part[c][q] = 0.0f; }
     }
     __device__ __forceinline__ void store(const SpmmParams& p, int64_t row, int lane, int64_t NV,
-                                          int32_t k, uint64_t pol) {
+                                          int64_t div, uint64_t pol) {
         float* Crow = p.C + row * p.ldc;
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
@@ -432,7 +469,7 @@ struct RowAcc {
             if (vidx < NV) {
                 float res[VEC];
 #pragma unroll
-                for (int q = 0; q < VEC; ++q) res[q] = finish(tot[c][q] + part[c][q], p.reduce, k);
+                for (int q = 0; q < VEC; ++q) res[q] = finish(tot[c][q] + part[c][q], p.reduce, div);
                 store_out<VEC>(Crow, vidx, p.F, res, p.c_vec, pol);
             }
         }
@@ -518,7 +555,7 @@ spmm_tma(const SpmmParams p, int R) {
             __syncwarp();
             issue();                                           // refill the stage just released
         }
-        acc.store(p, r_begin + i, lane, NV, k, pol_a);
+        acc.store(p, r_begin + i, lane, NV, mean_div(p, __shfl_sync(kFull, ws.rs.d, i), k), pol_a);
     }
 }
 
@@ -537,7 +574,7 @@ spmm_bwd_warp(const BwdParams p) {
     const uint64_t pol_a = policy_evict_first();
     RowSampler rs;
     rs.init(ld_stream(p.rowptr + r, pol_a) - p.nnz_base, ld_stream(p.rowptr + r + 1, pol_a) - p.nnz_base,
-            p.s, p.strategy, p.seed, p.row_base + r);
+            p.s, p.strategy, p.seed, p.row_base + r, p.prime);
     if (rs.k == 0) return;
     const int64_t NV = (p.F + VEC - 1) / VEC;
     const float* dCrow = p.dC + r * p.ldc;
@@ -550,7 +587,7 @@ spmm_bwd_warp(const BwdParams p) {
             for (int q = 0; q < VEC; ++q) {
                 const int64_t col = vidx * VEC + q;
                 float v = (vidx < NV && col < p.F) ? ld_stream(dCrow + col, pol_a) : 0.0f;
-                x[c][q] = p.reduce == kMean ? __fdiv_rn(v, (float)rs.k) : v;
+                x[c][q] = p.reduce == kMean ? __fdiv_rn(v, (float)(p.mean_by_degree ? rs.d : (int64_t)rs.k)) : v;
             }
         }
         for (int32_t j0 = 0; j0 < rs.k; j0 += 32) {
@@ -623,14 +660,14 @@ __global__ void sample_count(const int64_t* __restrict__ rowptr, int64_t n, int3
 __global__ void __launch_bounds__(kThreads)
 sample_materialize(const int64_t* __restrict__ rowptr, int64_t nnz_base,
                    const int32_t* __restrict__ colind, const float* __restrict__ val, int64_t n,
-                   int32_t s, int32_t strategy, uint64_t seed, int64_t row_base,
+                   int32_t s, int32_t strategy, uint64_t seed, int64_t row_base, uint32_t prime,
                    const int64_t* __restrict__ s_rowptr, int32_t* __restrict__ s_colind,
                    float* __restrict__ s_val, int64_t* __restrict__ s_pos) {
     const int lane = threadIdx.x & 31;
     const int64_t r = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
     if (r >= n) return;
     RowSampler rs;
-    rs.init(rowptr[r] - nnz_base, rowptr[r + 1] - nnz_base, s, strategy, seed, row_base + r);
+    rs.init(rowptr[r] - nnz_base, rowptr[r + 1] - nnz_base, s, strategy, seed, row_base + r, prime);
     const int64_t o0 = s_rowptr[r];
     for (int32_t j = lane; j < rs.k; j += 32) {
         const int64_t pj = rs.pos(j);
@@ -644,10 +681,10 @@ sample_materialize(const int64_t* __restrict__ rowptr, int64_t nnz_base,
 // ------------------------------------------------------------------ host launchers
 namespace {
 
-template <int NCH, int D, int MINB>
+template <int NCH, int D, int MINB, typename TB = float>
 cudaError_t launch_cpasync_k(const SpmmParams& p, cudaStream_t st) {
     const int64_t blocks = (p.n_rows + kWarps - 1) / kWarps;
-    auto k = spmm_cpasync<NCH, D, MINB>;
+    auto k = spmm_cpasync<TB, NCH, D, MINB>;
     const size_t smem = (size_t)kWarps * D * NCH * 32 * 16;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -657,16 +694,28 @@ cudaError_t launch_cpasync_k(const SpmmParams& p, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+cudaError_t launch_cpasync_bf16(const SpmmParams& p, const Plan& plan, cudaStream_t st) {
+    switch (plan.nch) {
+        case 1: return launch_cpasync_k<1, 4, 5, uint16_t>(p, st);
+        case 2: return launch_cpasync_k<2, 4, 1, uint16_t>(p, st);
+        case 3: return launch_cpasync_k<3, 4, 1, uint16_t>(p, st);
+        case 4: return launch_cpasync_k<4, 4, 1, uint16_t>(p, st);
+        default: return launch_cpasync_k<8, 4, 1, uint16_t>(p, st);
+    }
+}
+
 cudaError_t launch_cpasync(const SpmmParams& p, const Plan& plan, cudaStream_t st) {
-    // (MINB = 8 -- 32 registers -- made ptxas emit code that traps with an illegal instruction
-    //  on B200; 6 is the tested ceiling)
+    if (plan.bf16) return launch_cpasync_bf16(p, plan, st);
+    // Register caps that force spills made this kernel trap with cudaErrorIllegalInstruction on
+    // B200 (MINB 8 for f32, 6 for bf16; profiles/r01.md) -- _build.py rejects any spilling
+    // spmm_cpasync instantiation, so MINB 5 (48 registers, 40 warps/SM) is the ceiling.
     if (plan.nch == 1) {
         const bool m4 = plan.minb <= 4;
         switch (plan.stages) {
-            case 2: return m4 ? launch_cpasync_k<1, 2, 4>(p, st) : launch_cpasync_k<1, 2, 6>(p, st);
-            case 3: return m4 ? launch_cpasync_k<1, 3, 4>(p, st) : launch_cpasync_k<1, 3, 6>(p, st);
-            case 8: return m4 ? launch_cpasync_k<1, 8, 4>(p, st) : launch_cpasync_k<1, 8, 6>(p, st);
-            default: return m4 ? launch_cpasync_k<1, 4, 4>(p, st) : launch_cpasync_k<1, 4, 6>(p, st);
+            case 2: return m4 ? launch_cpasync_k<1, 2, 4>(p, st) : launch_cpasync_k<1, 2, 5>(p, st);
+            case 3: return m4 ? launch_cpasync_k<1, 3, 4>(p, st) : launch_cpasync_k<1, 3, 5>(p, st);
+            case 8: return m4 ? launch_cpasync_k<1, 8, 4>(p, st) : launch_cpasync_k<1, 8, 5>(p, st);
+            default: return m4 ? launch_cpasync_k<1, 4, 4>(p, st) : launch_cpasync_k<1, 4, 5>(p, st);
         }
     }
     const bool d2 = plan.stages == 2;
@@ -788,6 +837,22 @@ static int env_int(const char* name, int dflt) {
     return e ? atoi(e) : dflt;
 }
 
+Plan make_plan_bf16(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C) {
+    // bf16 B (NEXT-4): cp.async ring only -- 16-B aligned rows (ldb % 8 == 0), F <= 2048.
+    Plan pl{};
+    const uintptr_t b = reinterpret_cast<uintptr_t>(B), c = reinterpret_cast<uintptr_t>(C);
+    const int64_t nv8 = (F + 7) / 8;
+    if (b % 16 != 0 || ldb % 8 != 0 || nv8 > 32 * 8) { pl.unsupported = true; return pl; }
+    pl.bf16 = true;
+    pl.cpasync = true;
+    pl.vec = 4;
+    const int64_t nch = (nv8 + 31) / 32;
+    pl.nch = nch <= 4 ? (int)nch : 8;
+    pl.stages = 4;
+    pl.c_vec = (c % 16 == 0) && (ldc % 4 == 0);
+    return pl;
+}
+
 Plan make_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C) {
     Plan pl{};
     const uintptr_t b = reinterpret_cast<uintptr_t>(B), c = reinterpret_cast<uintptr_t>(C);
@@ -825,7 +890,7 @@ Plan make_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C
         pl.tma = false;
         pl.nch = (int)((nv4 + 31) / 32);
         pl.stages = env_int("ES_SPMM_STAGES", 4);
-        pl.minb = env_int("ES_SPMM_MINB", pl.nch == 1 ? 6 : 1);
+        pl.minb = env_int("ES_SPMM_MINB", pl.nch == 1 ? 5 : 1);
     }
     if (pl.tma) {
         pl.nch = (int)((nv4 + 31) / 32);
@@ -873,13 +938,14 @@ cudaError_t launch_sample_count(const int64_t* rowptr, int64_t n, int32_t s, int
 
 cudaError_t launch_sample_materialize(const int64_t* rowptr, int64_t nnz_base, const int32_t* colind,
                                       const float* val, int64_t n, int32_t s, int32_t strategy,
-                                      uint64_t seed, int64_t row_base, const int64_t* s_rowptr,
-                                      int32_t* s_colind, float* s_val, int64_t* s_pos, cudaStream_t st) {
+                                      uint64_t seed, int64_t row_base, uint32_t prime,
+                                      const int64_t* s_rowptr, int32_t* s_colind, float* s_val,
+                                      int64_t* s_pos, cudaStream_t st) {
     if (n <= 0) return cudaSuccess;
     const int64_t blocks = (n + kWarps - 1) / kWarps;
     sample_materialize<<<(unsigned)blocks, kThreads, 0, st>>>(rowptr, nnz_base, colind, val, n, s,
-                                                               strategy, seed, row_base, s_rowptr,
-                                                               s_colind, s_val, s_pos);
+                                                               strategy, seed, row_base, prime,
+                                                               s_rowptr, s_colind, s_val, s_pos);
     return cudaGetLastError();
 }
 

@@ -142,3 +142,24 @@ def test_partition_rows(lib, P):
 def test_partition_degenerate(lib):
     assert es.es_partition_rows(np.zeros(1, np.int64), 4, 8, 3).tolist() == [0, 0, 0, 0]
     assert es.es_partition_rows(np.array([0, 5], np.int64), 4, 8, 4).tolist()[-1] == 1
+
+
+def test_options_validation(lib):
+    vp = ctypes.c_void_p
+    dummy = vp(16)
+    Opt = es.EsOptions
+
+    def run(opt, ldb=8, F=8, B=dummy):
+        return lib.es_spmm_run_ex(10, 10, dummy, 0, dummy, None, B, F, ldb, 4, 2, 0, 0, dummy, F, 0, 10,
+                                  ctypes.byref(opt), None)
+
+    assert run(Opt(4, 0, 0, 0)) == es.ES_ERR_INVALID_VALUE                 # struct_size too small
+    assert run(Opt(ctypes.sizeof(Opt), -3, 0, 0)) == es.ES_ERR_INVALID_VALUE
+    assert run(Opt(ctypes.sizeof(Opt), 0, 2, 0)) == es.ES_ERR_INVALID_VALUE
+    assert run(Opt(ctypes.sizeof(Opt), 0, 0, 7)) == es.ES_ERR_INVALID_VALUE
+    # bf16 needs 16-B rows: ldb % 8 != 0 or a misaligned B -> unsupported (decided before launch)
+    assert run(Opt.make(bf16=True), ldb=12, F=12) == es.ES_ERR_UNSUPPORTED
+    assert run(Opt.make(bf16=True), ldb=16, F=16, B=vp(0x1008)) == es.ES_ERR_UNSUPPORTED
+    # backward has no bf16 variant
+    assert lib.es_spmm_backward_ex(10, 10, dummy, 0, dummy, None, dummy, 8, 8, 4, 2, 0, 0, dummy, 8, 0, 10,
+                                   ctypes.byref(Opt.make(bf16=True)), None) == es.ES_ERR_UNSUPPORTED
