@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true", help="warm-L2 variant (not the headline)")
+    ap.add_argument("--bf16", action="store_true",
+                    help="NEXT-4 sensitivity variant: B stored as bf16 (fp32 accumulation); not the headline")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="replay each step from a captured CUDA graph (auto: when a step < 0.5 ms, "
                          "i.e. launch-bound configs)")
@@ -83,19 +85,22 @@ def measured_peaks():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def ldb_for(F):
-    return (F + 3) // 4 * 4          # rows padded to 16 B
+def ldb_for(F, elem=4):
+    """Rows padded to 16 B: 4 fp32 or 8 bf16 elements."""
+    m = 16 // elem
+    return (F + m - 1) // m * m
 
 
 def workload_name(a):
     return (f"{a.config}-shaped synthetic CSR, F={a.F}, s={a.s}, {a.strategy}, "
-            f"{'GraphSage mean' if a.reduce == 'mean' else 'GCN sum'}")
+            f"{'GraphSage mean' if a.reduce == 'mean' else 'GCN sum'}"
+            + (", B stored bf16 (NEXT-4 variant)" if getattr(a, "bf16", False) else ""))
 
 
-def byte_model(K, n_rows, F):
+def byte_model(K, n_rows, F, b_elem=4):
     """Algorithmic bytes of one pass: 8K (sampled colind+val) + 8(N+1) (rowptr)
-    + 4FK (B-row gathers) + 4FN (C store)."""
-    return 8 * K + 8 * (n_rows + 1) + 4 * F * K + 4 * F * n_rows
+    + 4FK (B-row gathers; 2FK with bf16 storage) + 4FN (C store)."""
+    return 8 * K + 8 * (n_rows + 1) + b_elem * F * K + 4 * F * n_rows
 
 
 # ------------------------------------------------------------------ clocks sampler
@@ -215,7 +220,9 @@ def main():
     rowptr, colind = synth.graph(a.config)
     n = len(rowptr) - 1
     nnz = int(rowptr[-1])
-    F, ldb = a.F, ldb_for(a.F)
+    F = a.F
+    b_elem = 2 if a.bf16 else 4
+    ldb = ldb_for(F, b_elem)
     _, seed_b = synth.seeds(a.config)
     B = synth.dense(n, F, seed_b, ld=ldb)
     val = np.ones(nnz, np.float32)                         # unweighted adjacency (L615), read by the kernel
@@ -230,13 +237,19 @@ def main():
     ci_d = torch.from_numpy(colind[e0:e1]).to(dev)
     va_d = torch.from_numpy(val[e0:e1]).to(dev)
     B_d = torch.from_numpy(B).to(dev)                      # replicated: no collective on the timed path
-    C_d = torch.empty((r1 - r0, ldb), dtype=torch.float32, device=dev)
+    if a.bf16:
+        B_d = B_d.to(torch.bfloat16)
+    C_d = torch.empty((r1 - r0, ldb_for(F)), dtype=torch.float32, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
     def launch(st):
-        es.es_spmm_run_rows(n, rp_d, e0, ci_d, va_d, B_d, a.s, strat_id, a.seed, red_id, r0, r1,
-                            F=F, C=C_d, stream=st)
+        if a.bf16:
+            es.es_spmm_run_ex(rp_d, ci_d, va_d, B_d, a.s, strat_id, a.seed, red_id, F=F, C=C_d,
+                              row_begin=r0, row_end=r1, n_rows=n, nnz_base=e0, stream=st)
+        else:
+            es.es_spmm_run_rows(n, rp_d, e0, ci_d, va_d, B_d, a.s, strat_id, a.seed, red_id, r0, r1,
+                                F=F, C=C_d, stream=st)
 
     lc0 = es.es_launch_count()
     for _ in range(a.warmup):
@@ -303,7 +316,7 @@ def main():
 
     # ---------------- roofline of the dominant (only) kernel, this rank's launch
     peak, peak_src = measured_peaks()
-    bytes_rank = byte_model(K_rank, r1 - r0, F)
+    bytes_rank = byte_model(K_rank, r1 - r0, F, b_elem)
     avg_launch = t_rank / a.steps
     achieved = bytes_rank / avg_launch / 1e9
     traffic = None
@@ -321,18 +334,19 @@ def main():
                 "frac": round(achieved / peak, 4), "traffic": traffic,
                 "peak_source": peak_src,
                 "bytes_per_launch": bytes_rank,
-                "bytes_model": "8K + 8(N+1) + 4FK + 4FN (sampled colind+val, rowptr, B gathers, C)",
-                "kernel": es.es_spmm_plan(F, ldb, ldb, B_d, C_d)}
+                "bytes_model": ("8K + 8(N+1) + 2FK + 4FN (bf16 B)" if a.bf16 else
+                                "8K + 8(N+1) + 4FK + 4FN (sampled colind+val, rowptr, B gathers, C)"),
+                "kernel": "es::spmm_cpasync<bf16>" if a.bf16 else es.es_spmm_plan(F, ldb, C_d.stride(0), B_d, C_d)}
 
     # ---------------- end to end through the public host API (pinned host buffers)
     e2e = None
-    if not a.no_e2e:
+    if not a.no_e2e and not a.bf16:
         e2e = run_e2e(a, es, torch, dev, stream, rowptr, colind, val, B, r0, r1, e0, e1, F, ldb,
                       strat_id, red_id, flops_all, world, dist, backend)
 
     # ---------------- CPU baseline: the oracle as it stands, rank 0 at N=1 only
     cpu = None
-    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+    if rank == 0 and world == 1 and not a.no_cpu_baseline and not a.bf16:
         cpu, _ = cpu_baseline(rowptr, colind, val, B, a, strat_id, red_id)
 
     if rank == 0:
@@ -367,7 +381,7 @@ def main():
                        "step_ms_min": round(1e3 * float(per_step.min()), 4),
                        "step_ms_median": round(1e3 * float(np.median(per_step)), 4),
                        "wall_s_timed_region": round(wall, 4),
-                       "bytes_model_per_step_all_ranks": byte_model(K_all, n, F)},
+                       "bytes_model_per_step_all_ranks": byte_model(K_all, n, F, b_elem)},
         }
         print(json.dumps(out), flush=True)
     if world > 1:
