@@ -1,0 +1,61 @@
+#!/usr/bin/env python3
+"""The BASELINE.json metric "vs s": sampled-SpMM GFLOP/s, algorithmic GB/s and roofline fraction
+for s in {16..512} x {Bucket, FastRand} on the dataset-shaped graphs (1 GPU, L2 flushed before
+every launch, CUDA events, median of 5).  Prints one JSON line per point."""
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import synth  # noqa: E402
+import paper_2104_10716_b200 as es  # noqa: E402
+from bench import byte_model, ldb_for, measured_peaks  # noqa: E402
+
+CASES = [("pubmed", 16, 0), ("arxiv", 128, 0), ("proteins", 128, 0), ("reddit", 128, 1), ("reddit", 602, 1)]
+
+
+def main():
+    dev = torch.device("cuda:0")
+    peak, _ = measured_peaks()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    only = sys.argv[1:] or None
+    for name, F, red in CASES:
+        if only and name not in only:
+            continue
+        rowptr, colind = synth.graph(name)
+        n = len(rowptr) - 1
+        d = np.diff(rowptr)
+        ldb = ldb_for(F)
+        B = torch.from_numpy(synth.dense(n, F, synth.seeds(name)[1], ld=ldb)).to(dev)
+        rp, ci = torch.from_numpy(rowptr).to(dev), torch.from_numpy(colind).to(dev)
+        va = torch.ones(len(colind), device=dev)
+        C = torch.empty((n, ldb), device=dev)
+        for s in (16, 32, 64, 128, 256, 512):
+            K = int(np.minimum(d, s).sum())
+            for strat in (1, 2):
+                ts = []
+                for i in range(7):
+                    flush.zero_()
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    es.es_spmm_run(rp, ci, va, B, s, strat, 0, red, F=F, C=C)
+                    e1.record()
+                    torch.cuda.synchronize()
+                    if i >= 2:
+                        ts.append(e0.elapsed_time(e1))
+                ms = float(np.median(ts))
+                gbs = byte_model(K, n, F) / (ms / 1e3) / 1e9
+                print(json.dumps({"graph": name, "F": F, "s": s, "strategy": "bucket" if strat == 1 else "fastrand",
+                                  "reduce": "mean" if red else "sum", "K": K, "rate": round(K / d.sum(), 4),
+                                  "ms": round(ms, 4), "GFLOPs": round(2 * F * K / (ms / 1e3) / 1e9, 1),
+                                  "model_GBs": round(gbs, 1), "frac": round(gbs / peak, 3),
+                                  "sampled_edges_per_s": round(K / (ms / 1e3)),
+                                  "plan": es.es_spmm_plan(F, ldb, ldb, B, C)}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
