@@ -161,8 +161,12 @@ def graph(name: str, cache: bool = True):
     np.cumsum(d, out=rowptr[1:])
     colind = columns(rowptr, len(d), np.maximum(d, 1), sg)
     if cache:
-        np.save(path + "_rowptr.npy", rowptr)
-        np.save(path + "_colind.npy", colind)
+        # atomic publish (several ranks of one node may generate the same graph concurrently);
+        # colind is published last because its presence marks the cache entry complete
+        for suffix, arr in (("_rowptr.npy", rowptr), ("_colind.npy", colind)):
+            tmp = f"{path}{suffix}.{os.getpid()}.tmp.npy"
+            np.save(tmp, arr)
+            os.replace(tmp, path + suffix)
     return rowptr, colind
 
 
