@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true", help="warm-L2 variant (not the headline)")
+    ap.add_argument("--allgather", action="store_true",
+                    help="NEXT-1 variant: the C all-gather fused into the SpMM epilogue (every rank "
+                         "stores its rows into all ranks' C over peer memory); N > 1")
     ap.add_argument("--bf16", action="store_true",
                     help="NEXT-4 sensitivity variant: B stored as bf16 (fp32 accumulation); not the headline")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
@@ -243,8 +246,17 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
+    peers = None
+    if a.allgather:
+        from paper_2104_10716_b200.dist import PeerBuffers
+        peers = PeerBuffers(n, C_d.stride(0), device=dev)
+
     def launch(st):
-        if a.bf16:
+        if peers is not None:
+            es.es_spmm_run_ex(rp_d, ci_d, va_d, B_d, a.s, strat_id, a.seed, red_id, F=F, C=peers.C,
+                              row_begin=r0, row_end=r1, n_rows=n, nnz_base=e0, c_peers=peers.peers,
+                              n_peers=peers.world, stream=st)
+        elif a.bf16:
             es.es_spmm_run_ex(rp_d, ci_d, va_d, B_d, a.s, strat_id, a.seed, red_id, F=F, C=C_d,
                               row_begin=r0, row_end=r1, n_rows=n, nnz_base=e0, stream=st)
         else:
@@ -368,6 +380,8 @@ def main():
                        "strategy": a.strategy, "reduce": a.reduce, "seed": a.seed,
                        "l2": "no flush (warm)" if a.no_flush else "flushed between timed steps (256 MiB write)",
                        "parallelism": f"row-partitioned x{world} (sampled-byte balanced), B replicated"
+                                      + ("; C all-gather fused into the SpMM epilogue (peer stores)"
+                                         if a.allgather else "")
                                       + ("" if backend == "nccl" else f" [{backend} validation run]"),
                        "timing": "sum of per-step CUDA-event times on the launch stream, max over ranks"
                                  + ("; each step replays a captured CUDA graph" if use_graph else "")},
@@ -384,6 +398,11 @@ def main():
                        "bytes_model_per_step_all_ranks": byte_model(K_all, n, F, b_elem)},
         }
         print(json.dumps(out), flush=True)
+    if peers is not None:
+        # every rank holds the full C: check this rank's copy of a peer's block against a local run
+        if world > 1:
+            dist.barrier()
+        peers.close()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

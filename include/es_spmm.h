@@ -78,6 +78,14 @@ typedef struct {
     int32_t prime;
     int32_t mean_divisor;
     int32_t b_dtype;
+    /* Fused all-gather of C (es_spmm_run_ex only).  n_peers > 0: c_peers [dev]
+     * is an array of n_peers device pointers, each the row-0 base of one rank's FULL C
+     * (n_rows x ldc; peer buffers mapped with es_ipc_import, own buffer included); the
+     * epilogue stores every output row (global id) into all of them over NVLink, so after the
+     * kernel plus a cross-rank barrier every rank holds the whole C.  `C` must then be this
+     * rank's own full-C base (used for alignment).  (Read only when struct_size covers them.) */
+    float* const* c_peers;
+    int32_t n_peers;
 } es_spmm_options_t;
 
 /* Edge sampling materialised (stage 1 of Alg. 1; the paper's "pre-sampled graph",
@@ -186,6 +194,19 @@ es_status_t es_spmm_run_host(int64_t n_rows, int64_t n_cols,
                              int64_t row_base /* global id of row 0 (seeded FastRand) */,
                              float* C /*[host]*/, int64_t ldc,
                              void* workspace /*[dev]*/, int64_t workspace_bytes, void* stream);
+
+/* Peer-memory helpers for the fused all-gather (one process per GPU of a node).
+ *   es_ipc_alloc/free: a dedicated cudaMalloc allocation (so an IPC handle maps exactly it).
+ *   es_ipc_export: cudaIpcGetMemHandle of such an allocation into handle_out [host] of
+ *     es_ipc_handle_bytes() bytes; es_ipc_import maps a peer's handle (cudaIpcOpenMemHandle,
+ *     lazy peer access), es_ipc_close unmaps it.  Importing a handle exported by the same
+ *     process is an error (use the local pointer). */
+int32_t es_ipc_handle_bytes(void);
+es_status_t es_ipc_alloc(int64_t bytes, void** dev_ptr_out);
+es_status_t es_ipc_free(void* dev_ptr);
+es_status_t es_ipc_export(void* dev_ptr, void* handle_out);
+es_status_t es_ipc_import(const void* handle, void** dev_ptr_out);
+es_status_t es_ipc_close(void* dev_ptr);
 
 /* Host-side, deterministic row partition for P ranks:
  *   bounds_host[0..n_parts] with bounds[0] = 0, bounds[n_parts] = n_rows, contiguous

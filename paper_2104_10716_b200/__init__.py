@@ -23,6 +23,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libesspmm.so")
 EXPORTS = ("es_spmm_sample", "es_spmm_run", "es_spmm_run_rows", "es_spmm_backward",
            "es_spmm_run_ex", "es_spmm_sample_ex", "es_spmm_backward_ex", "es_spmm_host_workspace_bytes",
+           "es_ipc_handle_bytes", "es_ipc_alloc", "es_ipc_free", "es_ipc_export", "es_ipc_import", "es_ipc_close",
            "es_spmm_run_host", "es_partition_rows", "es_spmm_plan", "es_launch_count",
            "es_status_string")
 
@@ -36,12 +37,14 @@ class EsError(RuntimeError):
 class EsOptions(ctypes.Structure):
     """es_spmm_options_t (include/es_spmm.h): NEXT-4 sensitivity variants."""
     _fields_ = [("struct_size", ctypes.c_int32), ("prime", ctypes.c_int32),
-                ("mean_divisor", ctypes.c_int32), ("b_dtype", ctypes.c_int32)]
+                ("mean_divisor", ctypes.c_int32), ("b_dtype", ctypes.c_int32),
+                ("c_peers", ctypes.c_void_p), ("n_peers", ctypes.c_int32)]
 
     @classmethod
-    def make(cls, prime: int = 0, mean_by_degree: bool = False, bf16: bool = False):
+    def make(cls, prime: int = 0, mean_by_degree: bool = False, bf16: bool = False, c_peers=None,
+             n_peers: int = 0):
         return cls(ctypes.sizeof(cls), prime, ES_MEAN_BY_DEGREE if mean_by_degree else ES_MEAN_BY_SAMPLED,
-                   ES_DTYPE_BF16 if bf16 else ES_DTYPE_F32)
+                   ES_DTYPE_BF16 if bf16 else ES_DTYPE_F32, _ptr(c_peers), n_peers)
 
 
 def load_library(path: str = LIB_PATH):
@@ -77,6 +80,18 @@ def load_library(path: str = LIB_PATH):
     lib.es_spmm_backward_ex.restype = st
     lib.es_spmm_backward_ex.argtypes = [i64, i64, vp, i64, vp, vp, vp, i64, i64, i32, i32, u64, i32, vp,
                                         i64, i64, i64, op, vp]
+    lib.es_ipc_handle_bytes.restype = i32
+    lib.es_ipc_handle_bytes.argtypes = []
+    lib.es_ipc_alloc.restype = st
+    lib.es_ipc_alloc.argtypes = [i64, ctypes.POINTER(ctypes.c_void_p)]
+    lib.es_ipc_free.restype = st
+    lib.es_ipc_free.argtypes = [vp]
+    lib.es_ipc_export.restype = st
+    lib.es_ipc_export.argtypes = [vp, ctypes.c_char_p]
+    lib.es_ipc_import.restype = st
+    lib.es_ipc_import.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]
+    lib.es_ipc_close.restype = st
+    lib.es_ipc_close.argtypes = [vp]
     lib.es_spmm_host_workspace_bytes.restype = i64
     lib.es_spmm_host_workspace_bytes.argtypes = [i64, i64, i64, i64, i64, i32]
     lib.es_spmm_run_host.restype = st
@@ -209,9 +224,12 @@ def es_spmm_run_rows(n_rows: int, rowptr_slice, nnz_base: int, colind_slice, val
 def es_spmm_run_ex(rowptr, colind, val, B, s: int, strategy: int, seed: int = 0,
                    reduce: int = ES_REDUCE_SUM, F: int | None = None, C=None, prime: int = 0,
                    mean_by_degree: bool = False, row_begin: int = 0, row_end: int | None = None,
-                   n_rows: int | None = None, nnz_base: int = 0, stream=None):
-    """es_spmm_run_rows with the NEXT-4 options: P' override, MEAN by original degree, and bf16
-    storage of B (pass a torch.bfloat16 B; accumulation stays fp32)."""
+                   n_rows: int | None = None, nnz_base: int = 0, c_peers=None, n_peers: int = 0,
+                   stream=None):
+    """es_spmm_run_rows with the options: P' override, MEAN by original degree, bf16 storage of
+    B (pass a torch.bfloat16 B; accumulation stays fp32) -- NEXT-4 -- and the fused all-gather
+    (c_peers: int64 CUDA tensor of n_peers full-C base pointers; C = this rank's full C) --
+    NEXT-1, see paper_2104_10716_b200.dist.PeerBuffers."""
     import torch
     _dev(rowptr, torch.int64, "rowptr")
     _dev(colind, torch.int32, "colind")
@@ -228,7 +246,7 @@ def es_spmm_run_ex(rowptr, colind, val, B, s: int, strategy: int, seed: int = 0,
         n_rows = row_end
     if C is None:
         C = torch.empty((row_end - row_begin, F), dtype=torch.float32, device=B.device)
-    opt = EsOptions.make(prime, mean_by_degree, B.dtype == torch.bfloat16)
+    opt = EsOptions.make(prime, mean_by_degree, B.dtype == torch.bfloat16, c_peers, n_peers)
     _check(load_library().es_spmm_run_ex(n_rows, B.shape[0], _ptr(rowptr), nnz_base, _ptr(colind), _ptr(val),
                                          _ptr(B), F, ldb, s, strategy, seed & (2**64 - 1), reduce, _ptr(C),
                                          C.stride(0), row_begin, row_end, ctypes.byref(opt), _stream(stream)),
@@ -342,6 +360,33 @@ def es_spmm_run_host(rowptr, colind, val, B, s: int, strategy: int, seed: int = 
                                            row_base, _ptr(C), C.stride(0), _ptr(workspace), workspace.numel(),
                                            _stream(stream)), "es_spmm_run_host")
     return C
+
+
+def es_ipc_alloc(nbytes: int) -> int:
+    p = ctypes.c_void_p()
+    _check(load_library().es_ipc_alloc(nbytes, ctypes.byref(p)), "es_ipc_alloc")
+    return int(p.value)
+
+
+def es_ipc_free(ptr: int) -> None:
+    _check(load_library().es_ipc_free(ptr), "es_ipc_free")
+
+
+def es_ipc_export(ptr: int) -> bytes:
+    lib = load_library()
+    buf = ctypes.create_string_buffer(lib.es_ipc_handle_bytes())
+    _check(lib.es_ipc_export(ptr, buf), "es_ipc_export")
+    return buf.raw
+
+
+def es_ipc_import(handle: bytes) -> int:
+    p = ctypes.c_void_p()
+    _check(load_library().es_ipc_import(handle, ctypes.byref(p)), "es_ipc_import")
+    return int(p.value)
+
+
+def es_ipc_close(ptr: int) -> None:
+    _check(load_library().es_ipc_close(ptr), "es_ipc_close")
 
 
 def es_partition_rows(rowptr_host, s: int, F: int, n_parts: int) -> np.ndarray:

@@ -4,6 +4,7 @@
 #include <atomic>
 #include <cstdint>
 #include <cstdio>
+#include <cstddef>
 #include <cstring>
 #include <vector>
 
@@ -30,18 +31,25 @@ struct Opts {
     uint32_t prime = 577;
     int32_t mean_by_degree = 0;
     int32_t bf16 = 0;
+    float* const* c_peers = nullptr;
+    int32_t n_peers = 0;
 };
 
 es_status_t read_opts(const es_spmm_options_t* o, Opts* out) {
     *out = Opts{};
     if (!o) return ES_OK;
-    if (o->struct_size < (int32_t)sizeof(es_spmm_options_t)) return ES_ERR_INVALID_VALUE;
+    if (o->struct_size < (int32_t)offsetof(es_spmm_options_t, c_peers)) return ES_ERR_INVALID_VALUE;
     if (o->prime < 0) return ES_ERR_INVALID_VALUE;
     if (o->mean_divisor != ES_MEAN_BY_SAMPLED && o->mean_divisor != ES_MEAN_BY_DEGREE) return ES_ERR_INVALID_VALUE;
     if (o->b_dtype != ES_DTYPE_F32 && o->b_dtype != ES_DTYPE_BF16) return ES_ERR_INVALID_VALUE;
     out->prime = o->prime == 0 ? 577u : (uint32_t)o->prime;
     out->mean_by_degree = o->mean_divisor == ES_MEAN_BY_DEGREE;
     out->bf16 = o->b_dtype == ES_DTYPE_BF16;
+    if (o->struct_size >= (int32_t)sizeof(es_spmm_options_t)) {
+        if (o->n_peers < 0 || (o->n_peers > 0 && !o->c_peers)) return ES_ERR_INVALID_VALUE;
+        out->c_peers = o->c_peers;
+        out->n_peers = o->n_peers;
+    }
     return ES_OK;
 }
 
@@ -75,6 +83,8 @@ es_status_t run_rows_impl(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
     p.prime = o.prime;
     p.mean_by_degree = o.mean_by_degree;
     p.b_bf16 = o.bf16;
+    p.c_peers = o.c_peers;
+    p.n_peers = o.n_peers;
     const es::Plan plan = o.bf16 ? es::make_plan_bf16(F, ldb, ldc, B, C) : es::make_plan(F, ldb, ldc, B, C);
     if (plan.unsupported) return ES_ERR_UNSUPPORTED;
     cudaError_t err = es::launch_spmm(p, plan, st);
@@ -219,6 +229,39 @@ es_status_t es_spmm_backward_ex(int64_t n_rows, int64_t n_cols, const int64_t* r
     cudaError_t err = es::launch_backward(p, as_stream(stream));
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return err == cudaSuccess ? ES_OK : ES_ERR_CUDA;
+}
+
+int32_t es_ipc_handle_bytes(void) { return (int32_t)sizeof(cudaIpcMemHandle_t); }
+
+es_status_t es_ipc_alloc(int64_t bytes, void** dev_ptr_out) {
+    if (bytes <= 0 || !dev_ptr_out) return ES_ERR_INVALID_VALUE;
+    return cudaMalloc(dev_ptr_out, (size_t)bytes) == cudaSuccess ? ES_OK : ES_ERR_CUDA;
+}
+
+es_status_t es_ipc_free(void* dev_ptr) {
+    if (!dev_ptr) return ES_ERR_INVALID_VALUE;
+    return cudaFree(dev_ptr) == cudaSuccess ? ES_OK : ES_ERR_CUDA;
+}
+
+es_status_t es_ipc_export(void* dev_ptr, void* handle_out) {
+    if (!dev_ptr || !handle_out) return ES_ERR_INVALID_VALUE;
+    cudaIpcMemHandle_t h;
+    if (cudaIpcGetMemHandle(&h, dev_ptr) != cudaSuccess) return ES_ERR_CUDA;
+    std::memcpy(handle_out, &h, sizeof(h));
+    return ES_OK;
+}
+
+es_status_t es_ipc_import(const void* handle, void** dev_ptr_out) {
+    if (!handle || !dev_ptr_out) return ES_ERR_INVALID_VALUE;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    return cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess ? ES_OK
+                                                                                              : ES_ERR_CUDA;
+}
+
+es_status_t es_ipc_close(void* dev_ptr) {
+    if (!dev_ptr) return ES_ERR_INVALID_VALUE;
+    return cudaIpcCloseMemHandle(dev_ptr) == cudaSuccess ? ES_OK : ES_ERR_CUDA;
 }
 
 es_status_t es_partition_rows(const int64_t* rowptr_host, int64_t n_rows, int32_t s, int64_t F,

@@ -23,6 +23,8 @@ struct SpmmParams {
     uint32_t prime;          // P' (577 unless overridden, NEXT-4)
     int32_t mean_by_degree;  // MEAN divides by d_i instead of k_i (NEXT-4)
     int32_t b_bf16;          // B stored as bf16 (fp32 accumulation, NEXT-4)
+    float* const* c_peers;   // fused all-gather: full-C bases of every rank (NEXT-1)
+    int32_t n_peers;         // 0: plain store to C
 };
 
 struct Plan {

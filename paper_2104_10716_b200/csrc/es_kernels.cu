@@ -48,6 +48,20 @@ __device__ __forceinline__ void store_out(float* Crow, int64_t vidx, int64_t F, 
     }
 }
 
+// a5 store of one VEC-wide piece of local row r: to C, or -- fused all-gather (NEXT-1) -- to
+// global row row_base + r of every rank's full C over peer memory (NVLink stores).
+template <int VEC>
+__device__ __forceinline__ void store_c(const SpmmParams& p, int64_t r, int64_t vidx, const float* res,
+                                        uint64_t pol) {
+    if (p.n_peers == 0) {
+        store_out<VEC>(p.C + r * p.ldc, vidx, p.F, res, p.c_vec, pol);
+        return;
+    }
+    const int64_t off = (p.row_base + r) * p.ldc;
+    for (int q = 0; q < p.n_peers; ++q)
+        store_out<VEC>(p.c_peers[q] + off, vidx, p.F, res, p.c_vec, pol);
+}
+
 // a5 epilogue: SUM, or MEAN = / div (IEEE) with div = k_i (reading R5) or d_i (NEXT-4 option)
 __device__ __forceinline__ float finish(float x, int reduce, int64_t div) {
     if (reduce == kMean) return div > 0 ? __fdiv_rn(x, (float)div) : 0.0f;
@@ -71,7 +85,6 @@ spmm_warp(const SpmmParams p) {
     rs.init(ld_stream(p.rowptr + r, pol_a) - p.nnz_base, ld_stream(p.rowptr + r + 1, pol_a) - p.nnz_base,
             p.s, p.strategy, p.seed, p.row_base + r, p.prime);
     const int64_t NV = (p.F + VEC - 1) / VEC;
-    float* Crow = p.C + r * p.ldc;
 
     for (int64_t v0 = 0; v0 < NV; v0 += 32 * NCH) {       // feature tiles (1 pass if NV <= 32*NCH)
         // part: sequential sum over the (<= 32) slots of the current chunk; tot: sum of chunk
@@ -143,7 +156,7 @@ spmm_warp(const SpmmParams p) {
                 float res[VEC];
 #pragma unroll
                 for (int q = 0; q < VEC; ++q) res[q] = finish(tot[c][q], p.reduce, mean_div(p, rs.d, rs.k));
-                store_out<VEC>(Crow, vidx, p.F, res, p.c_vec, pol_a);
+                store_c<VEC>(p, r, vidx, res, pol_a);
             }
         }
     }
@@ -212,7 +225,7 @@ spmm_subwarp(const SpmmParams p) {
         float res[VEC];
 #pragma unroll
         for (int q = 0; q < VEC; ++q) res[q] = finish(acc[q], p.reduce, mean_div(p, rs.d, rs.k));
-        store_out<VEC>(p.C + r * p.ldc, g, p.F, res, p.c_vec, pol_a);
+        store_c<VEC>(p, r, g, res, pol_a);
     }
 }
 
@@ -354,7 +367,7 @@ spmm_cpasync(const SpmmParams p) {
                 float res[4];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) res[q] = finish(tot[ch][4 * h + q], p.reduce, div);
-                store_out<4>(p.C + r * p.ldc, (int64_t)(lane + 32 * ch) * (EPP / 4) + h, p.F, res, p.c_vec, pol_a);
+                store_c<4>(p, r, (int64_t)(lane + 32 * ch) * (EPP / 4) + h, res, pol_a);
             }
         }
     }
@@ -462,7 +475,6 @@ struct RowAcc {
     }
     __device__ __forceinline__ void store(const SpmmParams& p, int64_t row, int lane, int64_t NV,
                                           int64_t div, uint64_t pol) {
-        float* Crow = p.C + row * p.ldc;
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
             const int64_t vidx = lane + 32 * c;
@@ -470,7 +482,7 @@ struct RowAcc {
                 float res[VEC];
 #pragma unroll
                 for (int q = 0; q < VEC; ++q) res[q] = finish(tot[c][q] + part[c][q], p.reduce, div);
-                store_out<VEC>(Crow, vidx, p.F, res, p.c_vec, pol);
+                store_c<VEC>(p, row, vidx, res, pol);
             }
         }
     }

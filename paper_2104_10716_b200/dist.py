@@ -99,3 +99,76 @@ def sampled_spmm_distributed(rowptr_host, colind_host, val_host, B_local, F: int
     if gather_c and world > 1:
         return allgather_rows(C, sh.bounds, group)
     return C
+
+
+# --------------------------------------------------------------------------- fused all-gather
+class _CudaArray:
+    """Minimal __cuda_array_interface__ holder to view a raw allocation as a torch tensor."""
+
+    def __init__(self, ptr: int, shape: tuple):
+        self.__cuda_array_interface__ = {"shape": shape, "typestr": "<f4", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+class PeerBuffers:
+    """A full-size C (n_rows x ldc fp32) on every rank, mapped into every other rank with CUDA
+    IPC (es_ipc_*), for the SpMM whose epilogue writes each output row into all ranks' C over
+    NVLink (the C all-gather fused into the SpMM, no separate collective).
+    Handles are exchanged once with all_gather_object (any backend)."""
+
+    def __init__(self, n_rows: int, ldc: int, group=None, device=None):
+        import torch
+        import torch.distributed as dist
+        from . import es_ipc_alloc, es_ipc_export, es_ipc_import
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.n_rows, self.ldc = n_rows, ldc
+        self.local_ptr = es_ipc_alloc(max(1, n_rows * ldc * 4))
+        handles = [es_ipc_export(self.local_ptr)]
+        if self.world > 1:
+            handles = [None] * self.world
+            dist.all_gather_object(handles, es_ipc_export(self.local_ptr), group=group)
+        self.ptrs, self.imported = [], []
+        for r, h in enumerate(handles):
+            if r == self.rank:
+                self.ptrs.append(self.local_ptr)
+            else:
+                ptr = es_ipc_import(h)
+                self.ptrs.append(ptr)
+                self.imported.append(ptr)
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.peers = torch.tensor(self.ptrs, dtype=torch.int64, device=dev)
+        self.C = torch.as_tensor(_CudaArray(self.local_ptr, (n_rows, ldc)), device=dev)
+
+    def close(self):
+        from . import es_ipc_close, es_ipc_free
+        for ptr in self.imported:
+            es_ipc_close(ptr)
+        self.imported = []
+        if self.local_ptr:
+            es_ipc_free(self.local_ptr)
+            self.local_ptr = 0
+
+
+def sampled_spmm_fused_allgather(rowptr_host, colind_host, val_host, B, F: int, s: int, strategy: int,
+                                 seed: int, reduce: int, peers: PeerBuffers, group=None, partition=None):
+    """This rank's row block through es_spmm_run_ex with the fused all-gather epilogue; on
+    return (after a barrier) peers.C holds the FULL C on every rank."""
+    import torch
+    import torch.distributed as dist
+    from . import es_spmm_run_ex
+    n_rows = len(rowptr_host) - 1
+    sh = plan(rowptr_host, s, F, peers.world, peers.rank, partition=partition)
+    rp, ci, va = local_csr(rowptr_host, colind_host, val_host, sh)
+    dev = B.device
+
+    def t(a):
+        return None if a is None else torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+    es_spmm_run_ex(t(rp), t(ci), t(va), B, s, strategy, seed, reduce, F=F, C=peers.C,
+                   row_begin=sh.r0, row_end=sh.r1, n_rows=n_rows, nnz_base=sh.e0,
+                   c_peers=peers.peers, n_peers=peers.world)
+    torch.cuda.synchronize(dev)
+    if peers.world > 1:
+        dist.barrier(group=group)
+    return peers.C

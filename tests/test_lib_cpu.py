@@ -22,7 +22,7 @@ def lib():
 def test_header_declarations_are_exported(lib):
     with open(os.path.join(ROOT, "include", "es_spmm.h")) as f:
         text = f.read()
-    declared = set(re.findall(r"^\s*(?:es_status_t|int64_t|const char\*)\s+(es_\w+)\s*\(", text, re.M))
+    declared = set(re.findall(r"^\s*(?:es_status_t|int64_t|int32_t|const char\*)\s+(es_\w+)\s*\(", text, re.M))
     assert declared == set(es.EXPORTS), declared ^ set(es.EXPORTS)
     for name in declared:
         assert hasattr(lib, name), name
