@@ -399,9 +399,8 @@ def main():
         }
         print(json.dumps(out), flush=True)
     if peers is not None:
-        # every rank holds the full C: check this rank's copy of a peer's block against a local run
         if world > 1:
-            dist.barrier()
+            dist.barrier()                   # no rank unmaps while a peer may still write into it
         peers.close()
     if world > 1:
         dist.barrier()
