@@ -4,20 +4,24 @@
 //   a1  d_i, k_i = min(d_i, s)                     Alg. 1 l.5-6
 //   a2  sample positions p_j (Bucket / Eq. 2)      Alg. 1 l.8, L1042-1067
 //   a3  stage 1: (colind, val) of the k_i slots    Alg. 1 l.7-11 -- staged in REGISTERS,
-//       one slot per lane (coalesced for Bucket), broadcast by warp shuffles
-//   a4  stage 2: gather-FMA over B rows             Alg. 1 l.12-15 -- 128-bit vector
-//       gathers, several B rows in flight per lane, fp32 FMA into two interleaved
-//       partial sums (even / odd slots; R8 error bound)
+//       one slot per lane (coalesced for Bucket), broadcast by warp shuffles, the next
+//       32-slot chunk requested one chunk ahead
+//   a4  stage 2: gather-FMA over B rows             Alg. 1 l.12-15 -- fp32 FMA of each slot
+//       into a per-32-slot partial, partials summed in order (DESIGN.md §6 error bound)
 //   a5  epilogue: SUM, or MEAN = / k_i (IEEE)      Alg. 1 l.16, L1570-1575 (R5)
 //
-// Thread mapping: the paper's "group of threads per row, threads
-// on neighbouring columns of B" (L996-1001, L1093-1098) becomes, on B200,
-//   * spmm_warp   : one warp per row; lane l owns feature vectors l + 32c, c < NCH
-//                   (F/VEC > 16, e.g. F=128: 1 float4 / lane; F=602 (ldb 604): 5);
-//   * spmm_subwarp: F/VEC <= 16: the warp is split into E = 32/G streams of G lanes,
-//                   stream e sums slots j = e (mod E), then an xor-shuffle tree.
-// The summation order depends only on (k_i, F, vector width), never on which rows a
-// launch covers: row blocks computed on different GPUs are bitwise identical.
+// Kernel families (make_plan picks one from F, ldb and alignment):
+//   * spmm_tma     : 512 < F <= 1024, 16-B rows: lane 0 of a one-warp CTA moves whole B rows
+//                    with cp.async.bulk into a 4-stage smem ring (mbarrier expect_tx);
+//   * spmm_cpasync : 64 < F <= 512, 16-B rows: every lane streams its own 16-B pieces of each
+//                    B row into a private smem ring with cp.async (no synchronisation);
+//   * spmm_warp    : other F/VEC > 16 (8-/4-B aligned rows, F > 1024): one warp per row,
+//                    lane l owns feature vectors l + 32c, U rows in flight in registers;
+//   * spmm_subwarp : F/VEC <= 16: the warp is split into E = 32/G streams of G lanes, stream e
+//                    sums slots j = e (mod E), then an xor-shuffle tree.
+// spmm_tma / spmm_cpasync / spmm_warp share one per-element summation order (bitwise equal).
+// The order depends only on (k_i, F, vector width), never on which rows a launch covers:
+// row blocks computed on different GPUs are bitwise identical.
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
