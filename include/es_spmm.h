@@ -86,6 +86,10 @@ typedef struct {
      * rank's own full-C base (used for alignment).  (Read only when struct_size covers them.) */
     float* const* c_peers;
     int32_t n_peers;
+    /* es_spmm_backward_ex only: 1 = bitwise-reproducible dB (stable radix sort of the sampled
+     * slots by column, one writer per dB row; takes stream-ordered scratch and synchronises the
+     * stream once to size it; K and n_cols must be < 2^31, else ES_ERR_UNSUPPORTED). */
+    int32_t deterministic;
 } es_spmm_options_t;
 
 /* Edge sampling materialised (stage 1 of Alg. 1; the paper's "pre-sampled graph",

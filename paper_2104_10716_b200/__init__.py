@@ -38,13 +38,14 @@ class EsOptions(ctypes.Structure):
     """es_spmm_options_t (include/es_spmm.h): NEXT-4 sensitivity variants."""
     _fields_ = [("struct_size", ctypes.c_int32), ("prime", ctypes.c_int32),
                 ("mean_divisor", ctypes.c_int32), ("b_dtype", ctypes.c_int32),
-                ("c_peers", ctypes.c_void_p), ("n_peers", ctypes.c_int32)]
+                ("c_peers", ctypes.c_void_p), ("n_peers", ctypes.c_int32),
+                ("deterministic", ctypes.c_int32)]
 
     @classmethod
     def make(cls, prime: int = 0, mean_by_degree: bool = False, bf16: bool = False, c_peers=None,
-             n_peers: int = 0):
+             n_peers: int = 0, deterministic: bool = False):
         return cls(ctypes.sizeof(cls), prime, ES_MEAN_BY_DEGREE if mean_by_degree else ES_MEAN_BY_SAMPLED,
-                   ES_DTYPE_BF16 if bf16 else ES_DTYPE_F32, _ptr(c_peers), n_peers)
+                   ES_DTYPE_BF16 if bf16 else ES_DTYPE_F32, _ptr(c_peers), n_peers, int(deterministic))
 
 
 def load_library(path: str = LIB_PATH):
@@ -283,14 +284,15 @@ def es_spmm_sample_ex(rowptr, colind, val, s: int, strategy: int, seed: int = 0,
 
 def es_spmm_backward_ex(rowptr, colind, val, dC, n_cols: int, s: int, strategy: int, seed: int = 0,
                         reduce: int = ES_REDUCE_SUM, prime: int = 0, mean_by_degree: bool = False,
-                        F: int | None = None, dB=None, stream=None):
-    """Backward with the P' / MEAN-divisor options (full CSR)."""
+                        F: int | None = None, dB=None, deterministic: bool = False, stream=None):
+    """Backward with the P' / MEAN-divisor options (full CSR); deterministic=True gives a
+    bitwise-reproducible dB (sort-based transpose, single writer per row)."""
     import torch
     F = dC.shape[1] if F is None else F
     if dB is None:
         dB = torch.zeros((n_cols, F), dtype=torch.float32, device=dC.device)
     n = rowptr.numel() - 1
-    opt = EsOptions.make(prime, mean_by_degree)
+    opt = EsOptions.make(prime, mean_by_degree, deterministic=deterministic)
     _check(load_library().es_spmm_backward_ex(n, n_cols, _ptr(rowptr), 0, _ptr(colind), _ptr(val), _ptr(dC), F,
                                               dC.stride(0), s, strategy, seed & (2**64 - 1), reduce, _ptr(dB),
                                               dB.stride(0), 0, n, ctypes.byref(opt), _stream(stream)),

@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["es_kernels.cu", "es_abi.cu"]
+SOURCES = ["es_kernels.cu", "es_backward_det.cu", "es_abi.cu"]
 HEADERS = ["es_device.cuh", "es_internal.h"]
 LIB = os.path.join(HERE, "libesspmm.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

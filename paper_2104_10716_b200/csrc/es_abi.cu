@@ -33,6 +33,7 @@ struct Opts {
     int32_t bf16 = 0;
     float* const* c_peers = nullptr;
     int32_t n_peers = 0;
+    int32_t deterministic = 0;
 };
 
 es_status_t read_opts(const es_spmm_options_t* o, Opts* out) {
@@ -45,11 +46,12 @@ es_status_t read_opts(const es_spmm_options_t* o, Opts* out) {
     out->prime = o->prime == 0 ? 577u : (uint32_t)o->prime;
     out->mean_by_degree = o->mean_divisor == ES_MEAN_BY_DEGREE;
     out->bf16 = o->b_dtype == ES_DTYPE_BF16;
-    if (o->struct_size >= (int32_t)sizeof(es_spmm_options_t)) {
+    if (o->struct_size >= (int32_t)offsetof(es_spmm_options_t, deterministic)) {
         if (o->n_peers < 0 || (o->n_peers > 0 && !o->c_peers)) return ES_ERR_INVALID_VALUE;
         out->c_peers = o->c_peers;
         out->n_peers = o->n_peers;
     }
+    if (o->struct_size >= (int32_t)sizeof(es_spmm_options_t)) out->deterministic = o->deterministic != 0;
     return ES_OK;
 }
 
@@ -226,6 +228,14 @@ es_status_t es_spmm_backward_ex(int64_t n_rows, int64_t n_cols, const int64_t* r
     if (a % 16 == 0 && b % 16 == 0 && ldc % 4 == 0 && ldb % 4 == 0) p.vec = 4;
     else if (a % 8 == 0 && b % 8 == 0 && ldc % 2 == 0 && ldb % 2 == 0) p.vec = 2;
     else p.vec = 1;
+    if (o.deterministic) {
+        int launches = 0;
+        bool too_large = false;
+        cudaError_t err = es::launch_backward_deterministic(p, n_cols, as_stream(stream), &launches, &too_large);
+        g_launches.fetch_add(launches, std::memory_order_relaxed);
+        if (too_large) return ES_ERR_UNSUPPORTED;
+        return err == cudaSuccess ? ES_OK : ES_ERR_CUDA;
+    }
     cudaError_t err = es::launch_backward(p, as_stream(stream));
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return err == cudaSuccess ? ES_OK : ES_ERR_CUDA;

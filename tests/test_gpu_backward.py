@@ -102,3 +102,19 @@ def test_autograd_gradient(graph):
         g = B.grad.cpu().numpy()
         ok, worst = bound_ok(g, rowptr, colind, val, W.cpu().numpy(), 1100, 24, 2, seed, 1)
         assert ok, worst
+
+
+@pytest.mark.parametrize("F", [1, 40, 128, 602])
+@pytest.mark.parametrize("reduce", [0, 1])
+def test_deterministic_backward_parity_and_reproducibility(graph, F, reduce):
+    rowptr, colind, val = graph
+    dC = synth.dense(900, F, seed=F + 3)
+    runs = [es.es_spmm_backward_ex(t(rowptr), t(colind), t(val), t(dC), 1100, 64, 2, 9, reduce,
+                                   deterministic=True).cpu().numpy() for _ in range(3)]
+    assert all(np.array_equal(runs[0].view(np.uint32), r.view(np.uint32)) for r in runs[1:])
+    ok, worst = bound_ok(runs[0], rowptr, colind, val, dC, 1100, 64, 2, 9, reduce)
+    assert ok, worst
+    ones = es.es_spmm_backward_ex(t(rowptr), t(colind), None, torch.ones((900, F), device=DEV), 1100, 64, 2, 9,
+                                  deterministic=True).cpu().numpy()
+    _, sc, _, _ = oracle.sample(rowptr, colind, None, 64, 2, 9)
+    assert np.array_equal(ones, np.repeat(np.bincount(sc, minlength=1100).astype(np.float32)[:, None], F, 1))
