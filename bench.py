@@ -89,8 +89,9 @@ def measured_peaks():
 
 
 def ldb_for(F, elem=4):
-    """Rows padded to 16 B: 4 fp32 or 8 bf16 elements."""
-    m = 16 // elem
+    """B/C rows padded to a multiple of 32 B, the DRAM/L2 sector:
+    F=602 fp32 -> 608 (2,432 B = 19 full 128-B L2 lines per gathered row)."""
+    m = 32 // elem
     return (F + m - 1) // m * m
 
 

@@ -30,11 +30,12 @@ def main():
     ap.add_argument("--steps", type=int, default=6)
     ap.add_argument("--variants", default="k=warp;k=tma,st=4")
     ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--ldb", type=int, default=0, help="override the B row pitch (floats)")
     a = ap.parse_args()
     dev = torch.device("cuda:0")
     rowptr, colind = synth.graph(a.config)
     n = len(rowptr) - 1
-    F, ldb = a.F, ldb_for(a.F)
+    F, ldb = a.F, (a.ldb or ldb_for(a.F))
     B = synth.dense(n, F, synth.seeds(a.config)[1], ld=ldb)
     rp = torch.from_numpy(rowptr).to(dev)
     ci = torch.from_numpy(colind).to(dev)
