@@ -119,7 +119,8 @@ es_status_t es_spmm_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, con
         snprintf(buf, (size_t)buf_len, "es::spmm_tma<nch%d,stages%d>(rows/warp %d)%s", pl.nch, pl.stages,
                  pl.rows_per_warp, pl.c_vec ? "" : " (scalar C)");
     else if (pl.cpasync)
-        snprintf(buf, (size_t)buf_len, "es::spmm_cpasync<stages%d>%s", pl.stages, pl.c_vec ? "" : " (scalar C)");
+        snprintf(buf, (size_t)buf_len, "es::spmm_cpasync%s<stages%d>%s", pl.halfwarp ? "_hw" : "", pl.stages,
+                 pl.c_vec ? "" : " (scalar C)");
     else if (pl.subwarp)
         snprintf(buf, (size_t)buf_len, "es::spmm_subwarp<vec%d,g%d>%s", pl.vec, pl.g, pl.c_vec ? "" : " (scalar C)");
     else

@@ -36,6 +36,7 @@ struct Plan {
     bool tma;          // TMA-ring kernel (spmm_tma)
     bool cpasync;      // cp.async ring kernel (spmm_cpasync)
     bool bf16;         // B stored as bf16 (cp.async ring only)
+    bool halfwarp;     // cp.async ring, two slots per step (spmm_cpasync_hw)
     bool unsupported;  // no kernel for this layout (bf16 with misaligned rows)
     int stages;         // ring depth (tma)
     int rows_per_warp;  // consecutive rows per warp (tma)

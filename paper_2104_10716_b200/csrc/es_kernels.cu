@@ -377,6 +377,117 @@ spmm_cpasync(const SpmmParams p) {
     }
 }
 
+// ------------------------------------------------------------------ cp.async ring, two slots per step
+// F <= 128 (F/4 <= 32 pieces): the two half-warps take alternate slots (even -> lanes 0-15, odd
+// -> lanes 16-31), each lane copying/consuming two 16-B pieces per slot, so the per-slot
+// bookkeeping (shuffles, address math, commit/wait) is paid once per two slots.  Each half
+// sums its slots in order with 32-slot-chunk partials; the halves are added at the end
+// (a + b in both halves, so every lane holds the same bits).  Deterministic; a different
+// (interleaved) order than spmm_cpasync, inside the same error bound.
+template <int D, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
+spmm_cpasync_hw(const SpmmParams p) {
+    static_assert(D >= 1 && D <= 8, "ring depth (2D slots must fit one 32-slot chunk)");
+    extern __shared__ __align__(16) float4 ring_smem[];          // [kWarps][D][2][32]
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int h = lane >> 4, sub = lane & 15;
+    const int64_t r = (int64_t)blockIdx.x * kWarps + warp;
+    if (r >= p.n_rows) return;
+    const uint64_t pol_a = policy_evict_first();
+    const uint64_t pol_b = policy_evict_last();
+    RowSampler rs;
+    rs.init(ld_stream(p.rowptr + r, pol_a) - p.nnz_base, ld_stream(p.rowptr + r + 1, pol_a) - p.nnz_base,
+            p.s, p.strategy, p.seed, p.row_base + r, p.prime);
+    const int NV = (int)((p.F + 3) / 4);                          // <= 32
+    const bool act0 = sub < NV, act1 = sub + 16 < NV;
+    const int32_t k = rs.k;
+    float4* my = ring_smem + (size_t)warp * D * 64 + h * 32 + sub;  // + stage*64 (+16 for piece 1)
+    const float* bl = p.B + sub * 4;
+
+    auto copy_slot = [&](int stage, int32_t c) {
+        const float* src = bl + (int64_t)c * p.ldb;
+        if (act0) cp_async16(my + stage * 64, src, pol_b);
+        if (act1) cp_async16(my + stage * 64 + 16, src + 64, pol_b);
+    };
+
+    int32_t c0 = 0, c1 = 0;
+    float a0 = 0.0f, a1 = 0.0f;
+    if (lane < k) {
+        const int64_t e = rs.beg + rs.pos(lane);
+        c0 = ld_stream(p.colind + e, pol_a);
+        a0 = p.val ? ld_stream(p.val + e, pol_a) : 1.0f;
+    }
+    if (32 + lane < k) {
+        const int64_t e = rs.beg + rs.pos(32 + lane);
+        c1 = ld_stream(p.colind + e, pol_a);
+        a1 = p.val ? ld_stream(p.val + e, pol_a) : 1.0f;
+    }
+    // prologue: steps 0 .. D-1 = slots 0 .. 2D-1 (chunk 0)
+#pragma unroll
+    for (int t = 0; t < D; ++t) {
+        const int32_t c = __shfl_sync(kFull, c0, 2 * t + h);
+        if (2 * t + h < k) copy_slot(t, c);
+        cp_async_commit();
+    }
+    float part[8], tot[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) { part[q] = 0.0f; tot[q] = 0.0f; }
+    for (int32_t j0 = 0; j0 < k; j0 += 32) {
+        const int n_steps = (min(32, k - j0) + 1) / 2;
+#pragma unroll 2
+        for (int u = 0; u < 16; ++u) {                           // step u: slots j0+2u (+h)
+            if (u >= n_steps) break;
+            const int st = (j0 / 2 + u) % D;
+            cp_async_wait<D - 1>();
+            const int slot = 2 * u + h;
+            const float av = __shfl_sync(kFull, a0, slot);
+            if (j0 + slot < k) {
+                if (act0) {
+                    const float4 x = my[st * 64];
+                    part[0] = fmaf(av, x.x, part[0]); part[1] = fmaf(av, x.y, part[1]);
+                    part[2] = fmaf(av, x.z, part[2]); part[3] = fmaf(av, x.w, part[3]);
+                }
+                if (act1) {
+                    const float4 x = my[st * 64 + 16];
+                    part[4] = fmaf(av, x.x, part[4]); part[5] = fmaf(av, x.y, part[5]);
+                    part[6] = fmaf(av, x.z, part[6]); part[7] = fmaf(av, x.w, part[7]);
+                }
+            }
+            const int tn = slot + 2 * D;                         // refill: step u + D
+            const int32_t cc = __shfl_sync(kFull, c0, tn & 31);
+            const int32_t cn = __shfl_sync(kFull, c1, tn & 31);
+            if (j0 + tn < k) copy_slot(st, tn < 32 ? cc : cn);
+            cp_async_commit();
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) { tot[q] += part[q]; part[q] = 0.0f; }
+        c0 = c1;
+        a0 = a1;
+        c1 = 0;
+        a1 = 0.0f;
+        if (j0 + 64 + lane < k) {
+            const int64_t e = rs.beg + rs.pos(j0 + 64 + lane);
+            c1 = ld_stream(p.colind + e, pol_a);
+            a1 = p.val ? ld_stream(p.val + e, pol_a) : 1.0f;
+        }
+    }
+    cp_async_wait<0>();
+    int64_t div = k;
+    if (p.reduce == kMean && p.mean_by_degree)
+        div = ld_stream(p.rowptr + r + 1, pol_a) - ld_stream(p.rowptr + r, pol_a);
+    float res[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const float o = __shfl_xor_sync(kFull, tot[q], 16);
+        res[q] = finish(h == 0 ? tot[q] + o : o + tot[q], p.reduce, div);
+    }
+    if (h == 0) {
+        if (act0) store_c<4>(p, r, sub, res, pol_a);
+        if (act1) store_c<4>(p, r, sub + 16, res + 4, pol_a);
+    }
+}
+
 // ------------------------------------------------------------------ per-warp slot stream
 // A warp owns R <= 32 consecutive rows; their sampled slots form one flat stream (row by
 // row, slot order).  Row i's metadata (a1) lives in lane i; (col, val) of 32 consecutive
@@ -720,8 +831,28 @@ cudaError_t launch_cpasync_bf16(const SpmmParams& p, const Plan& plan, cudaStrea
     }
 }
 
+template <int D, int MINB>
+cudaError_t launch_cpasync_hw_k(const SpmmParams& p, cudaStream_t st) {
+    const int64_t blocks = (p.n_rows + kWarps - 1) / kWarps;
+    const size_t smem = (size_t)kWarps * D * 64 * 16;
+    auto k = spmm_cpasync_hw<D, MINB>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    k<<<(unsigned)blocks, kThreads, smem, st>>>(p);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_cpasync(const SpmmParams& p, const Plan& plan, cudaStream_t st) {
     if (plan.bf16) return launch_cpasync_bf16(p, plan, st);
+    if (plan.halfwarp) {
+        switch (plan.stages) {
+            case 2: return plan.minb >= 5 ? launch_cpasync_hw_k<2, 5>(p, st) : launch_cpasync_hw_k<2, 4>(p, st);
+            case 8: return plan.minb >= 5 ? launch_cpasync_hw_k<8, 5>(p, st) : launch_cpasync_hw_k<8, 4>(p, st);
+            default: return plan.minb >= 5 ? launch_cpasync_hw_k<4, 5>(p, st) : launch_cpasync_hw_k<4, 4>(p, st);
+        }
+    }
     // Register caps that force spills made this kernel trap with cudaErrorIllegalInstruction on
     // B200 (MINB 8 for f32, 6 for bf16; profiles/r01.md) -- _build.py rejects any spilling
     // spmm_cpasync instantiation, so MINB 5 (48 registers, 40 warps/SM) is the ceiling.
@@ -907,6 +1038,9 @@ Plan make_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C
         pl.nch = (int)((nv4 + 31) / 32);
         pl.stages = env_int("ES_SPMM_STAGES", 4);
         pl.minb = env_int("ES_SPMM_MINB", pl.nch == 1 ? 5 : 1);
+        // two slots per step for F <= 128 (profiles/r01.md: Reddit F=128 1.88 vs 1.99 ms,
+        // Proteins 1.19 vs 1.30 ms); ES_SPMM_HALFWARP=0 selects the one-slot ring
+        pl.halfwarp = pl.nch == 1 && env_int("ES_SPMM_HALFWARP", 1) != 0;
     }
     if (pl.tma) {
         pl.nch = (int)((nv4 + 31) / 32);

@@ -95,12 +95,17 @@ FS = [(1, 1), (3, 3), (3, 4), (7, 8), (16, 16), (17, 17), (32, 32), (64, 64), (1
       (128, 128), (129, 132), (256, 256), (602, 602), (602, 604), (1000, 1000), (1100, 1104)]
 
 
-@pytest.fixture(params=["auto", "warp", "tma", "cpasync"])
+@pytest.fixture(params=["auto", "warp", "tma", "cpasync", "halfwarp"])
 def kernel(request, monkeypatch):
     """Run a test under the automatic plan and with each kernel family forced where it
-    applies (TMA ring, LDG warp-per-row, LDG register-ring stream)."""
+    applies (TMA ring, LDG warp-per-row, cp.async ring, cp.async ring with two slots per step)."""
+    monkeypatch.setenv("ES_SPMM_HALFWARP", "0")
     if request.param == "auto":
+        monkeypatch.delenv("ES_SPMM_HALFWARP", raising=False)
         monkeypatch.delenv("ES_SPMM_KERNEL", raising=False)
+    elif request.param == "halfwarp":
+        monkeypatch.setenv("ES_SPMM_KERNEL", "cpasync")
+        monkeypatch.setenv("ES_SPMM_HALFWARP", "1")
     else:
         monkeypatch.setenv("ES_SPMM_KERNEL", request.param)
     return request.param

@@ -70,8 +70,11 @@ def test_host_validation_rejects_bad_arguments(lib):
 
 
 def test_plan_selection(lib, monkeypatch):
-    assert es.es_spmm_plan(128, 128, 128).startswith("es::spmm_cpasync<stages4>")
+    assert es.es_spmm_plan(128, 128, 128).startswith("es::spmm_cpasync_hw<stages4>")
     assert es.es_spmm_plan(200, 200, 200).startswith("es::spmm_cpasync<stages4>")
+    monkeypatch.setenv("ES_SPMM_HALFWARP", "0")
+    assert es.es_spmm_plan(128, 128, 128).startswith("es::spmm_cpasync<stages4>")
+    monkeypatch.delenv("ES_SPMM_HALFWARP")
     assert es.es_spmm_plan(256, 256, 256).startswith("es::spmm_cpasync<stages4>")
     assert es.es_spmm_plan(512, 512, 512).startswith("es::spmm_cpasync<stages4>")
     assert es.es_spmm_plan(602, 604, 604).startswith("es::spmm_tma<nch5,stages4>")
