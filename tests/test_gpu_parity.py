@@ -302,7 +302,7 @@ def test_full_proteins():
     _full("proteins", 128, 128, 256, ES_FASTRAND, 0, ES_REDUCE_SUM)
 
 
-@pytest.mark.parametrize("F,ldb", [(602, 604), (128, 128)])
+@pytest.mark.parametrize("F,ldb", [(602, 608), (602, 604), (128, 128)])   # 608 = bench.py layout
 @pytest.mark.parametrize("strat", STRATS)
 def test_full_reddit(F, ldb, strat, kernel):
     _full("reddit", F, ldb, 256, strat, 0, ES_REDUCE_MEAN)
