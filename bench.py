@@ -2,9 +2,12 @@
 """Benchmark of the ES-SpMM hot path (BASELINE.json metric) on 1..8 B200s.
 
 One "step" = one pass of the whole hot path (degree/cap, sampling,
-staging, gather-FMA, epilogue) over the configured graph: ONE fused kernel launch per
-rank (es_spmm_run_rows on the rank's row block).  Inputs are resident in HBM when the
-timed region starts; L2 is flushed (256 MiB write) before every timed step.
+staging, gather-FMA, epilogue) over the configured graph, as ONE library call per rank on
+the rank's row block: es_spmm_run_ex with a workspace when the library asks for one (the
+feature-sliced path for B beyond L2: count + scan + sample materialisation + one slab kernel
+per 64-float feature slice), else the single fused kernel (es_spmm_run_rows).  Inputs are
+resident in HBM when the timed region starts; L2 is flushed (256 MiB write) before every
+timed step.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config reddit] [--F 602]
                   [--s 256] [--strategy fastrand|bucket] [--reduce mean|sum]
@@ -52,8 +55,9 @@ def parse():
     ap.add_argument("--reduce", default=None, choices=["sum", "mean"])
     ap.add_argument("--seed", type=int, default=0, help="FastRand seed (0 = paper-exact Eq. 2)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--kernel", default="auto", choices=["auto", "tma", "warp"],
-                    help="kernel family (A/B measurement; auto = the library's plan)")
+    ap.add_argument("--kernel", default="auto", choices=["auto", "fused", "slab", "tma", "warp"],
+                    help="kernel family (A/B measurement; auto = the library's plan, fused = never the "
+                         "feature-sliced path, slab = always where it applies)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true", help="warm-L2 variant (not the headline)")
@@ -73,8 +77,10 @@ def parse():
             setattr(a, k, d[k])
     if a.warmup < 3:
         a.warmup = 3
-    if a.kernel != "auto":
+    if a.kernel in ("tma", "warp"):
         os.environ["ES_SPMM_KERNEL"] = a.kernel
+    if a.kernel != "auto":
+        os.environ["ES_SPMM_SLAB"] = "1" if a.kernel == "slab" else "0"
     return a
 
 
@@ -251,9 +257,17 @@ def main():
     if a.allgather:
         from paper_2104_10716_b200.dist import PeerBuffers
         peers = PeerBuffers(n, C_d.stride(0), device=dev)
+    # the library's plan: a workspace (allocated once, outside the timed region) selects the
+    # feature-sliced path when B does not fit L2 but a 64-float slab of it does
+    ws = None
+    if peers is None and not a.bf16:
+        ws = es.es_spmm_workspace(r1 - r0, n, e1 - e0, F, ldb, a.s, True, device=dev)
 
     def launch(st):
-        if peers is not None:
+        if ws is not None:
+            es.es_spmm_run_ex(rp_d, ci_d, va_d, B_d, a.s, strat_id, a.seed, red_id, F=F, C=C_d,
+                              row_begin=r0, row_end=r1, n_rows=n, nnz_base=e0, workspace=ws, stream=st)
+        elif peers is not None:
             es.es_spmm_run_ex(rp_d, ci_d, va_d, B_d, a.s, strat_id, a.seed, red_id, F=F, C=peers.C,
                               row_begin=r0, row_end=r1, n_rows=n, nnz_base=e0, c_peers=peers.peers,
                               n_peers=peers.world, stream=st)
@@ -338,7 +352,7 @@ def main():
         try:
             with open(prof) as f:
                 tj = json.load(f)
-            key = f"{a.config}|F{F}|s{a.s}|{a.strategy}|{a.reduce}"
+            key = f"{a.config}|F{F}|s{a.s}|{a.strategy}|{a.reduce}" + ("|slab" if ws is not None else "")
             if key in tj and world == 1:
                 traffic = tj[key]["dram_bytes_per_launch"]
         except Exception:
@@ -349,7 +363,12 @@ def main():
                 "bytes_per_launch": bytes_rank,
                 "bytes_model": ("8K + 8(N+1) + 2FK + 4FN (bf16 B)" if a.bf16 else
                                 "8K + 8(N+1) + 4FK + 4FN (sampled colind+val, rowptr, B gathers, C)"),
-                "kernel": "es::spmm_cpasync<bf16>" if a.bf16 else es.es_spmm_plan(F, ldb, C_d.stride(0), B_d, C_d)}
+                "kernel": ("es::spmm_cpasync<bf16>" if a.bf16 else
+                           f"es::spmm_slab<G{os.environ.get('ES_SPMM_SLAB_G', '8')},"
+                           f"D{os.environ.get('ES_SPMM_SLAB_STAGES', '4')}> x{(F + 63) // 64} feature slices "
+                           f"+ sample_count/scan/sample_materialize (the step's {launches_per_step} launches: "
+                           f"achieved = the step's algorithmic bytes / step time)" if ws is not None else
+                           es.es_spmm_plan(F, ldb, C_d.stride(0), B_d, C_d))}
 
     # ---------------- end to end through the public host API (pinned host buffers)
     e2e = None

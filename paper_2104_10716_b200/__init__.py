@@ -24,7 +24,7 @@ LIB_PATH = os.path.join(_HERE, "libesspmm.so")
 EXPORTS = ("es_spmm_sample", "es_spmm_run", "es_spmm_run_rows", "es_spmm_backward",
            "es_spmm_run_ex", "es_spmm_sample_ex", "es_spmm_backward_ex", "es_spmm_host_workspace_bytes",
            "es_ipc_handle_bytes", "es_ipc_alloc", "es_ipc_free", "es_ipc_export", "es_ipc_import", "es_ipc_close",
-           "es_spmm_run_host", "es_partition_rows", "es_spmm_plan", "es_launch_count",
+           "es_spmm_run_host", "es_partition_rows", "es_spmm_plan", "es_launch_count", "es_spmm_workspace_bytes",
            "es_status_string")
 
 _lib = None
@@ -39,13 +39,16 @@ class EsOptions(ctypes.Structure):
     _fields_ = [("struct_size", ctypes.c_int32), ("prime", ctypes.c_int32),
                 ("mean_divisor", ctypes.c_int32), ("b_dtype", ctypes.c_int32),
                 ("c_peers", ctypes.c_void_p), ("n_peers", ctypes.c_int32),
-                ("deterministic", ctypes.c_int32)]
+                ("deterministic", ctypes.c_int32), ("workspace", ctypes.c_void_p),
+                ("workspace_bytes", ctypes.c_int64)]
 
     @classmethod
     def make(cls, prime: int = 0, mean_by_degree: bool = False, bf16: bool = False, c_peers=None,
-             n_peers: int = 0, deterministic: bool = False):
+             n_peers: int = 0, deterministic: bool = False, workspace=None):
+        ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
         return cls(ctypes.sizeof(cls), prime, ES_MEAN_BY_DEGREE if mean_by_degree else ES_MEAN_BY_SAMPLED,
-                   ES_DTYPE_BF16 if bf16 else ES_DTYPE_F32, _ptr(c_peers), n_peers, int(deterministic))
+                   ES_DTYPE_BF16 if bf16 else ES_DTYPE_F32, _ptr(c_peers), n_peers, int(deterministic),
+                   _ptr(workspace), ws_bytes)
 
 
 def load_library(path: str = LIB_PATH):
@@ -98,6 +101,8 @@ def load_library(path: str = LIB_PATH):
     lib.es_spmm_run_host.restype = st
     lib.es_spmm_run_host.argtypes = [i64, i64, vp, vp, vp, vp, i64, i64, i32, i32, u64, i32, i64, vp,
                                      i64, vp, i64, vp]
+    lib.es_spmm_workspace_bytes.restype = i64
+    lib.es_spmm_workspace_bytes.argtypes = [i64, i64, i64, i64, i64, i32, i32]
     lib.es_partition_rows.restype = st
     lib.es_partition_rows.argtypes = [vp, i64, i32, i64, i32, vp]
     lib.es_spmm_plan.restype = st
@@ -226,11 +231,12 @@ def es_spmm_run_ex(rowptr, colind, val, B, s: int, strategy: int, seed: int = 0,
                    reduce: int = ES_REDUCE_SUM, F: int | None = None, C=None, prime: int = 0,
                    mean_by_degree: bool = False, row_begin: int = 0, row_end: int | None = None,
                    n_rows: int | None = None, nnz_base: int = 0, c_peers=None, n_peers: int = 0,
-                   stream=None):
+                   workspace=None, stream=None):
     """es_spmm_run_rows with the options: P' override, MEAN by original degree, bf16 storage of
-    B (pass a torch.bfloat16 B; accumulation stays fp32) -- NEXT-4 -- and the fused all-gather
+    B (pass a torch.bfloat16 B; accumulation stays fp32) -- NEXT-4 -- the fused all-gather
     (c_peers: int64 CUDA tensor of n_peers full-C base pointers; C = this rank's full C) --
-    NEXT-1, see paper_2104_10716_b200.dist.PeerBuffers."""
+    NEXT-1, see paper_2104_10716_b200.dist.PeerBuffers -- and the slab path's workspace (a
+    CUDA uint8 tensor of es_spmm_workspace_bytes(...) bytes, or None)."""
     import torch
     _dev(rowptr, torch.int64, "rowptr")
     _dev(colind, torch.int32, "colind")
@@ -247,12 +253,27 @@ def es_spmm_run_ex(rowptr, colind, val, B, s: int, strategy: int, seed: int = 0,
         n_rows = row_end
     if C is None:
         C = torch.empty((row_end - row_begin, F), dtype=torch.float32, device=B.device)
-    opt = EsOptions.make(prime, mean_by_degree, B.dtype == torch.bfloat16, c_peers, n_peers)
+    opt = EsOptions.make(prime, mean_by_degree, B.dtype == torch.bfloat16, c_peers, n_peers,
+                         workspace=workspace)
     _check(load_library().es_spmm_run_ex(n_rows, B.shape[0], _ptr(rowptr), nnz_base, _ptr(colind), _ptr(val),
                                          _ptr(B), F, ldb, s, strategy, seed & (2**64 - 1), reduce, _ptr(C),
                                          C.stride(0), row_begin, row_end, ctypes.byref(opt), _stream(stream)),
            "es_spmm_run_ex")
     return C
+
+
+def es_spmm_workspace_bytes(n_rows: int, n_cols: int, nnz: int, F: int, ldb: int, s: int,
+                            has_val: bool = True) -> int:
+    """Workspace bytes for es_spmm_run_ex's slab path (0: the shape does not take it)."""
+    return int(load_library().es_spmm_workspace_bytes(n_rows, n_cols, nnz, F, ldb, s, int(bool(has_val))))
+
+
+def es_spmm_workspace(n_rows: int, n_cols: int, nnz: int, F: int, ldb: int, s: int, has_val: bool = True,
+                      device=None):
+    """A workspace tensor for es_spmm_run_ex (None when the slab path is not taken)."""
+    import torch
+    nb = es_spmm_workspace_bytes(n_rows, n_cols, nnz, F, ldb, s, has_val)
+    return torch.empty(nb, dtype=torch.uint8, device=device) if nb > 0 else None
 
 
 def es_spmm_sample_ex(rowptr, colind, val, s: int, strategy: int, seed: int = 0, row_base: int = 0,

@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["es_kernels.cu", "es_backward_det.cu", "es_abi.cu"]
+SOURCES = ["es_kernels.cu", "es_slab.cu", "es_backward_det.cu", "es_abi.cu"]
 HEADERS = ["es_device.cuh", "es_internal.h"]
 LIB = os.path.join(HERE, "libesspmm.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -38,7 +38,7 @@ def _check_no_spills(ptxas_log: str, src: str) -> None:
     for line in ptxas_log.splitlines():
         if "Compiling entry function" in line:
             entry = line.split("'")[1] if "'" in line else line
-        elif "spill stores" in line and entry and "spmm_cpasync" in entry:
+        elif "spill stores" in line and entry and ("spmm_cpasync" in entry or "spmm_slab" in entry):
             stores = int(line.split("bytes spill stores")[0].split(",")[-1].strip().split()[0])
             if stores:
                 raise RuntimeError(f"{src}: {entry} spills ({line.strip()}); lower its MINB")

@@ -4,6 +4,7 @@
 #include <atomic>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstddef>
 #include <cstring>
 #include <vector>
@@ -34,6 +35,8 @@ struct Opts {
     float* const* c_peers = nullptr;
     int32_t n_peers = 0;
     int32_t deterministic = 0;
+    void* workspace = nullptr;
+    int64_t workspace_bytes = 0;
 };
 
 es_status_t read_opts(const es_spmm_options_t* o, Opts* out) {
@@ -51,8 +54,48 @@ es_status_t read_opts(const es_spmm_options_t* o, Opts* out) {
         out->c_peers = o->c_peers;
         out->n_peers = o->n_peers;
     }
-    if (o->struct_size >= (int32_t)sizeof(es_spmm_options_t)) out->deterministic = o->deterministic != 0;
+    if (o->struct_size >= (int32_t)offsetof(es_spmm_options_t, workspace)) out->deterministic = o->deterministic != 0;
+    if (o->struct_size >= (int32_t)sizeof(es_spmm_options_t)) {
+        if (o->workspace_bytes < 0 || (o->workspace_bytes > 0 && !o->workspace)) return ES_ERR_INVALID_VALUE;
+        out->workspace = o->workspace;
+        out->workspace_bytes = o->workspace_bytes;
+    }
     return ES_OK;
+}
+
+// ---- slab path (es_slab.cu): when, and the workspace layout
+constexpr int64_t kSlabF = 64;                       // floats per feature slice (256-B slab rows)
+
+int64_t env_i64(const char* name, int64_t dflt) {
+    const char* e = getenv(name);
+    return e ? atoll(e) : dflt;
+}
+
+// Shape-only choice: B (n_cols x ldb fp32) does not fit L2 but a 64-float slab of it does.
+// ES_SPMM_SLAB=0 disables, =1 forces (tuning / A-B measurement).
+bool slab_wanted(int64_t n_cols, int64_t F, int64_t ldb) {
+    const int64_t force = env_i64("ES_SPMM_SLAB", -1);
+    if (force == 0 || F <= kSlabF / 4) return false;
+    if (force == 1) return true;
+    const int64_t l2_b = env_i64("ES_SPMM_SLAB_MIN_B_MB", 96) << 20;    // B beyond this: slice
+    const int64_t slab_max = env_i64("ES_SPMM_SLAB_MAX_SLAB_MB", 80) << 20;
+    return F >= env_i64("ES_SPMM_SLAB_MIN_F", 128) && n_cols * ldb * 4 > l2_b &&
+           n_cols * kSlabF * 4 <= slab_max;
+}
+
+int64_t slab_align(int64_t x) { return (x + 255) & ~(int64_t)255; }
+
+struct SlabLayout {
+    int64_t off_rowptr, off_temp, temp_bytes, off_col, off_val, bytes_fixed;
+};
+SlabLayout slab_layout(int64_t n) {
+    SlabLayout L{};
+    L.off_rowptr = 0;
+    L.off_temp = slab_align(8 * (n + 1));
+    L.temp_bytes = (int64_t)es::slab_scan_temp_bytes(n);
+    L.off_col = slab_align(L.off_temp + L.temp_bytes);
+    L.bytes_fixed = L.off_col;
+    return L;
 }
 
 es_status_t run_rows_impl(int64_t n_rows, int64_t n_cols, const int64_t* rowptr, int64_t nnz_base,
@@ -89,6 +132,53 @@ es_status_t run_rows_impl(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
     p.n_peers = o.n_peers;
     const es::Plan plan = o.bf16 ? es::make_plan_bf16(F, ldb, ldc, B, C) : es::make_plan(F, ldb, ldc, B, C);
     if (plan.unsupported) return ES_ERR_UNSUPPORTED;
+    const uintptr_t bu = reinterpret_cast<uintptr_t>(B), cu = reinterpret_cast<uintptr_t>(C);
+    if (o.workspace && !o.bf16 && o.n_peers == 0 && bu % 16 == 0 && ldb % 4 == 0 && cu % 16 == 0 &&
+        ldc % 4 == 0 && slab_wanted(n_cols, F, ldb)) {
+        const SlabLayout L = slab_layout(n);
+        const int64_t per_slot = val ? 8 : 4;
+        const int64_t cap = (o.workspace_bytes - L.bytes_fixed - 256) / per_slot;
+        if (cap >= 1) {
+            char* ws = static_cast<char*>(o.workspace);
+            int64_t* s_rowptr = reinterpret_cast<int64_t*>(ws + L.off_rowptr);
+            int32_t* s_col = reinterpret_cast<int32_t*>(ws + L.off_col);
+            float* s_val = val ? reinterpret_cast<float*>(ws + slab_align(L.off_col + 4 * cap)) : nullptr;
+            int launches = 0;
+            cudaError_t err = es::launch_slab_count(rowptr, n, s, s_rowptr, ws + L.off_temp,
+                                                    (size_t)L.temp_bytes, st, &launches);
+            if (err == cudaSuccess) {
+                err = es::launch_sample_materialize(rowptr, nnz_base, colind, val, n, s, strategy, seed,
+                                                    row_begin, o.prime, s_rowptr, s_col, s_val, nullptr, st,
+                                                    cap);
+                ++launches;
+            }
+            const int stages = (int)env_i64("ES_SPMM_SLAB_STAGES", 4);
+            const int lanes = (int)env_i64("ES_SPMM_SLAB_G", 8);
+            for (int64_t c0 = 0; err == cudaSuccess && c0 < F; c0 += kSlabF) {
+                es::SlabParams sp{};
+                sp.s_rowptr = s_rowptr;
+                sp.slot_base = 0;
+                sp.cap = cap;
+                sp.s_colind = s_col;
+                sp.s_val = s_val;
+                sp.rowptr = rowptr;
+                sp.B = static_cast<const float*>(B) + c0;
+                sp.ldb = ldb;
+                sp.w = (int32_t)(F - c0 < kSlabF ? F - c0 : kSlabF);
+                sp.nv = (sp.w + 3) / 4;
+                sp.C = C + c0;
+                sp.ldc = ldc;
+                sp.c_vec = 1;
+                sp.n_rows = n;
+                sp.reduce = reduce;
+                sp.mean_by_degree = o.mean_by_degree;
+                err = es::launch_slab_pass(sp, lanes, stages, st);
+                ++launches;
+            }
+            g_launches.fetch_add(launches, std::memory_order_relaxed);
+            return err == cudaSuccess ? ES_OK : ES_ERR_CUDA;
+        }
+    }
     cudaError_t err = es::launch_spmm(p, plan, st);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return err == cudaSuccess ? ES_OK : ES_ERR_CUDA;
@@ -110,6 +200,15 @@ const char* es_status_string(es_status_t status) {
 }
 
 int64_t es_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+int64_t es_spmm_workspace_bytes(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t F, int64_t ldb,
+                                int32_t s, int32_t has_val) {
+    if (n_rows <= 0 || n_cols < 0 || nnz < 0 || F < 1 || ldb < F || s < 1) return 0;
+    if (!slab_wanted(n_cols, F, ldb)) return 0;
+    const SlabLayout L = slab_layout(n_rows);
+    const int64_t cap = nnz < n_rows * (int64_t)s ? nnz : n_rows * (int64_t)s;
+    return L.bytes_fixed + 256 + slab_align(4 * (cap > 0 ? cap : 1)) + (has_val ? 4 * (cap > 0 ? cap : 1) : 0) + 256;
+}
 
 es_status_t es_spmm_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C,
                          char* buf, int32_t buf_len) {

@@ -63,6 +63,34 @@ struct BwdParams {
     int32_t mean_by_degree;
 };
 
+// One feature slice of the slab path (es_slab.cu): C[:, 0:w] of the slice from the compact
+// sampled slots (es_spmm_sample layout) and the slice's B columns.
+struct SlabParams {
+    const int64_t* s_rowptr;  // local row r: slots [s_rowptr[r] - slot_base, s_rowptr[r+1] - slot_base)
+    int64_t slot_base;
+    int64_t cap;              // slots the workspace holds (reads are clamped to it)
+    const int32_t* s_colind;
+    const float* s_val;       // NULL => 1.0
+    const int64_t* rowptr;    // original CSR rows (MEAN by degree only)
+    const float* B;           // the slice's first column, row pitch ldb (16-B aligned)
+    int64_t ldb;
+    int32_t w;                // floats in the slice (<= 64)
+    int32_t nv;               // 16-B pieces in the slice = ceil(w / 4) (<= 16)
+    float* C;                 // the slice's first column of local row 0
+    int64_t ldc;
+    int32_t c_vec;
+    int64_t n_rows;
+    int32_t reduce;
+    int32_t mean_by_degree;
+};
+
+cudaError_t launch_slab_pass(const SlabParams& p, int lanes_per_slot, int stages, cudaStream_t st);
+size_t slab_scan_temp_bytes(int64_t n);
+cudaError_t launch_slab_count(const int64_t* rowptr, int64_t n, int32_t s, int64_t* s_rowptr, void* temp,
+                              size_t temp_bytes, cudaStream_t st, int* launches);
+cudaError_t launch_sample_count_only(const int64_t* rowptr, int64_t n, int32_t s, int64_t* s_rowptr,
+                                     cudaStream_t st);
+
 cudaError_t launch_backward(const BwdParams& p, cudaStream_t st);
 cudaError_t launch_backward_deterministic(const BwdParams& p, int64_t n_cols, cudaStream_t st, int* launches,
                                           bool* too_large);
@@ -76,6 +104,6 @@ cudaError_t launch_sample_materialize(const int64_t* rowptr, int64_t nnz_base, c
                                       const float* val, int64_t n, int32_t s, int32_t strategy,
                                       uint64_t seed, int64_t row_base, uint32_t prime,
                                       const int64_t* s_rowptr, int32_t* s_colind, float* s_val,
-                                      int64_t* s_pos, cudaStream_t st);
+                                      int64_t* s_pos, cudaStream_t st, int64_t cap = INT64_MAX);
 
 }  // namespace es

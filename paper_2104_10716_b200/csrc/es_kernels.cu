@@ -789,14 +789,14 @@ sample_materialize(const int64_t* __restrict__ rowptr, int64_t nnz_base,
                    const int32_t* __restrict__ colind, const float* __restrict__ val, int64_t n,
                    int32_t s, int32_t strategy, uint64_t seed, int64_t row_base, uint32_t prime,
                    const int64_t* __restrict__ s_rowptr, int32_t* __restrict__ s_colind,
-                   float* __restrict__ s_val, int64_t* __restrict__ s_pos) {
+                   float* __restrict__ s_val, int64_t* __restrict__ s_pos, int64_t cap) {
     const int lane = threadIdx.x & 31;
     const int64_t r = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
     if (r >= n) return;
     RowSampler rs;
     rs.init(rowptr[r] - nnz_base, rowptr[r + 1] - nnz_base, s, strategy, seed, row_base + r, prime);
     const int64_t o0 = s_rowptr[r];
-    for (int32_t j = lane; j < rs.k; j += 32) {
+    for (int32_t j = lane; j < rs.k && o0 + j < cap; j += 32) {
         const int64_t pj = rs.pos(j);
         const int64_t e = rs.beg + pj;
         s_colind[o0 + j] = colind[e];
@@ -1007,7 +1007,7 @@ Plan make_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C
     else if (b % 8 == 0 && ldb % 2 == 0) pl.vec = 2;
     else pl.vec = 1;
     const int64_t nv = (F + pl.vec - 1) / pl.vec;
-    if (nv <= 16) {
+    if (nv <= 16) {                  // (tuning: ES_SPMM_CPASYNC_MIN_NV4 lowers the cp.async bound)
         pl.subwarp = true;
         int g = 1;
         while (g < nv) g <<= 1;
@@ -1031,7 +1031,7 @@ Plan make_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C
     // cp.async ring: 16-B aligned B, 16 < F/4 <= 128 by default (profiles/r01.md: Reddit F=128
     // 1.95 vs 2.27 ms, F=256 3.13 vs 4.55 (TMA), F=512 7.23 vs 7.51 (TMA); F=602 TMA wins 9.4 vs
     // 10.4); forced up to F/4 <= 256 with ES_SPMM_KERNEL=cpasync.
-    pl.cpasync = pl.vec == 4 && nv4 > 16 && nv4 <= 32 * 8 &&
+    pl.cpasync = pl.vec == 4 && nv4 > env_int("ES_SPMM_CPASYNC_MIN_NV4", 16) && nv4 <= 32 * 8 &&
                  (ov == 3 || (ov == 0 && nv4 <= 32 * 4));
     if (pl.cpasync) {
         pl.tma = false;
@@ -1067,12 +1067,17 @@ cudaError_t launch_spmm(SpmmParams p, const Plan& plan, cudaStream_t st) {
     }
 }
 
-cudaError_t launch_sample_count(const int64_t* rowptr, int64_t n, int32_t s, int64_t* s_rowptr,
-                                cudaStream_t st, int* launches) {
+cudaError_t launch_sample_count_only(const int64_t* rowptr, int64_t n, int32_t s, int64_t* s_rowptr,
+                                     cudaStream_t st) {
     const int64_t blocks = (n + 1 + 255) / 256;
     sample_count<<<(unsigned)(blocks > 0 ? blocks : 1), 256, 0, st>>>(rowptr, n, s, s_rowptr);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sample_count(const int64_t* rowptr, int64_t n, int32_t s, int64_t* s_rowptr,
+                                cudaStream_t st, int* launches) {
+    cudaError_t err = launch_sample_count_only(rowptr, n, s, s_rowptr, st);
     ++*launches;
-    cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess || n == 0) return err;
     size_t temp_bytes = 0;
     err = cub::DeviceScan::InclusiveSum(nullptr, temp_bytes, s_rowptr + 1, s_rowptr + 1, n, st);
@@ -1090,12 +1095,12 @@ cudaError_t launch_sample_materialize(const int64_t* rowptr, int64_t nnz_base, c
                                       const float* val, int64_t n, int32_t s, int32_t strategy,
                                       uint64_t seed, int64_t row_base, uint32_t prime,
                                       const int64_t* s_rowptr, int32_t* s_colind, float* s_val,
-                                      int64_t* s_pos, cudaStream_t st) {
+                                      int64_t* s_pos, cudaStream_t st, int64_t cap) {
     if (n <= 0) return cudaSuccess;
     const int64_t blocks = (n + kWarps - 1) / kWarps;
     sample_materialize<<<(unsigned)blocks, kThreads, 0, st>>>(rowptr, nnz_base, colind, val, n, s,
                                                                strategy, seed, row_base, prime,
-                                                               s_rowptr, s_colind, s_val, s_pos);
+                                                               s_rowptr, s_colind, s_val, s_pos, cap);
     return cudaGetLastError();
 }
 

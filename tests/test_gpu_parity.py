@@ -5,6 +5,8 @@ Bars (BASELINE.json north_star):
   * fp32 values: |g - o| <= max(1e-5 |o|, 1e-6) with non-negative inputs (val in [0.5,1.5)
     or 1, B in [0,1)); signed B uses |g - o| <= 1e-5 * sum|val*B| + 1e-6 (cancellation).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -42,6 +44,20 @@ def to_dev(rowptr, colind, val):
             None if val is None else torch.from_numpy(np.ascontiguousarray(val)).to(DEV))
 
 
+def slab_forced():
+    return os.environ.get("ES_SPMM_SLAB") == "1"
+
+
+def run_any(rp, ci, v, Bd, s, strat, seed, reduce, F, C=None):
+    """es_spmm_run, or -- under the `slab` kernel param -- es_spmm_run_ex with a workspace (the
+    feature-sliced path)."""
+    if slab_forced():
+        n = rp.numel() - 1
+        ws = es.es_spmm_workspace(n, Bd.shape[0], ci.numel(), F, Bd.shape[1], s, v is not None, device=DEV)
+        return es.es_spmm_run_ex(rp, ci, v, Bd, s, strat, seed, reduce, F=F, C=C, workspace=ws)
+    return es.es_spmm_run(rp, ci, v, Bd, s, strat, seed, reduce, F=F, C=C)
+
+
 def run_gpu(rowptr, colind, val, B, s, strat, seed=0, reduce=ES_REDUCE_SUM, F=None, ldc=None):
     rp, ci, v = to_dev(rowptr, colind, val)
     Bd = torch.from_numpy(np.ascontiguousarray(B)).to(DEV)
@@ -50,7 +66,7 @@ def run_gpu(rowptr, colind, val, B, s, strat, seed=0, reduce=ES_REDUCE_SUM, F=No
     C = None
     if ldc is not None:
         C = torch.full((n, ldc), -7.0, dtype=torch.float32, device=DEV)
-    out = es.es_spmm_run(rp, ci, v, Bd, s, strat, seed, reduce, F=F, C=C)
+    out = run_any(rp, ci, v, Bd, s, strat, seed, reduce, F, C)
     torch.cuda.synchronize()
     return out.cpu().numpy()
 
@@ -95,7 +111,7 @@ FS = [(1, 1), (3, 3), (3, 4), (7, 8), (16, 16), (17, 17), (32, 32), (64, 64), (1
       (128, 128), (129, 132), (256, 256), (602, 602), (602, 604), (1000, 1000), (1100, 1104)]
 
 
-@pytest.fixture(params=["auto", "warp", "tma", "cpasync", "halfwarp"])
+@pytest.fixture(params=["auto", "warp", "tma", "cpasync", "halfwarp", "slab", "slab16"])
 def kernel(request, monkeypatch):
     """Run a test under the automatic plan and with each kernel family forced where it
     applies (TMA ring, LDG warp-per-row, cp.async ring, cp.async ring with two slots per step)."""
@@ -103,6 +119,10 @@ def kernel(request, monkeypatch):
     if request.param == "auto":
         monkeypatch.delenv("ES_SPMM_HALFWARP", raising=False)
         monkeypatch.delenv("ES_SPMM_KERNEL", raising=False)
+    elif request.param.startswith("slab"):         # feature-sliced path (es_slab.cu), forced
+        monkeypatch.delenv("ES_SPMM_KERNEL", raising=False)
+        monkeypatch.setenv("ES_SPMM_SLAB", "1")
+        monkeypatch.setenv("ES_SPMM_SLAB_G", "16" if request.param == "slab16" else "8")
     elif request.param == "halfwarp":
         monkeypatch.setenv("ES_SPMM_KERNEL", "cpasync")
         monkeypatch.setenv("ES_SPMM_HALFWARP", "1")
@@ -205,15 +225,21 @@ def test_row_slices_bitwise_equal_full(ragged, kernel):
     B = synth.dense(3001, 602, seed=8, ld=604)
     Bd = torch.from_numpy(B).to(DEV)
     rp, ci, v = to_dev(rowptr, colind, val)
-    full = es.es_spmm_run(rp, ci, v, Bd, 256, ES_FASTRAND, 99, ES_REDUCE_MEAN, F=602).cpu().numpy()
+    full = run_any(rp, ci, v, Bd, 256, ES_FASTRAND, 99, ES_REDUCE_MEAN, 602).cpu().numpy()
     bounds = es.es_partition_rows(rowptr, 256, 602, 3)
     for a, b in zip(bounds[:-1], bounds[1:]):
         e0, e1 = rowptr[a], rowptr[b]
         rps = torch.from_numpy(rowptr[a:b + 1].copy()).to(DEV)
         cis = torch.from_numpy(colind[e0:e1].copy()).to(DEV)
         vs = torch.from_numpy(val[e0:e1].copy()).to(DEV)
-        part = es.es_spmm_run_rows(len(rowptr) - 1, rps, int(e0), cis, vs, Bd, 256, ES_FASTRAND, 99,
-                                   ES_REDUCE_MEAN, int(a), int(b), F=602).cpu().numpy()
+        if slab_forced():
+            ws = es.es_spmm_workspace(int(b - a), 3001, int(e1 - e0), 602, 604, 256, True, device=DEV)
+            part = es.es_spmm_run_ex(rps, cis, vs, Bd, 256, ES_FASTRAND, 99, ES_REDUCE_MEAN, F=602,
+                                     row_begin=int(a), row_end=int(b), n_rows=len(rowptr) - 1,
+                                     nnz_base=int(e0), workspace=ws).cpu().numpy()
+        else:
+            part = es.es_spmm_run_rows(len(rowptr) - 1, rps, int(e0), cis, vs, Bd, 256, ES_FASTRAND, 99,
+                                       ES_REDUCE_MEAN, int(a), int(b), F=602).cpu().numpy()
         assert np.array_equal(part, full[a:b])
 
 
@@ -259,7 +285,7 @@ def _full(name, F, ldb, s, strat, seed, reduce, n_check=1500):
     val = np.ones(len(colind), np.float32)
     rp, ci, v = to_dev(rowptr, colind, val)
     Bd = torch.from_numpy(B).to(DEV)
-    C = es.es_spmm_run(rp, ci, v, Bd, s, strat, seed, reduce, F=F)
+    C = run_any(rp, ci, v, Bd, s, strat, seed, reduce, F)
     torch.cuda.synchronize()
     d = np.diff(rowptr)
     rng = np.random.default_rng(0)

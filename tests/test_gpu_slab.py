@@ -1,0 +1,138 @@
+"""The feature-sliced ("slab") path of es_spmm_run_ex (es_slab.cu) on the GPU:
+parity with the oracle (values within the 1e-5 bar, val NULL, MEAN by degree, the P' option),
+the documented per-element order (G = 16 is bitwise spmm_cpasync_hw), row blocks bitwise equal
+to the full launch, and the workspace contract."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2104_10716_b200 as es  # noqa: E402
+
+DEV = "cuda:0"
+
+
+def t(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def rel_ok(g, o, rtol=1e-5, atol=1e-6):
+    err = np.abs(np.asarray(g, np.float64) - np.asarray(o, np.float64))
+    return bool(np.all(err <= np.maximum(rtol * np.abs(o), atol))), float(err.max())
+
+
+@pytest.fixture(scope="module")
+def graph():
+    # several 8-row CTAs, a ragged tail, empty rows, rows past s, FastRand duplicate degrees
+    return synth.random_csr(1301, 2300, seed=41, max_deg=400, special=(577, 1154, 1009, 300, 65, 33, 1))
+
+
+@pytest.fixture(params=["8", "16"])
+def lanes(request, monkeypatch):
+    monkeypatch.setenv("ES_SPMM_SLAB", "1")
+    monkeypatch.setenv("ES_SPMM_SLAB_G", request.param)
+    monkeypatch.delenv("ES_SPMM_SLAB_STAGES", raising=False)
+    return int(request.param)
+
+
+def slab(rowptr, colind, val, B, s, strat, seed, reduce, F, **kw):
+    ws = es.es_spmm_workspace(len(rowptr) - 1, B.shape[0], len(colind), F, B.shape[1], s, val is not None,
+                              device=DEV)
+    assert ws is not None
+    vd = None if val is None else t(val)
+    return es.es_spmm_run_ex(t(rowptr), t(colind), vd, t(B), s, strat, seed, reduce, F=F, workspace=ws,
+                             **kw).cpu().numpy()
+
+
+@pytest.mark.parametrize("F,ld", [(17, 20), (64, 64), (65, 68), (200, 200), (602, 604), (602, 608)])
+@pytest.mark.parametrize("strat", [1, 2])
+def test_slab_parity(graph, lanes, F, ld, strat):
+    rowptr, colind, val = graph
+    B = synth.dense(2300, F, seed=F + 1, ld=ld)
+    for s, seed, reduce in [(32, 0, 0), (256, 5, 1), (1000, 0, 1), (1, 3, 0)]:
+        g = slab(rowptr, colind, val, B, s, strat, seed, reduce, F)
+        o = oracle.spmm(rowptr, colind, val, B, s, strat, seed=seed, reduce=reduce, F=F)
+        ok, err = rel_ok(g, o)
+        assert ok, (F, ld, s, seed, reduce, err)
+
+
+def test_slab_val_null_and_ones_exact(graph, lanes):
+    """val NULL (no slot values stored) and B == 1: C = k_i exactly (SUM), 1 (MEAN)."""
+    rowptr, colind, _ = graph
+    d = np.diff(rowptr)
+    B = np.ones((2300, 608), np.float32)
+    for s in (1, 64, 700):
+        for strat in (1, 2):
+            g = slab(rowptr, colind, None, B, s, strat, 3, 0, 602)
+            assert np.array_equal(g, np.repeat(np.minimum(d, s)[:, None], 602, 1).astype(np.float32))
+            gm = slab(rowptr, colind, None, B, s, strat, 3, 1, 602)
+            assert np.array_equal(gm, np.repeat((d > 0)[:, None], 602, 1).astype(np.float32))
+
+
+def test_slab_options(graph, lanes):
+    rowptr, colind, val = graph
+    B = synth.dense(2300, 300, seed=9, ld=300)
+    g = slab(rowptr, colind, val, B, 40, 2, 5, 1, 300, prime=7)
+    o = oracle.spmm(rowptr, colind, val, B, 40, 2, seed=5, reduce=1, F=300, prime=7)
+    assert rel_ok(g, o)[0]
+    d = np.diff(rowptr)
+    ones = np.ones((2300, 300), np.float32)
+    g = slab(rowptr, colind, None, ones, 64, 2, 0, 1, 300, mean_by_degree=True)
+    k = np.minimum(d, 64)
+    want = np.where(d > 0, k.astype(np.float32) / np.maximum(d, 1).astype(np.float32), 0).astype(np.float32)
+    assert np.array_equal(g, np.repeat(want[:, None], 300, 1))
+
+
+def test_g16_is_bitwise_cpasync_hw(graph, monkeypatch):
+    """The documented order: with 16 lanes per slot the slab kernel sums exactly as the fused
+    two-slots-per-step ring (spmm_cpasync_hw) does, so F <= 128 results are bitwise equal."""
+    rowptr, colind, val = graph
+    B = synth.dense(2300, 128, seed=4)
+    monkeypatch.setenv("ES_SPMM_KERNEL", "cpasync")
+    monkeypatch.setenv("ES_SPMM_HALFWARP", "1")
+    fused = es.es_spmm_run(t(rowptr), t(colind), t(val), t(B), 256, 2, 7, 1, F=128).cpu().numpy()
+    monkeypatch.setenv("ES_SPMM_SLAB", "1")
+    monkeypatch.setenv("ES_SPMM_SLAB_G", "16")
+    g = slab(rowptr, colind, val, B, 256, 2, 7, 1, 128)
+    assert np.array_equal(g, fused)
+
+
+def test_slab_row_blocks_bitwise(graph, lanes):
+    """Row blocks (es_spmm_run_ex on a CSR slice, global row ids) == the full launch, bitwise."""
+    rowptr, colind, val = graph
+    B = synth.dense(2300, 602, seed=8, ld=608)
+    full = slab(rowptr, colind, val, B, 256, 2, 99, 1, 602)
+    bounds = es.es_partition_rows(rowptr, 256, 602, 3)
+    for a, b in zip(bounds[:-1], bounds[1:]):
+        e0, e1 = int(rowptr[a]), int(rowptr[b])
+        ws = es.es_spmm_workspace(int(b - a), 2300, e1 - e0, 602, 608, 256, True, device=DEV)
+        part = es.es_spmm_run_ex(t(rowptr[a:b + 1]), t(colind[e0:e1]), t(val[e0:e1]), t(B), 256, 2, 99, 1,
+                                 F=602, row_begin=int(a), row_end=int(b), n_rows=len(rowptr) - 1,
+                                 nnz_base=e0, workspace=ws).cpu().numpy()
+        assert np.array_equal(part, full[a:b])
+
+
+def test_slab_ldc_padding_untouched(graph, lanes):
+    rowptr, colind, val = graph
+    B = synth.dense(2300, 130, seed=2, ld=132)
+    ws = es.es_spmm_workspace(1301, 2300, len(colind), 130, 132, 64, True, device=DEV)
+    C = torch.full((1301, 140), -7.0, dtype=torch.float32, device=DEV)
+    es.es_spmm_run_ex(t(rowptr), t(colind), t(val), t(B), 64, 1, 0, 0, F=130, C=C, workspace=ws)
+    Ch = C.cpu().numpy()
+    assert np.all(Ch[:, 130:] == -7.0)
+    o = oracle.spmm(rowptr, colind, val, B, 64, 1, F=130)
+    assert rel_ok(Ch[:, :130], o)[0]
+
+
+def test_auto_plan_takes_slab_only_for_wide_uncached_b():
+    # Reddit-shaped F=602: B (566 MB) > L2, a 64-float slab (60 MB) fits -> workspace wanted
+    assert es.es_spmm_workspace_bytes(232965, 232965, 114615945, 602, 608, 256) > 0
+    # B fits L2 (Proteins-shaped F=128, 68 MB) or is too tall for any slab (10M rows) -> none
+    assert es.es_spmm_workspace_bytes(132534, 132534, 79_100_000, 128, 128, 256) == 0
+    assert es.es_spmm_workspace_bytes(10_000_000, 10_000_000, 10**9, 256, 256, 128) == 0

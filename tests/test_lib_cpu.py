@@ -166,3 +166,23 @@ def test_options_validation(lib):
     # backward has no bf16 variant
     assert lib.es_spmm_backward_ex(10, 10, dummy, 0, dummy, None, dummy, 8, 8, 4, 2, 0, 0, dummy, 8, 0, 10,
                                    ctypes.byref(Opt.make(bf16=True)), None) == es.ES_ERR_UNSUPPORTED
+
+
+def test_workspace_bytes_plan(lib, monkeypatch):
+    """es_spmm_workspace_bytes (host only): the slab path is asked for exactly when B exceeds L2
+    and a 64-float slab of it fits, and the bound covers min(nnz, n*s) slots (+ values)."""
+    monkeypatch.delenv("ES_SPMM_SLAB", raising=False)
+    reddit = es.es_spmm_workspace_bytes(232965, 232965, 114615945, 602, 608, 256)
+    assert reddit >= 8 * 232965 * 256 + 8 * 232966            # n*s < nnz here: n*s slots
+    assert es.es_spmm_workspace_bytes(232965, 232965, 114615945, 602, 608, 256, has_val=False) < reddit
+    assert es.es_spmm_workspace_bytes(232965, 232965, 114615945, 128, 128, 256) > 0     # B 119 MB
+    assert es.es_spmm_workspace_bytes(132534, 132534, 79_100_000, 128, 128, 256) == 0   # B fits L2
+    assert es.es_spmm_workspace_bytes(10_000_000, 10_000_000, 10**9, 256, 256, 128) == 0  # slab > L2
+    assert es.es_spmm_workspace_bytes(232965, 232965, 114615945, 64, 64, 256) == 0      # one slice
+    small = es.es_spmm_workspace_bytes(232965, 232965, 1000, 602, 608, 256)
+    assert 8 * 1000 <= small - 8 * 232966 < 8 * 1000 + 4096                             # nnz < n*s
+    assert es.es_spmm_workspace_bytes(10, 10, 10, 602, 600, 4) == 0                     # ldb < F
+    monkeypatch.setenv("ES_SPMM_SLAB", "0")
+    assert es.es_spmm_workspace_bytes(232965, 232965, 114615945, 602, 608, 256) == 0
+    monkeypatch.setenv("ES_SPMM_SLAB", "1")
+    assert es.es_spmm_workspace_bytes(100, 100, 1000, 602, 608, 256) > 0
