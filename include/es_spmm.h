@@ -91,13 +91,14 @@ typedef struct {
      * stream once to size it; K and n_cols must be < 2^31, else ES_ERR_UNSUPPORTED). */
     int32_t deterministic;
     /* Feature-sliced ("slab") path (es_spmm_run_ex only).  A caller-owned device
-     * workspace of workspace_bytes >= es_spmm_workspace_bytes(...) bytes lets the call, when B
-     * does not fit L2 but a 64-float slab of it does, materialise the sampled slots once
-     * (es_spmm_sample's layout) and run the gather-FMA one 64-float feature slice at a time, each
-     * slice's B slab L2-resident.  Same C as the fused kernels within the parity bound (per
-     * element the slot order of spmm_cpasync_hw).  NULL (or a layout the path does not take:
-     * bf16 B, fused all-gather, unaligned B/C) = the fused kernels.  The workspace must not be
-     * used by another call in flight. */
+     * workspace of workspace_bytes >= es_spmm_workspace_bytes(...) bytes makes the call
+     * materialise the sampled slots once (es_spmm_sample's layout) and run the gather-FMA one
+     * 64-float feature slice at a time, each slice's B slab (n_cols x 256 B) L2-resident.  Pass
+     * it only when es_spmm_workspace_bytes returned > 0 (that is where it was measured faster);
+     * the call takes the path whenever a workspace is given and the slab fits L2.  Same C as
+     * the fused kernels within the parity bound.  NULL, or a layout the path does not take (bf16
+     * B, fused all-gather, B or C not 16-B aligned, F <= 16) = the fused kernels.  The
+     * workspace must not be shared by calls in flight. */
     void* workspace;
     int64_t workspace_bytes;
 } es_spmm_options_t;
@@ -105,8 +106,9 @@ typedef struct {
 /* Bytes of workspace es_spmm_run_ex needs to take the slab path for rows holding `nnz` stored
  * entries (nnz >= rowptr[row_end] - rowptr[row_begin] is a precondition like the CSR
  * invariants; the kernels never read or write past the workspace), sampling cap s, feature
- * width F, and B of n_cols rows with pitch ldb.  0 when the shape does not call for the slab
- * path (B fits L2, or a 64-float slab of it does not, or F <= 64): pass no workspace then.
+ * width F, and B of n_cols rows with pitch ldb.  > 0 when the measured plan prefers the slab
+ * path: F >= 128, a 64-float slab of B fits L2, and either B itself does not (> 96 MB) or
+ * rows are long (nnz >= 64 * n_rows).  0 otherwise: pass no workspace then.
  * has_val = 0 when val will be NULL (no slot values are stored). */
 int64_t es_spmm_workspace_bytes(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t F, int64_t ldb,
                                 int32_t s, int32_t has_val);

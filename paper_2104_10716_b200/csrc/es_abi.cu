@@ -71,16 +71,26 @@ int64_t env_i64(const char* name, int64_t dflt) {
     return e ? atoll(e) : dflt;
 }
 
-// Shape-only choice: B (n_cols x ldb fp32) does not fit L2 but a 64-float slab of it does.
-// ES_SPMM_SLAB=0 disables, =1 forces (tuning / A-B measurement).
-bool slab_wanted(int64_t n_cols, int64_t F, int64_t ldb) {
+// Run time (a workspace was passed): the slab path runs whenever it can -- F > 16 and a
+// 64-float slab of B (n_cols x 256 B) fits L2.  ES_SPMM_SLAB=0 disables, =1 forces.
+bool slab_feasible(int64_t n_cols, int64_t F) {
     const int64_t force = env_i64("ES_SPMM_SLAB", -1);
     if (force == 0 || F <= kSlabF / 4) return false;
     if (force == 1) return true;
+    return n_cols * kSlabF * 4 <= (env_i64("ES_SPMM_SLAB_MAX_SLAB_MB", 80) << 20);
+}
+
+// es_spmm_workspace_bytes's choice (measured, profiles/r01.md "Slab path"): feasible, F >= 128,
+// and either B does not fit L2 (Reddit-shaped: 9.8 -> 8.2 ms at F=602, 1.89 -> 1.71 at F=128)
+// or rows are long (>= 64 stored entries on average: Proteins-shaped F=128 1.21 -> 1.11 ms, B
+// L2-resident -- the 8-lane, 2-piece ring beats the fused two-slot ring); short rows keep the
+// single fused kernel (Arxiv-shaped: 0.19 fused vs 0.37 ms sliced).
+bool slab_wanted(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t F, int64_t ldb) {
+    if (!slab_feasible(n_cols, F)) return false;
+    if (env_i64("ES_SPMM_SLAB", -1) == 1) return true;
     const int64_t l2_b = env_i64("ES_SPMM_SLAB_MIN_B_MB", 96) << 20;    // B beyond this: slice
-    const int64_t slab_max = env_i64("ES_SPMM_SLAB_MAX_SLAB_MB", 80) << 20;
-    return F >= env_i64("ES_SPMM_SLAB_MIN_F", 128) && n_cols * ldb * 4 > l2_b &&
-           n_cols * kSlabF * 4 <= slab_max;
+    return F >= env_i64("ES_SPMM_SLAB_MIN_F", 128) &&
+           (n_cols * ldb * 4 > l2_b || nnz >= env_i64("ES_SPMM_SLAB_MIN_DEG", 64) * n_rows);
 }
 
 int64_t slab_align(int64_t x) { return (x + 255) & ~(int64_t)255; }
@@ -134,7 +144,7 @@ es_status_t run_rows_impl(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
     if (plan.unsupported) return ES_ERR_UNSUPPORTED;
     const uintptr_t bu = reinterpret_cast<uintptr_t>(B), cu = reinterpret_cast<uintptr_t>(C);
     if (o.workspace && !o.bf16 && o.n_peers == 0 && bu % 16 == 0 && ldb % 4 == 0 && cu % 16 == 0 &&
-        ldc % 4 == 0 && slab_wanted(n_cols, F, ldb)) {
+        ldc % 4 == 0 && slab_feasible(n_cols, F)) {
         const SlabLayout L = slab_layout(n);
         const int64_t per_slot = val ? 8 : 4;
         const int64_t cap = (o.workspace_bytes - L.bytes_fixed - 256) / per_slot;
@@ -204,7 +214,7 @@ int64_t es_launch_count(void) { return g_launches.load(std::memory_order_relaxed
 int64_t es_spmm_workspace_bytes(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t F, int64_t ldb,
                                 int32_t s, int32_t has_val) {
     if (n_rows <= 0 || n_cols < 0 || nnz < 0 || F < 1 || ldb < F || s < 1) return 0;
-    if (!slab_wanted(n_cols, F, ldb)) return 0;
+    if (!slab_wanted(n_rows, n_cols, nnz, F, ldb)) return 0;
     const SlabLayout L = slab_layout(n_rows);
     const int64_t cap = nnz < n_rows * (int64_t)s ? nnz : n_rows * (int64_t)s;
     return L.bytes_fixed + 256 + slab_align(4 * (cap > 0 ? cap : 1)) + (has_val ? 4 * (cap > 0 ? cap : 1) : 0) + 256;

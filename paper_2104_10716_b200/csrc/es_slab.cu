@@ -28,16 +28,10 @@ constexpr unsigned kAll = 0xffffffffu;
 
 // 16-B global -> shared copy, zero-filling when src_bytes == 0 (no global read is made): the
 // ring is refilled branch-free, slots past the row's end land as zeros.
-// CA: .ca (L1-allocating: hot B rows re-gathered by the SM's other warps hit in L1) instead of
-// .cg (L2 only).
-template <bool CA>
+// (.cg: L2 only -- the .ca form, L1-allocating, measured slower: profiles/r01.md)
 __device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const void* src, uint32_t src_bytes) {
-    if constexpr (CA)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" :: "r"(dst), "l"(src), "r"(src_bytes)
-                     : "memory");
-    else
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" :: "r"(dst), "l"(src), "r"(src_bytes)
-                     : "memory");
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" :: "r"(dst), "l"(src), "r"(src_bytes)
+                 : "memory");
 }
 
 __device__ __forceinline__ float4 lds128(uint32_t addr) {
@@ -54,13 +48,13 @@ __device__ __forceinline__ float4 lds128(uint32_t addr) {
 // consumed, into the stage it released.  Per element: group e sums slots j = e (mod S) in slot
 // order (32-slot-chunk partials), then an xor tree over the groups (G = 16: spmm_cpasync_hw's
 // order, bitwise).
-template <int G, int D, int MINB, bool FULL, bool CA>
+template <int G, int D, int MINB, bool FULL>
 __global__ void __launch_bounds__(kSlabThreads, MINB)
 spmm_slab(const SlabParams p) {
     constexpr int S = 32 / G;            // slots per step
     constexpr int P = 16 / G;            // pieces per lane
     constexpr int U = 32 / S;            // steps per 32-slot chunk (= G)
-    static_assert(G == 4 || G == 8 || G == 16, "lanes per slot");
+    static_assert(G == 8 || G == 16, "lanes per slot");
     static_assert(D >= 2 && U % D == 0, "ring depth must divide the steps of a chunk");
     constexpr int kStage = 32 * P;                               // float4 per warp stage
     extern __shared__ __align__(16) float4 slab_ring[];          // [warps][D][S][P][G]
@@ -83,7 +77,7 @@ spmm_slab(const SlabParams p) {
 #pragma unroll
         for (int q = 0; q < P; ++q) {
             const bool on = FULL ? valid : (valid && sub + G * q < p.nv);
-            cp_async16_zfill<CA>(my_s + (stage * kStage + q * G) * 16, src + q * G * 16, on ? 16u : 0u);
+            cp_async16_zfill(my_s + (stage * kStage + q * G) * 16, src + q * G * 16, on ? 16u : 0u);
         }
     };
     auto load_pair = [&](int64_t j, int32_t& c, float& a) {      // slot j of the row (coalesced)
@@ -177,141 +171,11 @@ spmm_slab(const SlabParams p) {
     }
 }
 
-// Register-staged variant (no shared memory): the cp.async ring above moves every B byte
-// through shared memory twice (LDGSTS write + LDS read), which made L1/shared bandwidth the
-// limit once the slab is L2-resident (profiles/r01.md: l1tex 79 % of peak).  Here each lane
-// LDGs its 16-B pieces straight into registers, U steps ahead of their use.  Same groups,
-// pieces and per-element order as spmm_slab<G>, so the two are bitwise interchangeable.
-template <int LD>
-__device__ __forceinline__ float4 ldg_piece(const char* src) {
-    float4 v;
-    if constexpr (LD == 0)       // L1-allocating (hot B rows are re-read by the SM's other warps)
-        asm volatile("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];"
-                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(src));
-    else
-        asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(src));
-    return v;
-}
-
-template <int G, int U, int MINB, bool FULL, int LD>
-__global__ void __launch_bounds__(kSlabThreads, MINB)
-spmm_slab_ldg(const SlabParams p) {
-    constexpr int S = 32 / G;            // slots per step
-    constexpr int P = 16 / G;            // pieces per lane
-    constexpr int NS = 32 / S;           // steps per 32-slot chunk
-    static_assert(G == 4 || G == 8 || G == 16, "lanes per slot");
-    static_assert(U >= 1 && NS % U == 0, "steps in flight must divide the steps of a chunk");
-    const int lane = threadIdx.x & 31;
-    const int e = lane / G, sub = lane % G;
-    const int64_t r = (int64_t)blockIdx.x * kSlabWarps + (threadIdx.x >> 5);
-    if (r >= p.n_rows) return;
-    const int64_t beg = ld_stream(p.s_rowptr + r, policy_evict_first()) - p.slot_base;
-    int64_t end = ld_stream(p.s_rowptr + r + 1, policy_evict_first()) - p.slot_base;
-    if (end > p.cap) end = p.cap;
-    const int32_t k = end > beg ? (int32_t)(end - beg) : 0;
-    const char* bl = reinterpret_cast<const char*>(p.B) + sub * 16;
-    const uint32_t row_bytes = (uint32_t)(p.ldb * 4);
-
-    float4 buf[U][P];
-    auto fetch = [&](int b, int32_t col, bool valid) {
-        const char* src = bl + (uint64_t)(uint32_t)col * row_bytes;
-#pragma unroll
-        for (int q = 0; q < P; ++q) {
-            const bool on = FULL ? valid : (valid && sub + G * q < p.nv);
-            if (on) buf[b][q] = ldg_piece<LD>(src + q * G * 16);
-            else buf[b][q] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-        }
-    };
-    auto load_pair = [&](int64_t j, int32_t& c, float& a) {
-        const uint64_t pol = policy_evict_first();
-        c = ld_stream(p.s_colind + beg + j, pol);
-        a = p.s_val ? ld_stream(p.s_val + beg + j, pol) : 1.0f;
-    };
-    int32_t c0 = 0, c1 = 0;
-    float a0 = 0.0f, a1 = 0.0f;
-    if (lane < k) load_pair(lane, c0, a0);
-    if (32 + lane < k) load_pair(32 + lane, c1, a1);
-#pragma unroll
-    for (int t = 0; t < U; ++t) fetch(t, __shfl_sync(kAll, c0, S * t + e), S * t + e < k);
-    float part[P][4], tot[P][4];
-#pragma unroll
-    for (int q = 0; q < P; ++q)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) { part[q][c] = 0.0f; tot[q][c] = 0.0f; }
-    for (int32_t j0 = 0; j0 < k; j0 += 32) {
-#pragma unroll
-        for (int u = 0; u < NS; ++u) {
-            const int b = u % U;
-            const float av = __shfl_sync(kAll, a0, S * u + e);
-#pragma unroll
-            for (int q = 0; q < P; ++q) {
-                part[q][0] = fmaf(av, buf[b][q].x, part[q][0]);
-                part[q][1] = fmaf(av, buf[b][q].y, part[q][1]);
-                part[q][2] = fmaf(av, buf[b][q].z, part[q][2]);
-                part[q][3] = fmaf(av, buf[b][q].w, part[q][3]);
-            }
-            const int tn = u + U;
-            const int32_t cn = __shfl_sync(kAll, tn < NS ? c0 : c1, (S * tn + e) & 31);
-            fetch(b, cn, j0 + S * tn + e < k);
-        }
-#pragma unroll
-        for (int q = 0; q < P; ++q)
-#pragma unroll
-            for (int c = 0; c < 4; ++c) { tot[q][c] += part[q][c]; part[q][c] = 0.0f; }
-        c0 = c1;
-        a0 = a1;
-        c1 = 0;
-        a1 = 0.0f;
-        if (j0 + 64 + lane < k) load_pair(j0 + 64 + lane, c1, a1);
-    }
-    const uint64_t pol_a = policy_evict_first();
-    int64_t div = k;
-    if (p.reduce == kMean && p.mean_by_degree)
-        div = ld_stream(p.rowptr + r + 1, pol_a) - ld_stream(p.rowptr + r, pol_a);
-#pragma unroll
-    for (int o = G; o < 32; o <<= 1)
-#pragma unroll
-        for (int q = 0; q < P; ++q)
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const float other = __shfl_xor_sync(kAll, tot[q][c], o);
-                tot[q][c] = (lane & o) ? other + tot[q][c] : tot[q][c] + other;
-            }
-    if (e == 0) {
-#pragma unroll
-        for (int q = 0; q < P; ++q) {
-            const int piece = sub + G * q;
-            if (FULL || piece < p.nv) {
-                float res[4];
-#pragma unroll
-                for (int c = 0; c < 4; ++c)
-                    res[c] = p.reduce == kMean ? (div > 0 ? __fdiv_rn(tot[q][c], (float)div) : 0.0f) : tot[q][c];
-                float* dst = p.C + r * p.ldc + piece * 4;
-                const int rem = p.w - piece * 4;
-                if (p.c_vec && rem >= 4) st_stream4(dst, res, pol_a);
-                else
-#pragma unroll
-                    for (int c = 0; c < 4; ++c)
-                        if (c < rem) st_stream(dst + c, res[c], pol_a);
-            }
-        }
-    }
-}
-
-template <int G, int U, int MINB, int LD>
-cudaError_t launch_slab_ldg_k(const SlabParams& p, cudaStream_t st) {
-    const int64_t blocks = (p.n_rows + kSlabWarps - 1) / kSlabWarps;
-    auto k = p.nv == 16 ? spmm_slab_ldg<G, U, MINB, true, LD> : spmm_slab_ldg<G, U, MINB, false, LD>;
-    k<<<(unsigned)blocks, kSlabThreads, 0, st>>>(p);
-    return cudaGetLastError();
-}
-
-template <int G, int D, int MINB, bool CA = false>
+template <int G, int D, int MINB>
 cudaError_t launch_slab_k(const SlabParams& p, cudaStream_t st) {
     const int64_t blocks = (p.n_rows + kSlabWarps - 1) / kSlabWarps;
     const size_t smem = (size_t)kSlabWarps * D * 32 * (16 / G) * 16;
-    auto k = p.nv == 16 ? spmm_slab<G, D, MINB, true, CA> : spmm_slab<G, D, MINB, false, CA>;
+    auto k = p.nv == 16 ? spmm_slab<G, D, MINB, true> : spmm_slab<G, D, MINB, false>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -322,35 +186,18 @@ cudaError_t launch_slab_k(const SlabParams& p, cudaStream_t st) {
 
 }  // namespace
 
+// Instantiations: G = 8 (default: 2 pieces per lane, 4 slots per step) or 16; D = 2, 4, 8.
+// MINB = the register cap that does not spill (spilling cp.async kernels trapped on B200,
+// _build.py refuses them).  Measured alternatives (register-staged LDG with every cache
+// operator, cp.async.ca, 4 lanes per slot, a row-stream variant over a padded layout) were
+// all slower: profiles/r01.md "Slab path".
 cudaError_t launch_slab_pass(const SlabParams& p, int lanes_per_slot, int stages, cudaStream_t st) {
     if (p.n_rows <= 0) return cudaSuccess;
-    // stages >= 100: register-staged variant, (stages - 100) % 10 = steps in flight U,
-    // (stages - 100) / 10 = 0 L1-allocating / 1 L1::no_allocate (tuning)
-    if (stages >= 100) {
-        const int u = (stages - 100) % 10, ld = (stages - 100) / 10;
-        if (lanes_per_slot == 16) {
-            if (ld) return u == 2 ? launch_slab_ldg_k<16, 2, 4, 1>(p, st) : launch_slab_ldg_k<16, 4, 3, 1>(p, st);
-            return u == 2 ? launch_slab_ldg_k<16, 2, 4, 0>(p, st) : launch_slab_ldg_k<16, 4, 3, 0>(p, st);
-        }
-        if (ld) return u == 2 ? launch_slab_ldg_k<8, 2, 3, 1>(p, st) : launch_slab_ldg_k<8, 4, 2, 1>(p, st);
-        return u == 2 ? launch_slab_ldg_k<8, 2, 3, 0>(p, st) : launch_slab_ldg_k<8, 4, 2, 0>(p, st);
-    }
-    if (stages >= 50) {              // 50 + D: the cp.async ring with .ca copies (tuning)
-        if (lanes_per_slot == 16) return stages == 58 ? launch_slab_k<16, 8, 5, true>(p, st)
-                                                      : launch_slab_k<16, 4, 6, true>(p, st);
-        return stages == 58 ? launch_slab_k<8, 8, 4, true>(p, st) : launch_slab_k<8, 4, 4, true>(p, st);
-    }
     if (lanes_per_slot == 16) {
         switch (stages) {
             case 2: return launch_slab_k<16, 2, 5>(p, st);
             case 8: return launch_slab_k<16, 8, 5>(p, st);
             default: return launch_slab_k<16, 4, 6>(p, st);
-        }
-    }
-    if (lanes_per_slot == 4) {
-        switch (stages) {
-            case 2: return launch_slab_k<4, 2, 3>(p, st);
-            default: return launch_slab_k<4, 4, 3>(p, st);
         }
     }
     switch (stages) {

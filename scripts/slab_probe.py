@@ -51,6 +51,9 @@ def main():
                 ts.append(e0.elapsed_time(e1))
         return float(np.median(ts)), float(min(ts))
 
+    # G:stages
+    variants = [tuple(x.split(":")) for x in os.environ.get("SLAB_VARIANTS", "16:4,8:4").split(",")]
+
     def clear():
         for k in [k for k in os.environ if k.startswith("ES_SPMM_")]:
             os.environ.pop(k)
@@ -59,7 +62,8 @@ def main():
     ms, mn = timed(lambda: es.es_spmm_run(rp, ci, va, Bd, s, 2, 0, 1, F=F, C=C))
     print(json.dumps({"variant": "fused", "plan": es.es_spmm_plan(F, ldb, ldb, Bd, C), "ms": round(ms, 3),
                       "min_ms": round(mn, 3), "algo_GBps": round(bm / ms / 1e6, 1)}), flush=True)
-    for g, st in [("16", "4"), ("8", "4"), ("16", "54"), ("16", "58"), ("8", "54"), ("8", "58")]:
+    for v in variants:
+        g, st = v[0], v[1]
         clear()
         os.environ["ES_SPMM_SLAB"] = "1"
         os.environ["ES_SPMM_SLAB_STAGES"] = st
@@ -69,7 +73,7 @@ def main():
         ms, mn = timed(lambda: es.es_spmm_run_ex(rp, ci, va, Bd, s, 2, 0, 1, F=F, C=C2, workspace=ws))
         d = (C2[:, :F] - C[:, :F]).abs().max().item()
         rel = ((C2[:, :F] - C[:, :F]).abs() / C[:, :F].abs().clamp_min(1e-6)).max().item()
-        print(json.dumps({"variant": f"slab G={g} stages={st}", "ws_MB": round(ws.numel() / 2**20, 1), "ms": round(ms, 3),
+        print(json.dumps({"variant": f"slab {':'.join(v)}", "ws_MB": round(ws.numel() / 2**20, 1), "ms": round(ms, 3),
                           "min_ms": round(mn, 3), "algo_GBps": round(bm / ms / 1e6, 1),
                           "max_abs_diff_vs_fused": d, "max_rel_diff_vs_fused": rel}), flush=True)
 

@@ -169,14 +169,15 @@ def test_options_validation(lib):
 
 
 def test_workspace_bytes_plan(lib, monkeypatch):
-    """es_spmm_workspace_bytes (host only): the slab path is asked for exactly when B exceeds L2
-    and a 64-float slab of it fits, and the bound covers min(nnz, n*s) slots (+ values)."""
+    """es_spmm_workspace_bytes (host only): the slab path is asked for when a 64-float slab of B
+    fits L2 and B does not, or rows are long; the bound covers min(nnz, n*s) slots (+ values)."""
     monkeypatch.delenv("ES_SPMM_SLAB", raising=False)
     reddit = es.es_spmm_workspace_bytes(232965, 232965, 114615945, 602, 608, 256)
     assert reddit >= 8 * 232965 * 256 + 8 * 232966            # n*s < nnz here: n*s slots
     assert es.es_spmm_workspace_bytes(232965, 232965, 114615945, 602, 608, 256, has_val=False) < reddit
     assert es.es_spmm_workspace_bytes(232965, 232965, 114615945, 128, 128, 256) > 0     # B 119 MB
-    assert es.es_spmm_workspace_bytes(132534, 132534, 79_100_000, 128, 128, 256) == 0   # B fits L2
+    assert es.es_spmm_workspace_bytes(132534, 132534, 79_100_000, 128, 128, 256) > 0    # long rows
+    assert es.es_spmm_workspace_bytes(169343, 169343, 2_330_000, 128, 128, 64) == 0     # short rows
     assert es.es_spmm_workspace_bytes(10_000_000, 10_000_000, 10**9, 256, 256, 128) == 0  # slab > L2
     assert es.es_spmm_workspace_bytes(232965, 232965, 114615945, 64, 64, 256) == 0      # one slice
     small = es.es_spmm_workspace_bytes(232965, 232965, 1000, 602, 608, 256)
