@@ -13,6 +13,7 @@
 // half adds its partial to its total every 32 slots; the two totals are added at the end --
 // the summation order of spmm_cpasync_hw, so results match that kernel bitwise.
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include <cub/device/device_scan.cuh>
 
@@ -48,8 +49,10 @@ __device__ __forceinline__ float4 lds128(uint32_t addr) {
 // consumed, into the stage it released.  Per element: group e sums slots j = e (mod S) in slot
 // order (32-slot-chunk partials), then an xor tree over the groups (G = 16: spmm_cpasync_hw's
 // order, bitwise).
-template <int G, int D, int MINB, bool FULL>
-__global__ void __launch_bounds__(kSlabThreads, MINB)
+// W warps per CTA (register cap as for MINB 256-thread CTAs per SM): small CTAs free their
+// slot as soon as their few rows are done instead of waiting for the longest of 8 rows.
+template <int G, int D, int MINB, bool FULL, int W>
+__global__ void __launch_bounds__(32 * W, MINB * 8 / W)
 spmm_slab(const SlabParams p) {
     constexpr int S = 32 / G;            // slots per step
     constexpr int P = 16 / G;            // pieces per lane
@@ -61,7 +64,7 @@ spmm_slab(const SlabParams p) {
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int e = lane / G, sub = lane % G;
-    const int64_t r = (int64_t)blockIdx.x * kSlabWarps + warp;
+    const int64_t r = (int64_t)blockIdx.x * W + warp;
     if (r >= p.n_rows) return;
     const int64_t beg = ld_stream(p.s_rowptr + r, policy_evict_first()) - p.slot_base;
     int64_t end = ld_stream(p.s_rowptr + r + 1, policy_evict_first()) - p.slot_base;
@@ -171,16 +174,27 @@ spmm_slab(const SlabParams p) {
     }
 }
 
-template <int G, int D, int MINB>
-cudaError_t launch_slab_k(const SlabParams& p, cudaStream_t st) {
-    const int64_t blocks = (p.n_rows + kSlabWarps - 1) / kSlabWarps;
-    const size_t smem = (size_t)kSlabWarps * D * 32 * (16 / G) * 16;
-    auto k = p.nv == 16 ? spmm_slab<G, D, MINB, true> : spmm_slab<G, D, MINB, false>;
+template <int G, int D, int MINB, int W>
+cudaError_t launch_slab_w(const SlabParams& p, cudaStream_t st) {
+    const int64_t blocks = (p.n_rows + W - 1) / W;
+    const size_t smem = (size_t)W * D * 32 * (16 / G) * 16;
+    auto k = p.nv == 16 ? spmm_slab<G, D, MINB, true, W> : spmm_slab<G, D, MINB, false, W>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
-    k<<<(unsigned)blocks, kSlabThreads, smem, st>>>(p);
+    k<<<(unsigned)blocks, 32 * W, smem, st>>>(p);
+    return cudaGetLastError();
+}
+
+template <int G, int D, int MINB>
+cudaError_t launch_slab_k(const SlabParams& p, cudaStream_t st) {
+    const char* we = getenv("ES_SPMM_SLAB_CTA_WARPS");     // tuning: warps per CTA (default 8)
+    const int w = we ? atoi(we) : 4;
+    if (w == 1) return launch_slab_w<G, D, MINB, 1>(p, st);
+    if (w == 2) return launch_slab_w<G, D, MINB, 2>(p, st);
+    if (w == 4) return launch_slab_w<G, D, MINB, 4>(p, st);
+    return launch_slab_w<G, D, MINB, 8>(p, st);
     return cudaGetLastError();
 }
 
@@ -197,7 +211,7 @@ cudaError_t launch_slab_pass(const SlabParams& p, int lanes_per_slot, int stages
         switch (stages) {
             case 2: return launch_slab_k<16, 2, 5>(p, st);
             case 8: return launch_slab_k<16, 8, 5>(p, st);
-            default: return launch_slab_k<16, 4, 6>(p, st);
+            default: return launch_slab_k<16, 4, 5>(p, st);
         }
     }
     switch (stages) {

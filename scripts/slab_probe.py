@@ -51,7 +51,7 @@ def main():
                 ts.append(e0.elapsed_time(e1))
         return float(np.median(ts)), float(min(ts))
 
-    # G:stages
+    # G:stages[:warps per CTA]
     variants = [tuple(x.split(":")) for x in os.environ.get("SLAB_VARIANTS", "16:4,8:4").split(",")]
 
     def clear():
@@ -68,6 +68,8 @@ def main():
         os.environ["ES_SPMM_SLAB"] = "1"
         os.environ["ES_SPMM_SLAB_STAGES"] = st
         os.environ["ES_SPMM_SLAB_G"] = g
+        if len(v) > 2:
+            os.environ["ES_SPMM_SLAB_CTA_WARPS"] = v[2]
         ws = es.es_spmm_workspace(n, n, len(colind), F, ldb, s, True, device=dev)
         C2.zero_()
         ms, mn = timed(lambda: es.es_spmm_run_ex(rp, ci, va, Bd, s, 2, 0, 1, F=F, C=C2, workspace=ws))
