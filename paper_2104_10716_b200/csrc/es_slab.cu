@@ -43,21 +43,21 @@ __device__ __forceinline__ float4 lds128(uint32_t addr) {
 }
 
 // One warp per row, split into S = 32/G groups of G lanes.  Step u of a 32-slot chunk consumes
-// slots S*u + e (group e = lane / G); lane `sub` = lane % G of a group owns the P = 16/G
-// 16-B pieces sub + G*q (q < P) of the slice (nv <= 16 pieces), so each LDGSTS instruction of a
-// group covers G*16 contiguous bytes.  The copy for step u + D is issued right after step u is
+// slots S*u + e (group e = lane / G); lane `sub` = lane % G of a group owns the P 16-B pieces
+// sub + G*q (q < P) of the slice (nv <= G*P <= 16 pieces), so each LDGSTS instruction of a
+// group covers G*16 contiguous bytes.  A narrow last slice uses fewer lanes per slot (more
+// slots per step, fewer steps).  The copy for step u + D is issued right after step u is
 // consumed, into the stage it released.  Per element: group e sums slots j = e (mod S) in slot
 // order (32-slot-chunk partials), then an xor tree over the groups (G = 16: spmm_cpasync_hw's
 // order, bitwise).
 // W warps per CTA (register cap as for MINB 256-thread CTAs per SM): small CTAs free their
 // slot as soon as their few rows are done instead of waiting for the longest of 8 rows.
-template <int G, int D, int MINB, bool FULL, int W>
+template <int G, int P, int D, int MINB, bool FULL, int W>
 __global__ void __launch_bounds__(32 * W, MINB * 8 / W)
 spmm_slab(const SlabParams p) {
     constexpr int S = 32 / G;            // slots per step
-    constexpr int P = 16 / G;            // pieces per lane
     constexpr int U = 32 / S;            // steps per 32-slot chunk (= G)
-    static_assert(G == 8 || G == 16, "lanes per slot");
+    static_assert((G == 2 || G == 4 || G == 8 || G == 16) && G * P <= 16, "lanes x pieces per slot");
     static_assert(D >= 2 && U % D == 0, "ring depth must divide the steps of a chunk");
     constexpr int kStage = 32 * P;                               // float4 per warp stage
     extern __shared__ __align__(16) float4 slab_ring[];          // [warps][D][S][P][G]
@@ -174,11 +174,11 @@ spmm_slab(const SlabParams p) {
     }
 }
 
-template <int G, int D, int MINB, int W>
+template <int G, int P, int D, int MINB, int W>
 cudaError_t launch_slab_w(const SlabParams& p, cudaStream_t st) {
     const int64_t blocks = (p.n_rows + W - 1) / W;
-    const size_t smem = (size_t)W * D * 32 * (16 / G) * 16;
-    auto k = p.nv == 16 ? spmm_slab<G, D, MINB, true, W> : spmm_slab<G, D, MINB, false, W>;
+    const size_t smem = (size_t)W * D * 32 * P * 16;
+    auto k = p.nv == G * P ? spmm_slab<G, P, D, MINB, true, W> : spmm_slab<G, P, D, MINB, false, W>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -187,15 +187,14 @@ cudaError_t launch_slab_w(const SlabParams& p, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-template <int G, int D, int MINB>
+template <int G, int D, int MINB, int P = 16 / G>
 cudaError_t launch_slab_k(const SlabParams& p, cudaStream_t st) {
-    const char* we = getenv("ES_SPMM_SLAB_CTA_WARPS");     // tuning: warps per CTA (default 8)
+    const char* we = getenv("ES_SPMM_SLAB_CTA_WARPS");     // tuning: warps per CTA (default 4)
     const int w = we ? atoi(we) : 4;
-    if (w == 1) return launch_slab_w<G, D, MINB, 1>(p, st);
-    if (w == 2) return launch_slab_w<G, D, MINB, 2>(p, st);
-    if (w == 4) return launch_slab_w<G, D, MINB, 4>(p, st);
-    return launch_slab_w<G, D, MINB, 8>(p, st);
-    return cudaGetLastError();
+    if (w == 1) return launch_slab_w<G, P, D, MINB, 1>(p, st);
+    if (w == 2) return launch_slab_w<G, P, D, MINB, 2>(p, st);
+    if (w == 8) return launch_slab_w<G, P, D, MINB, 8>(p, st);
+    return launch_slab_w<G, P, D, MINB, 4>(p, st);
 }
 
 }  // namespace
@@ -214,6 +213,10 @@ cudaError_t launch_slab_pass(const SlabParams& p, int lanes_per_slot, int stages
             default: return launch_slab_k<16, 4, 5>(p, st);
         }
     }
+    // narrow last slice: 4 lanes x 2 pieces (8 slots per step) for <= 8 pieces, 2 x 2 (16 slots
+    // per step) for <= 4 -- half / a quarter of the steps of a full slice
+    if (p.nv <= 4) return launch_slab_k<2, 2, 4, 2>(p, st);
+    if (p.nv <= 8) return launch_slab_k<4, 4, 4, 2>(p, st);
     switch (stages) {
         case 2: return launch_slab_k<8, 2, 4>(p, st);
         case 8: return launch_slab_k<8, 8, 4>(p, st);
