@@ -101,6 +101,11 @@ typedef struct {
      * workspace must not be shared by calls in flight. */
     void* workspace;
     int64_t workspace_bytes;
+    /* Slab path only: 1 = skip the sampling stage (a1-a3) and reuse the sampled slots already in
+     * `workspace` from an earlier call on the same rows with the same s, strategy, seed and P'
+     * (e.g. the layers of a GNN aggregating over one sampled graph, or timing the gather passes
+     * alone).  The caller guarantees that earlier call; nothing is checked. */
+    int32_t reuse_sampled;
 } es_spmm_options_t;
 
 /* Bytes of workspace es_spmm_run_ex needs to take the slab path for rows holding `nnz` stored

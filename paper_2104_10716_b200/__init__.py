@@ -40,15 +40,15 @@ class EsOptions(ctypes.Structure):
                 ("mean_divisor", ctypes.c_int32), ("b_dtype", ctypes.c_int32),
                 ("c_peers", ctypes.c_void_p), ("n_peers", ctypes.c_int32),
                 ("deterministic", ctypes.c_int32), ("workspace", ctypes.c_void_p),
-                ("workspace_bytes", ctypes.c_int64)]
+                ("workspace_bytes", ctypes.c_int64), ("reuse_sampled", ctypes.c_int32)]
 
     @classmethod
     def make(cls, prime: int = 0, mean_by_degree: bool = False, bf16: bool = False, c_peers=None,
-             n_peers: int = 0, deterministic: bool = False, workspace=None):
+             n_peers: int = 0, deterministic: bool = False, workspace=None, reuse_sampled: bool = False):
         ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
         return cls(ctypes.sizeof(cls), prime, ES_MEAN_BY_DEGREE if mean_by_degree else ES_MEAN_BY_SAMPLED,
                    ES_DTYPE_BF16 if bf16 else ES_DTYPE_F32, _ptr(c_peers), n_peers, int(deterministic),
-                   _ptr(workspace), ws_bytes)
+                   _ptr(workspace), ws_bytes, int(reuse_sampled))
 
 
 def load_library(path: str = LIB_PATH):
@@ -231,12 +231,13 @@ def es_spmm_run_ex(rowptr, colind, val, B, s: int, strategy: int, seed: int = 0,
                    reduce: int = ES_REDUCE_SUM, F: int | None = None, C=None, prime: int = 0,
                    mean_by_degree: bool = False, row_begin: int = 0, row_end: int | None = None,
                    n_rows: int | None = None, nnz_base: int = 0, c_peers=None, n_peers: int = 0,
-                   workspace=None, stream=None):
+                   workspace=None, reuse_sampled: bool = False, stream=None):
     """es_spmm_run_rows with the options: P' override, MEAN by original degree, bf16 storage of
     B (pass a torch.bfloat16 B; accumulation stays fp32) -- NEXT-4 -- the fused all-gather
     (c_peers: int64 CUDA tensor of n_peers full-C base pointers; C = this rank's full C) --
     NEXT-1, see paper_2104_10716_b200.dist.PeerBuffers -- and the slab path's workspace (a
-    CUDA uint8 tensor of es_spmm_workspace_bytes(...) bytes, or None)."""
+    CUDA uint8 tensor of es_spmm_workspace_bytes(...) bytes, or None; reuse_sampled skips the
+    sampling stage and reuses the slots a previous call left in it)."""
     import torch
     _dev(rowptr, torch.int64, "rowptr")
     _dev(colind, torch.int32, "colind")
@@ -254,7 +255,7 @@ def es_spmm_run_ex(rowptr, colind, val, B, s: int, strategy: int, seed: int = 0,
     if C is None:
         C = torch.empty((row_end - row_begin, F), dtype=torch.float32, device=B.device)
     opt = EsOptions.make(prime, mean_by_degree, B.dtype == torch.bfloat16, c_peers, n_peers,
-                         workspace=workspace)
+                         workspace=workspace, reuse_sampled=reuse_sampled)
     _check(load_library().es_spmm_run_ex(n_rows, B.shape[0], _ptr(rowptr), nnz_base, _ptr(colind), _ptr(val),
                                          _ptr(B), F, ldb, s, strategy, seed & (2**64 - 1), reduce, _ptr(C),
                                          C.stride(0), row_begin, row_end, ctypes.byref(opt), _stream(stream)),

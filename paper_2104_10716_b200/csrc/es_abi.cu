@@ -37,6 +37,7 @@ struct Opts {
     int32_t deterministic = 0;
     void* workspace = nullptr;
     int64_t workspace_bytes = 0;
+    int32_t reuse_sampled = 0;
 };
 
 es_status_t read_opts(const es_spmm_options_t* o, Opts* out) {
@@ -55,11 +56,12 @@ es_status_t read_opts(const es_spmm_options_t* o, Opts* out) {
         out->n_peers = o->n_peers;
     }
     if (o->struct_size >= (int32_t)offsetof(es_spmm_options_t, workspace)) out->deterministic = o->deterministic != 0;
-    if (o->struct_size >= (int32_t)sizeof(es_spmm_options_t)) {
+    if (o->struct_size >= (int32_t)offsetof(es_spmm_options_t, reuse_sampled)) {
         if (o->workspace_bytes < 0 || (o->workspace_bytes > 0 && !o->workspace)) return ES_ERR_INVALID_VALUE;
         out->workspace = o->workspace;
         out->workspace_bytes = o->workspace_bytes;
     }
+    if (o->struct_size >= (int32_t)sizeof(es_spmm_options_t)) out->reuse_sampled = o->reuse_sampled != 0;
     return ES_OK;
 }
 
@@ -154,9 +156,11 @@ es_status_t run_rows_impl(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
             int32_t* s_col = reinterpret_cast<int32_t*>(ws + L.off_col);
             float* s_val = val ? reinterpret_cast<float*>(ws + slab_align(L.off_col + 4 * cap)) : nullptr;
             int launches = 0;
-            cudaError_t err = es::launch_slab_count(rowptr, n, s, s_rowptr, ws + L.off_temp,
-                                                    (size_t)L.temp_bytes, st, &launches);
-            if (err == cudaSuccess) {
+            cudaError_t err = cudaSuccess;
+            if (!o.reuse_sampled)
+                err = es::launch_slab_count(rowptr, n, s, s_rowptr, ws + L.off_temp, (size_t)L.temp_bytes, st,
+                                            &launches);
+            if (err == cudaSuccess && !o.reuse_sampled) {
                 err = es::launch_sample_materialize(rowptr, nnz_base, colind, val, n, s, strategy, seed,
                                                     row_begin, o.prime, s_rowptr, s_col, s_val, nullptr, st,
                                                     cap);

@@ -130,7 +130,7 @@ def test_slab_ldc_padding_untouched(graph, lanes):
     assert rel_ok(Ch[:, :130], o)[0]
 
 
-def test_auto_plan_takes_slab_only_for_wide_uncached_b():
+def test_auto_plan_choice():
     # Reddit-shaped F=602: B (566 MB) > L2, a 64-float slab (60 MB) fits -> workspace wanted
     assert es.es_spmm_workspace_bytes(232965, 232965, 114615945, 602, 608, 256) > 0
     # B fits L2 with long rows (Proteins-shaped) -> wanted; short rows (Arxiv-shaped) or a B too
@@ -138,3 +138,19 @@ def test_auto_plan_takes_slab_only_for_wide_uncached_b():
     assert es.es_spmm_workspace_bytes(132534, 132534, 79_100_000, 128, 128, 256) > 0
     assert es.es_spmm_workspace_bytes(169343, 169343, 2_330_000, 128, 128, 64) == 0
     assert es.es_spmm_workspace_bytes(10_000_000, 10_000_000, 10**9, 256, 256, 128) == 0
+
+
+def test_reuse_sampled_slots(graph, lanes):
+    """reuse_sampled: the gather passes alone over the slots an earlier call sampled into the
+    workspace (a second feature matrix over the same sampled graph) == a full call, bitwise."""
+    rowptr, colind, val = graph
+    B1 = synth.dense(2300, 300, seed=21, ld=300)
+    B2 = synth.dense(2300, 300, seed=22, ld=300)
+    ws = es.es_spmm_workspace(1301, 2300, len(colind), 300, 300, 96, True, device=DEV)
+    rp, ci, v = t(rowptr), t(colind), t(val)
+    es.es_spmm_run_ex(rp, ci, v, t(B1), 96, 2, 13, 1, F=300, workspace=ws)
+    g2 = es.es_spmm_run_ex(rp, ci, v, t(B2), 96, 2, 13, 1, F=300, workspace=ws, reuse_sampled=True)
+    full2 = slab(rowptr, colind, val, B2, 96, 2, 13, 1, 300)
+    assert np.array_equal(g2.cpu().numpy(), full2)
+    o = oracle.spmm(rowptr, colind, val, B2, 96, 2, seed=13, reduce=1, F=300)
+    assert rel_ok(full2, o)[0]
