@@ -51,7 +51,7 @@ def main():
                 ts.append(e0.elapsed_time(e1))
         return float(np.median(ts)), float(min(ts))
 
-    # G:stages[:warps per CTA]
+    # G:stages[:warps per CTA[:tma warps per CTA]]
     variants = [tuple(x.split(":")) for x in os.environ.get("SLAB_VARIANTS", "16:4,8:4").split(",")]
 
     def clear():
@@ -70,6 +70,8 @@ def main():
         os.environ["ES_SPMM_SLAB_G"] = g
         if len(v) > 2:
             os.environ["ES_SPMM_SLAB_CTA_WARPS"] = v[2]
+        if len(v) > 3:
+            os.environ["ES_SPMM_SLAB_TMA"] = v[3]
         ws = es.es_spmm_workspace(n, n, len(colind), F, ldb, s, True, device=dev)
         C2.zero_()
         ms, mn = timed(lambda: es.es_spmm_run_ex(rp, ci, va, Bd, s, 2, 0, 1, F=F, C=C2, workspace=ws))
