@@ -30,6 +30,24 @@ def main():
                 C = es.es_spmm_run(rp, ci, va, B, 64, strat, 5, red, F=F)
         torch.cuda.synchronize()
         print("ok", F, ldb, es.es_spmm_plan(F, ldb, F, B, C), flush=True)
+    # slab path (forced): 8 x 2 and 16 x 1 lanes per slot, narrow tails, and a workspace sized
+    # for a quarter of the stored entries (slots past its capacity are never read or written)
+    os.environ.pop("ES_SPMM_KERNEL", None)
+    os.environ["ES_SPMM_SLAB"] = "1"
+    for g in ("8", "16"):
+        os.environ["ES_SPMM_SLAB_G"] = g
+        for F, ldb in ((602, 608), (130, 132), (200, 200), (17, 20)):
+            B = t(synth.dense(700, F, seed=F, ld=ldb))
+            for nnz in (len(colind), len(colind) // 4):
+                ws = es.es_spmm_workspace(300, 700, nnz, F, ldb, 64, True, device=dev)
+                for strat in (1, 2):
+                    es.es_spmm_run_ex(rp, ci, va, B, 64, strat, 5, 1, F=F, workspace=ws)
+                es.es_spmm_run_ex(rp, ci, None, B, 64, 2, 5, 0, F=F, workspace=ws)
+                es.es_spmm_run_ex(rp, ci, va, B, 64, 2, 5, 1, F=F, workspace=ws, reuse_sampled=True)
+            torch.cuda.synchronize()
+            print("ok slab", g, F, ldb, flush=True)
+    os.environ.pop("ES_SPMM_SLAB", None)
+    os.environ.pop("ES_SPMM_SLAB_G", None)
     es.es_spmm_sample(rp, ci, va, 40, 2, 9)
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
     es.es_spmm_run_host(pin(rowptr), pin(colind), pin(val), pin(synth.dense(700, 602, 1, ld=604)), 64, 2, 0,
