@@ -16,6 +16,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import synth  # noqa: E402
 import paper_2104_10716_b200 as es  # noqa: E402
+
+if os.environ.get("ES_LIB"):                 # A/B a library built with other compile-time knobs
+    es.load_library(os.environ["ES_LIB"])
 from bench import byte_model, ldb_for  # noqa: E402
 
 
