@@ -82,17 +82,18 @@ bool slab_feasible(int64_t n_cols, int64_t F) {
     return n_cols * kSlabF * 4 <= (env_i64("ES_SPMM_SLAB_MAX_SLAB_MB", 80) << 20);
 }
 
-// es_spmm_workspace_bytes's choice (measured, profiles/r01.md "Slab path"): feasible, F >= 128,
-// and either B does not fit L2 (Reddit-shaped: 9.8 -> 8.2 ms at F=602, 1.89 -> 1.71 at F=128)
-// or rows are long (>= 64 stored entries on average: Proteins-shaped F=128 1.21 -> 1.11 ms, B
-// L2-resident -- the 8-lane, 2-piece ring beats the fused two-slot ring); short rows keep the
-// single fused kernel (Arxiv-shaped: 0.19 fused vs 0.37 ms sliced).
-bool slab_wanted(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t F, int64_t ldb) {
+// es_spmm_workspace_bytes's choice (measured, profiles/r01.md "Slab path" and the s-sweep in
+// BASELINE.md): feasible, F >= 128, and rows that sample >= 128 slots on average -- the bound
+// used is min(s, nnz / n_rows).  Reddit-shaped s=256: F=602 9.8 -> 7.8 ms, F=128 1.89 -> 1.65;
+// Proteins-shaped (B L2-resident) 1.21 -> 1.08.  Below ~128 slots per row the per-row start-up
+// of each slice pass outweighs the L2-resident gathers (Reddit F=602 s=16: 2.0 vs 4.9 TFLOP/s,
+// s=64: 5.0-5.2 vs 5.1-6.2), and short rows (Arxiv-shaped, mean degree 14) keep the fused kernel.
+bool slab_wanted(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t F, int64_t s) {
     if (!slab_feasible(n_cols, F)) return false;
     if (env_i64("ES_SPMM_SLAB", -1) == 1) return true;
-    const int64_t l2_b = env_i64("ES_SPMM_SLAB_MIN_B_MB", 96) << 20;    // B beyond this: slice
-    return F >= env_i64("ES_SPMM_SLAB_MIN_F", 128) &&
-           (n_cols * ldb * 4 > l2_b || nnz >= env_i64("ES_SPMM_SLAB_MIN_DEG", 64) * n_rows);
+    const int64_t mean_deg = n_rows > 0 ? nnz / n_rows : 0;
+    const int64_t k_est = s < mean_deg ? s : mean_deg;
+    return F >= env_i64("ES_SPMM_SLAB_MIN_F", 128) && k_est >= env_i64("ES_SPMM_SLAB_MIN_K", 128);
 }
 
 int64_t slab_align(int64_t x) { return (x + 255) & ~(int64_t)255; }
@@ -218,7 +219,7 @@ int64_t es_launch_count(void) { return g_launches.load(std::memory_order_relaxed
 int64_t es_spmm_workspace_bytes(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t F, int64_t ldb,
                                 int32_t s, int32_t has_val) {
     if (n_rows <= 0 || n_cols < 0 || nnz < 0 || F < 1 || ldb < F || s < 1) return 0;
-    if (!slab_wanted(n_rows, n_cols, nnz, F, ldb)) return 0;
+    if (!slab_wanted(n_rows, n_cols, nnz, F, s)) return 0;
     const SlabLayout L = slab_layout(n_rows);
     const int64_t cap = nnz < n_rows * (int64_t)s ? nnz : n_rows * (int64_t)s;
     return L.bytes_fixed + 256 + slab_align(4 * (cap > 0 ? cap : 1)) + (has_val ? 4 * (cap > 0 ? cap : 1) : 0) + 256;

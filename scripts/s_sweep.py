@@ -1,7 +1,9 @@
 #!/usr/bin/env python3
 """The BASELINE.json metric "vs s": sampled-SpMM GFLOP/s, algorithmic GB/s and roofline fraction
 for s in {16..512} x {Bucket, FastRand} on the dataset-shaped graphs (1 GPU, L2 flushed before
-every launch, CUDA events, median of 5).  Prints one JSON line per point."""
+every call, CUDA events, median of 5), through the library's plan: es_spmm_run_ex with the
+workspace es_spmm_workspace_bytes asks for (the slab path) where it asks, else the fused kernel
+(ES_SPMM_SLAB=0 forces the fused kernel everywhere).  Prints one JSON line per point."""
 import json
 import os
 import sys
@@ -36,13 +38,17 @@ def main():
         C = torch.empty((n, ldb), device=dev)
         for s in (16, 32, 64, 128, 256, 512):
             K = int(np.minimum(d, s).sum())
+            ws = es.es_spmm_workspace(n, n, len(colind), F, ldb, s, True, device=dev)
             for strat in (1, 2):
                 ts = []
                 for i in range(7):
                     flush.zero_()
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     e0.record()
-                    es.es_spmm_run(rp, ci, va, B, s, strat, 0, red, F=F, C=C)
+                    if ws is not None:
+                        es.es_spmm_run_ex(rp, ci, va, B, s, strat, 0, red, F=F, C=C, workspace=ws)
+                    else:
+                        es.es_spmm_run(rp, ci, va, B, s, strat, 0, red, F=F, C=C)
                     e1.record()
                     torch.cuda.synchronize()
                     if i >= 2:
@@ -54,7 +60,8 @@ def main():
                                   "ms": round(ms, 4), "GFLOPs": round(2 * F * K / (ms / 1e3) / 1e9, 1),
                                   "model_GBs": round(gbs, 1), "frac": round(gbs / peak, 3),
                                   "sampled_edges_per_s": round(K / (ms / 1e3)),
-                                  "plan": es.es_spmm_plan(F, ldb, ldb, B, C)}), flush=True)
+                                  "plan": "slab path (spmm_slab x %d + sampling)" % ((F + 63) // 64)
+                                  if ws is not None else es.es_spmm_plan(F, ldb, ldb, B, C)}), flush=True)
 
 
 if __name__ == "__main__":

@@ -324,7 +324,11 @@ def test_full_arxiv(s, strat):
     _full("arxiv", 128, 128, s, strat, 0, ES_REDUCE_SUM)
 
 
-def test_full_proteins():
+@pytest.mark.parametrize("path", ["fused", "slab"])
+def test_full_proteins(path, monkeypatch):
+    """Config 3 at full size; bench.py takes the slab path here (long rows), so both are checked."""
+    if path == "slab":
+        monkeypatch.setenv("ES_SPMM_SLAB", "1")
     _full("proteins", 128, 128, 256, ES_FASTRAND, 0, ES_REDUCE_SUM)
 
 

@@ -170,7 +170,8 @@ def test_options_validation(lib):
 
 def test_workspace_bytes_plan(lib, monkeypatch):
     """es_spmm_workspace_bytes (host only): the slab path is asked for when a 64-float slab of B
-    fits L2 and B does not, or rows are long; the bound covers min(nnz, n*s) slots (+ values)."""
+    fits L2, F >= 128 and rows sample >= 128 slots on average; the bound covers min(nnz, n*s)
+    slots (+ values)."""
     monkeypatch.delenv("ES_SPMM_SLAB", raising=False)
     reddit = es.es_spmm_workspace_bytes(232965, 232965, 114615945, 602, 608, 256)
     assert reddit >= 8 * 232965 * 256 + 8 * 232966            # n*s < nnz here: n*s slots
@@ -180,8 +181,11 @@ def test_workspace_bytes_plan(lib, monkeypatch):
     assert es.es_spmm_workspace_bytes(169343, 169343, 2_330_000, 128, 128, 64) == 0     # short rows
     assert es.es_spmm_workspace_bytes(10_000_000, 10_000_000, 10**9, 256, 256, 128) == 0  # slab > L2
     assert es.es_spmm_workspace_bytes(232965, 232965, 114615945, 64, 64, 256) == 0      # one slice
+    assert es.es_spmm_workspace_bytes(232965, 232965, 114615945, 602, 608, 64) == 0     # s < 128
+    monkeypatch.setenv("ES_SPMM_SLAB", "1")
     small = es.es_spmm_workspace_bytes(232965, 232965, 1000, 602, 608, 256)
     assert 8 * 1000 <= small - 8 * 232966 < 8 * 1000 + 4096                             # nnz < n*s
+    monkeypatch.delenv("ES_SPMM_SLAB")
     assert es.es_spmm_workspace_bytes(10, 10, 10, 602, 600, 4) == 0                     # ldb < F
     monkeypatch.setenv("ES_SPMM_SLAB", "0")
     assert es.es_spmm_workspace_bytes(232965, 232965, 114615945, 602, 608, 256) == 0
