@@ -260,17 +260,17 @@ def main():
     # the library's plan: a workspace (allocated once, outside the timed region) selects the
     # feature-sliced path when B does not fit L2 but a 64-float slab of it does
     ws = None
-    if peers is None and not a.bf16:
+    if not a.bf16:
         ws = es.es_spmm_workspace(r1 - r0, n, e1 - e0, F, ldb, a.s, True, device=dev)
 
     def launch(st):
-        if ws is not None:
-            es.es_spmm_run_ex(rp_d, ci_d, va_d, B_d, a.s, strat_id, a.seed, red_id, F=F, C=C_d,
-                              row_begin=r0, row_end=r1, n_rows=n, nnz_base=e0, workspace=ws, stream=st)
-        elif peers is not None:
+        if peers is not None:
             es.es_spmm_run_ex(rp_d, ci_d, va_d, B_d, a.s, strat_id, a.seed, red_id, F=F, C=peers.C,
                               row_begin=r0, row_end=r1, n_rows=n, nnz_base=e0, c_peers=peers.peers,
-                              n_peers=peers.world, stream=st)
+                              n_peers=peers.world, workspace=ws, stream=st)
+        elif ws is not None:
+            es.es_spmm_run_ex(rp_d, ci_d, va_d, B_d, a.s, strat_id, a.seed, red_id, F=F, C=C_d,
+                              row_begin=r0, row_end=r1, n_rows=n, nnz_base=e0, workspace=ws, stream=st)
         elif a.bf16:
             es.es_spmm_run_ex(rp_d, ci_d, va_d, B_d, a.s, strat_id, a.seed, red_id, F=F, C=C_d,
                               row_begin=r0, row_end=r1, n_rows=n, nnz_base=e0, stream=st)

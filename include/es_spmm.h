@@ -96,8 +96,9 @@ typedef struct {
      * 64-float feature slice at a time, each slice's B slab (n_cols x 256 B) L2-resident.  Pass
      * it only when es_spmm_workspace_bytes returned > 0 (that is where it was measured faster);
      * the call takes the path whenever a workspace is given and the slab fits L2.  Same C as
-     * the fused kernels within the parity bound.  NULL, or a layout the path does not take (bf16
-     * B, fused all-gather, B or C not 16-B aligned, F <= 16) = the fused kernels.  The
+     * the fused kernels within the parity bound; the fused all-gather (c_peers) applies to it as
+     * well.  NULL, or a layout the path does not take (bf16 B, B or C not 16-B aligned,
+     * F <= 16) = the fused kernels.  The
      * workspace must not be shared by calls in flight. */
     void* workspace;
     int64_t workspace_bytes;

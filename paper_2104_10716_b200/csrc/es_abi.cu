@@ -146,7 +146,7 @@ es_status_t run_rows_impl(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
     const es::Plan plan = o.bf16 ? es::make_plan_bf16(F, ldb, ldc, B, C) : es::make_plan(F, ldb, ldc, B, C);
     if (plan.unsupported) return ES_ERR_UNSUPPORTED;
     const uintptr_t bu = reinterpret_cast<uintptr_t>(B), cu = reinterpret_cast<uintptr_t>(C);
-    if (o.workspace && !o.bf16 && o.n_peers == 0 && bu % 16 == 0 && ldb % 4 == 0 && cu % 16 == 0 &&
+    if (o.workspace && !o.bf16 && bu % 16 == 0 && ldb % 4 == 0 && cu % 16 == 0 &&
         ldc % 4 == 0 && slab_feasible(n_cols, F)) {
         const SlabLayout L = slab_layout(n);
         const int64_t per_slot = val ? 8 : 4;
@@ -182,6 +182,10 @@ es_status_t run_rows_impl(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
                 sp.w = (int32_t)(F - c0 < kSlabF ? F - c0 : kSlabF);
                 sp.nv = (sp.w + 3) / 4;
                 sp.C = C + c0;
+                sp.c_peers = o.c_peers;
+                sp.n_peers = o.n_peers;
+                sp.row_base = row_begin;
+                sp.col0 = c0;
                 sp.ldc = ldc;
                 sp.c_vec = 1;
                 sp.n_rows = n;

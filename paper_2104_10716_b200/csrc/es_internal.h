@@ -82,6 +82,10 @@ struct SlabParams {
     int64_t n_rows;
     int32_t reduce;
     int32_t mean_by_degree;
+    float* const* c_peers;    // fused all-gather (NEXT-1): full-C bases of every rank, or NULL
+    int32_t n_peers;
+    int64_t row_base;         // global id of local row 0 (peer stores)
+    int64_t col0;             // the slice's first column (peer stores)
 };
 
 cudaError_t launch_slab_pass(const SlabParams& p, int lanes_per_slot, int stages, cudaStream_t st);

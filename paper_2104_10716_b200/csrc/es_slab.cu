@@ -162,13 +162,20 @@ spmm_slab(const SlabParams p) {
 #pragma unroll
                 for (int c = 0; c < 4; ++c)
                     res[c] = p.reduce == kMean ? (div > 0 ? __fdiv_rn(tot[q][c], (float)div) : 0.0f) : tot[q][c];
-                float* dst = p.C + r * p.ldc + piece * 4;
                 const int rem = p.w - piece * 4;                 // valid floats of this piece
-                if (p.c_vec && rem >= 4) st_stream4(dst, res, pol_a);
-                else
+                auto put = [&](float* dst) {
+                    if (p.c_vec && rem >= 4) st_stream4(dst, res, pol_a);
+                    else
 #pragma unroll
-                    for (int c = 0; c < 4; ++c)
-                        if (c < rem) st_stream(dst + c, res[c], pol_a);
+                        for (int c = 0; c < 4; ++c)
+                            if (c < rem) st_stream(dst + c, res[c], pol_a);
+                };
+                if (p.n_peers == 0) {
+                    put(p.C + r * p.ldc + piece * 4);
+                } else {                                         // fused all-gather: every rank's C
+                    const int64_t off = (p.row_base + r) * p.ldc + p.col0 + piece * 4;
+                    for (int q2 = 0; q2 < p.n_peers; ++q2) put(p.c_peers[q2] + off);
+                }
             }
         }
     }
@@ -209,7 +216,7 @@ cudaError_t launch_slab_pass(const SlabParams& p, int lanes_per_slot, int stages
     if (lanes_per_slot == 16) {
         switch (stages) {
             case 2: return launch_slab_k<16, 2, 5>(p, st);
-            case 8: return launch_slab_k<16, 8, 5>(p, st);
+            case 8: return launch_slab_k<16, 8, 4>(p, st);
             default: return launch_slab_k<16, 4, 5>(p, st);
         }
     }

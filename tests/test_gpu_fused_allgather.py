@@ -29,7 +29,10 @@ def graph():
     return rowptr, colind, val, B
 
 
-def test_two_local_peer_buffers():
+@pytest.mark.parametrize("path", ["fused", "slab"])
+def test_two_local_peer_buffers(path, monkeypatch):
+    if path == "slab":                  # the feature-sliced path's epilogue stores to the peers too
+        monkeypatch.setenv("ES_SPMM_SLAB", "1")
     rowptr, colind, val, B = graph()
     dev = torch.device("cuda:0")
     bufs = [es.es_ipc_alloc(N * 132 * 4) for _ in range(2)]
@@ -43,9 +46,11 @@ def test_two_local_peer_buffers():
         for a, b in zip(bounds[:-1], bounds[1:]):
             e0, e1 = rowptr[a], rowptr[b]
             t = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+            ws = (es.es_spmm_workspace(int(b - a), NC, int(e1 - e0), F, 132, 64, True, device=dev)
+                  if path == "slab" else None)
             es.es_spmm_run_ex(t(rowptr[a:b + 1]), t(colind[e0:e1]), t(val[e0:e1]), Bd, 64, 2, 3, 1, F=F,
                               C=views[0], row_begin=int(a), row_end=int(b), n_rows=N, nnz_base=int(e0),
-                              c_peers=peers, n_peers=2)
+                              c_peers=peers, n_peers=2, workspace=ws)
         torch.cuda.synchronize()
         want = oracle.spmm(rowptr, colind, val, B, 64, 2, seed=3, reduce=1, F=F)
         for v in views:
