@@ -199,7 +199,11 @@ es_status_t es_spmm_backward(int64_t n_rows, int64_t n_cols,
                              float* dB /*[dev] n_cols x ldb*/, int64_t ldb,
                              int64_t row_begin, int64_t row_end, void* stream);
 
-/* es_spmm_backward with options (prime, mean_divisor; b_dtype must be ES_DTYPE_F32). */
+/* es_spmm_backward with options (prime, mean_divisor, deterministic; b_dtype must be
+ * ES_DTYPE_F32).  A workspace (as for es_spmm_run_ex, dC/dB 16-B aligned, ldc/ldb % 4 == 0)
+ * selects the feature-sliced backward: one pass per 64-float slice, the dB slab L2-resident while
+ * its reductions land; with reuse_sampled = 1 it reuses the slots the forward call sampled into
+ * that workspace (same rows, s, strategy, seed, P').  deterministic = 1 takes precedence. */
 es_status_t es_spmm_backward_ex(int64_t n_rows, int64_t n_cols,
                                 const int64_t* rowptr, int64_t nnz_base,
                                 const int32_t* colind, const float* val,

@@ -306,15 +306,19 @@ def es_spmm_sample_ex(rowptr, colind, val, s: int, strategy: int, seed: int = 0,
 
 def es_spmm_backward_ex(rowptr, colind, val, dC, n_cols: int, s: int, strategy: int, seed: int = 0,
                         reduce: int = ES_REDUCE_SUM, prime: int = 0, mean_by_degree: bool = False,
-                        F: int | None = None, dB=None, deterministic: bool = False, stream=None):
+                        F: int | None = None, dB=None, deterministic: bool = False, workspace=None,
+                        reuse_sampled: bool = False, stream=None):
     """Backward with the P' / MEAN-divisor options (full CSR); deterministic=True gives a
-    bitwise-reproducible dB (sort-based transpose, single writer per row)."""
+    bitwise-reproducible dB (sort-based transpose, single writer per row); a workspace (as for
+    es_spmm_run_ex) selects the feature-sliced backward, reuse_sampled=True reuses the slots the
+    forward left in it."""
     import torch
     F = dC.shape[1] if F is None else F
     if dB is None:
         dB = torch.zeros((n_cols, F), dtype=torch.float32, device=dC.device)
     n = rowptr.numel() - 1
-    opt = EsOptions.make(prime, mean_by_degree, deterministic=deterministic)
+    opt = EsOptions.make(prime, mean_by_degree, deterministic=deterministic, workspace=workspace,
+                         reuse_sampled=reuse_sampled)
     _check(load_library().es_spmm_backward_ex(n, n_cols, _ptr(rowptr), 0, _ptr(colind), _ptr(val), _ptr(dC), F,
                                               dC.stride(0), s, strategy, seed & (2**64 - 1), reduce, _ptr(dB),
                                               dB.stride(0), 0, n, ctypes.byref(opt), _stream(stream)),

@@ -111,6 +111,41 @@ SlabLayout slab_layout(int64_t n) {
     return L;
 }
 
+// The workspace's sampled-slot arrays (es_spmm_sample layout); false if it holds no slot.
+struct SlabSlots {
+    int64_t* s_rowptr;
+    int32_t* s_col;
+    float* s_val;
+    int64_t cap;
+    void* temp;
+    size_t temp_bytes;
+};
+bool slab_slots(const Opts& o, int64_t n, bool has_val, SlabSlots* out) {
+    const SlabLayout L = slab_layout(n);
+    const int64_t per_slot = has_val ? 8 : 4;
+    const int64_t cap = (o.workspace_bytes - L.bytes_fixed - 256) / per_slot;
+    if (cap < 1) return false;
+    char* ws = static_cast<char*>(o.workspace);
+    out->s_rowptr = reinterpret_cast<int64_t*>(ws + L.off_rowptr);
+    out->s_col = reinterpret_cast<int32_t*>(ws + L.off_col);
+    out->s_val = has_val ? reinterpret_cast<float*>(ws + slab_align(L.off_col + 4 * cap)) : nullptr;
+    out->cap = cap;
+    out->temp = ws + L.off_temp;
+    out->temp_bytes = (size_t)L.temp_bytes;
+    return true;
+}
+// a1-a3 once into the workspace: count, scan, materialise
+cudaError_t slab_sample(const SlabSlots& sl, const int64_t* rowptr, int64_t nnz_base, const int32_t* colind,
+                        const float* val, int64_t n, int32_t s, int32_t strategy, uint64_t seed, int64_t row_begin,
+                        uint32_t prime, cudaStream_t st, int* launches) {
+    cudaError_t err = es::launch_slab_count(rowptr, n, s, sl.s_rowptr, sl.temp, sl.temp_bytes, st, launches);
+    if (err != cudaSuccess) return err;
+    err = es::launch_sample_materialize(rowptr, nnz_base, colind, val, n, s, strategy, seed, row_begin, prime,
+                                        sl.s_rowptr, sl.s_col, sl.s_val, nullptr, st, sl.cap);
+    ++*launches;
+    return err;
+}
+
 es_status_t run_rows_impl(int64_t n_rows, int64_t n_cols, const int64_t* rowptr, int64_t nnz_base,
                           const int32_t* colind, const float* val, const void* B, int64_t F,
                           int64_t ldb, int32_t s, int32_t strategy, uint64_t seed, int32_t reduce,
@@ -148,34 +183,22 @@ es_status_t run_rows_impl(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
     const uintptr_t bu = reinterpret_cast<uintptr_t>(B), cu = reinterpret_cast<uintptr_t>(C);
     if (o.workspace && !o.bf16 && bu % 16 == 0 && ldb % 4 == 0 && cu % 16 == 0 &&
         ldc % 4 == 0 && slab_feasible(n_cols, F)) {
-        const SlabLayout L = slab_layout(n);
-        const int64_t per_slot = val ? 8 : 4;
-        const int64_t cap = (o.workspace_bytes - L.bytes_fixed - 256) / per_slot;
-        if (cap >= 1) {
-            char* ws = static_cast<char*>(o.workspace);
-            int64_t* s_rowptr = reinterpret_cast<int64_t*>(ws + L.off_rowptr);
-            int32_t* s_col = reinterpret_cast<int32_t*>(ws + L.off_col);
-            float* s_val = val ? reinterpret_cast<float*>(ws + slab_align(L.off_col + 4 * cap)) : nullptr;
-            int launches = 0;
-            cudaError_t err = cudaSuccess;
+        SlabSlots sl;
+        int launches = 0;
+        cudaError_t err = cudaSuccess;
+        if (slab_slots(o, n, val != nullptr, &sl)) {
             if (!o.reuse_sampled)
-                err = es::launch_slab_count(rowptr, n, s, s_rowptr, ws + L.off_temp, (size_t)L.temp_bytes, st,
-                                            &launches);
-            if (err == cudaSuccess && !o.reuse_sampled) {
-                err = es::launch_sample_materialize(rowptr, nnz_base, colind, val, n, s, strategy, seed,
-                                                    row_begin, o.prime, s_rowptr, s_col, s_val, nullptr, st,
-                                                    cap);
-                ++launches;
-            }
+                err = slab_sample(sl, rowptr, nnz_base, colind, val, n, s, strategy, seed, row_begin, o.prime, st,
+                                  &launches);
             const int stages = (int)env_i64("ES_SPMM_SLAB_STAGES", 4);
             const int lanes = (int)env_i64("ES_SPMM_SLAB_G", 8);
             for (int64_t c0 = 0; err == cudaSuccess && c0 < F; c0 += kSlabF) {
                 es::SlabParams sp{};
-                sp.s_rowptr = s_rowptr;
+                sp.s_rowptr = sl.s_rowptr;
                 sp.slot_base = 0;
-                sp.cap = cap;
-                sp.s_colind = s_col;
-                sp.s_val = s_val;
+                sp.cap = sl.cap;
+                sp.s_colind = sl.s_col;
+                sp.s_val = sl.s_val;
                 sp.rowptr = rowptr;
                 sp.B = static_cast<const float*>(B) + c0;
                 sp.ldb = ldb;
@@ -353,6 +376,37 @@ es_status_t es_spmm_backward_ex(int64_t n_rows, int64_t n_cols, const int64_t* r
         cudaError_t err = es::launch_backward_deterministic(p, n_cols, as_stream(stream), &launches, &too_large);
         g_launches.fetch_add(launches, std::memory_order_relaxed);
         if (too_large) return ES_ERR_UNSUPPORTED;
+        return err == cudaSuccess ? ES_OK : ES_ERR_CUDA;
+    }
+    // slab path (a workspace was passed): the gradient one 64-float slice at a time, the dB slab
+    // L2-resident while its reductions land; the sampled slots come from the workspace
+    // (reuse_sampled: the forward's) or are sampled here
+    SlabSlots sl;
+    if (o.workspace && p.vec == 4 && slab_feasible(n_cols, F) && slab_slots(o, n, val != nullptr, &sl)) {
+        cudaStream_t st = as_stream(stream);
+        int launches = 0;
+        cudaError_t err = cudaSuccess;
+        if (!o.reuse_sampled)
+            err = slab_sample(sl, rowptr, nnz_base, colind, val, n, s, strategy, seed, row_begin, o.prime, st,
+                              &launches);
+        for (int64_t c0 = 0; err == cudaSuccess && c0 < F; c0 += kSlabF) {
+            es::SlabParams sp{};
+            sp.s_rowptr = sl.s_rowptr;
+            sp.cap = sl.cap;
+            sp.s_colind = sl.s_col;
+            sp.s_val = sl.s_val;
+            sp.rowptr = rowptr;
+            sp.ldb = ldb;
+            sp.w = (int32_t)(F - c0 < kSlabF ? F - c0 : kSlabF);
+            sp.nv = (sp.w + 3) / 4;
+            sp.ldc = ldc;
+            sp.n_rows = n;
+            sp.reduce = reduce;
+            sp.mean_by_degree = o.mean_by_degree;
+            err = es::launch_slab_backward(sp, dC + c0, dB + c0, st);
+            ++launches;
+        }
+        g_launches.fetch_add(launches, std::memory_order_relaxed);
         return err == cudaSuccess ? ES_OK : ES_ERR_CUDA;
     }
     cudaError_t err = es::launch_backward(p, as_stream(stream));

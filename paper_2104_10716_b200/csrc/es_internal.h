@@ -89,6 +89,8 @@ struct SlabParams {
 };
 
 cudaError_t launch_slab_pass(const SlabParams& p, int lanes_per_slot, int stages, cudaStream_t st);
+// backward slab pass: p.C/ldc describe dC's slice (read), dB the slice of the gradient (reduced into)
+cudaError_t launch_slab_backward(const SlabParams& p, const float* dC, float* dB, cudaStream_t st);
 size_t slab_scan_temp_bytes(int64_t n);
 cudaError_t launch_slab_count(const int64_t* rowptr, int64_t n, int32_t s, int64_t* s_rowptr, void* temp,
                               size_t temp_bytes, cudaStream_t st, int* launches);

@@ -204,6 +204,73 @@ cudaError_t launch_slab_k(const SlabParams& p, cudaStream_t st) {
     return launch_slab_w<G, P, D, MINB, 4>(p, st);
 }
 
+// ---------------------------------------------------------------- backward (NEXT-2), slab path
+// dB[col_ij, c0:c0+w] += w_ij * dC[i, c0:c0+w] over the compact sampled slots, one launch per
+// 64-float slice, so the dB slab the reductions land in (n_cols x 256 B) stays L2-resident and
+// the 16-B vector reductions (red.global.add.v4.f32) resolve in L2 instead of read-modify-
+// writing HBM.  One warp per row; the row's dC slice is read once into registers (MEAN: divided
+// by the row's divisor with IEEE division, as the fused backward); 4 slots per step (groups of 8
+// lanes, 2 pieces each).  Addition order across rows is not deterministic (as the fused one).
+template <int W>
+__global__ void __launch_bounds__(32 * W, 32 / W)
+spmm_slab_bwd(const SlabParams p, const float* __restrict__ dC, float* __restrict__ dB) {
+    constexpr int G = 8, P = 2, S = 4;
+    const int lane = threadIdx.x & 31;
+    const int e = lane / G, sub = lane % G;
+    const int64_t r = (int64_t)blockIdx.x * W + (threadIdx.x >> 5);
+    if (r >= p.n_rows) return;
+    const uint64_t pol_a = policy_evict_first();
+    const int64_t beg = ld_stream(p.s_rowptr + r, pol_a) - p.slot_base;
+    int64_t end = ld_stream(p.s_rowptr + r + 1, pol_a) - p.slot_base;
+    if (end > p.cap) end = p.cap;
+    const int32_t k = end > beg ? (int32_t)(end - beg) : 0;
+    if (k == 0) return;
+    float div = (float)k;
+    if (p.reduce == kMean && p.mean_by_degree)
+        div = (float)(ld_stream(p.rowptr + r + 1, pol_a) - ld_stream(p.rowptr + r, pol_a));
+    float x[P][4];
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+        const int piece = sub + G * q;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int col = piece * 4 + c;
+            float v = col < p.w ? ld_stream(dC + r * p.ldc + col, pol_a) : 0.0f;
+            x[q][c] = p.reduce == kMean ? __fdiv_rn(v, div) : v;
+        }
+    }
+    const int64_t ldb = p.ldb;
+    for (int32_t j0 = 0; j0 < k; j0 += 32) {
+        int32_t cj = 0;
+        float aj = 0.0f;
+        if (j0 + lane < k) {
+            cj = ld_stream(p.s_colind + beg + j0 + lane, pol_a);
+            aj = p.s_val ? ld_stream(p.s_val + beg + j0 + lane, pol_a) : 1.0f;
+        }
+        const int n_here = min(32, k - j0);
+        for (int u = 0; u < (n_here + S - 1) / S; ++u) {
+            const int slot = S * u + e;
+            const int32_t cn = __shfl_sync(kAll, cj, slot);
+            const float av = __shfl_sync(kAll, aj, slot);
+            if (slot < n_here) {
+                float* brow = dB + (int64_t)(uint32_t)cn * ldb;
+#pragma unroll
+                for (int q = 0; q < P; ++q) {
+                    const int piece = sub + G * q;
+                    if (piece < p.nv) {
+                        if (piece * 4 + 4 <= p.w)
+                            red_add4(brow + piece * 4, av * x[q][0], av * x[q][1], av * x[q][2], av * x[q][3]);
+                        else
+#pragma unroll
+                            for (int c = 0; c < 4; ++c)
+                                if (piece * 4 + c < p.w) red_add1(brow + piece * 4 + c, av * x[q][c]);
+                    }
+                }
+            }
+        }
+    }
+}
+
 }  // namespace
 
 // Instantiations: G = 8 (default: 2 pieces per lane, 4 slots per step) or 16; D = 2, 4, 8.
@@ -229,6 +296,13 @@ cudaError_t launch_slab_pass(const SlabParams& p, int lanes_per_slot, int stages
         case 8: return launch_slab_k<8, 8, 4>(p, st);
         default: return launch_slab_k<8, 4, 4>(p, st);
     }
+}
+
+cudaError_t launch_slab_backward(const SlabParams& p, const float* dC, float* dB, cudaStream_t st) {
+    if (p.n_rows <= 0) return cudaSuccess;
+    constexpr int W = 4;
+    spmm_slab_bwd<W><<<(unsigned)((p.n_rows + W - 1) / W), 32 * W, 0, st>>>(p, dC, dB);
+    return cudaGetLastError();
 }
 
 size_t slab_scan_temp_bytes(int64_t n) {

@@ -90,12 +90,18 @@ def test_row_blocks_accumulate_into_one_dB(graph):
     assert torch.allclose(dB, full, rtol=1e-5, atol=1e-6)
 
 
-def test_autograd_gradient(graph):
+@pytest.mark.parametrize("path", ["fused", "slab"])
+def test_autograd_gradient(graph, path, monkeypatch):
     rowptr, colind, val = graph
-    B = t(synth.dense(1100, 32, seed=8)).requires_grad_(True)
-    W = t(synth.dense(900, 32, seed=9))
+    F = 32 if path == "fused" else 136
+    B = t(synth.dense(1100, F, seed=8)).requires_grad_(True)
+    W = t(synth.dense(900, F, seed=9))
+    ws = None
+    if path == "slab":                      # forward samples into the workspace, backward reuses it
+        monkeypatch.setenv("ES_SPMM_SLAB", "1")
+        ws = es.es_spmm_workspace(900, 1100, len(colind), F, F, 24, True, device=DEV)
     for seed in (1, 2):                     # a new sampled subset per "iteration"
-        C = sampled_spmm(B, t(rowptr), t(colind), t(val), 24, 2, seed, 1)
+        C = sampled_spmm(B, t(rowptr), t(colind), t(val), 24, 2, seed, 1, workspace=ws)
         loss = (C * W).sum()
         B.grad = None
         loss.backward()
@@ -118,3 +124,27 @@ def test_deterministic_backward_parity_and_reproducibility(graph, F, reduce):
                                   deterministic=True).cpu().numpy()
     _, sc, _, _ = oracle.sample(rowptr, colind, None, 64, 2, 9)
     assert np.array_equal(ones, np.repeat(np.bincount(sc, minlength=1100).astype(np.float32)[:, None], F, 1))
+
+
+@pytest.mark.parametrize("F,ld", [(17, 20), (64, 64), (128, 128), (602, 604), (602, 608)])
+@pytest.mark.parametrize("strat", [1, 2])
+@pytest.mark.parametrize("reduce", [0, 1])
+def test_slab_backward_parity(graph, F, ld, strat, reduce, monkeypatch):
+    """The feature-sliced backward (a workspace passed): sampling its own slots, and reusing the
+    ones a forward call left in the workspace -- same order-independent bound."""
+    monkeypatch.setenv("ES_SPMM_SLAB", "1")
+    rowptr, colind, val = graph
+    dC = synth.dense(900, F, seed=F + 3, ld=ld)
+    B = synth.dense(1100, F, seed=F + 4, ld=ld)
+    ws = es.es_spmm_workspace(900, 1100, len(colind), F, ld, 64, True, device=DEV)
+    for reuse in (False, True):
+        if reuse:                                   # forward samples into the workspace first
+            es.es_spmm_run_ex(t(rowptr), t(colind), t(val), t(B), 64, strat, 9, reduce, F=F, workspace=ws)
+        dB = torch.zeros((1100, ld), dtype=torch.float32, device=DEV)
+        es.es_spmm_backward_ex(t(rowptr), t(colind), t(val), t(dC), 1100, 64, strat, 9, reduce, F=F, dB=dB,
+                               workspace=ws, reuse_sampled=reuse)
+        g = dB.cpu().numpy()
+        ok, worst = bound_ok(g[:, :F], rowptr, colind, val, dC[:, :F], 1100, 64, strat, 9, reduce)
+        assert ok, (reuse, worst)
+        if ld > F:
+            assert np.all(g[:, F:] == 0)
