@@ -10,12 +10,17 @@ Pubmed/Reddit (hidden 32 / 128), 3 layers on Arxiv/Proteins (hidden 256).
 * GraphSage-mean (L1256): h' = sigma(h W_self + mean_s(h) W_neigh) -- mean over the
   sampled neighbours at the input width, divided by k_i inside the kernel (L1570-1575).
 Weights are seeded random (no trained weights exist here).
+
+With a `workspace` (es_spmm_workspace(...) sized for the widest aggregation, has_val as the
+model's A), every aggregation the library's plan sends to the slab path runs there, and all
+but the first reuse the slots the first one sampled (reuse_sampled): the layers aggregate over
+one sampled graph, sampled once per forward.
 """
 from __future__ import annotations
 
 import numpy as np
 
-from . import ES_REDUCE_MEAN, ES_REDUCE_SUM, es_spmm_run
+from . import ES_REDUCE_MEAN, ES_REDUCE_SUM, es_spmm_run, es_spmm_run_ex, es_spmm_workspace_bytes
 
 
 def init_weights(model: str, dims: list[int], seed: int = 0) -> list[dict]:
@@ -32,13 +37,28 @@ def init_weights(model: str, dims: list[int], seed: int = 0) -> list[dict]:
     return layers
 
 
-def forward(model: str, rowptr, colind, val, X, layers, s: int, strategy: int, seed: int = 0):
+def forward(model: str, rowptr, colind, val, X, layers, s: int, strategy: int, seed: int = 0,
+            workspace=None):
     """Logits on the GPU.  rowptr/colind/val/X are CUDA tensors; returns an (N, classes) tensor.
     X may carry row padding (X.shape[1] >= the first layer's input width, e.g. ldb 604 for
     F = 602 so the aggregation gathers 16-B rows)."""
     import torch
     prev = torch.backends.cuda.matmul.allow_tf32
     torch.backends.cuda.matmul.allow_tf32 = False
+    n_rows, nnz = rowptr.numel() - 1, colind.numel()
+    sampled = [False]
+
+    def aggregate(rp, ci, v, B, s_, strat, seed_, reduce, F=None):
+        """The sampled SpMM through the library's plan (slab path + slot reuse with a workspace)."""
+        F = B.shape[1] if F is None else F
+        if workspace is not None and es_spmm_workspace_bytes(n_rows, B.shape[0], nnz, F, B.shape[1], s_,
+                                                             v is not None) > 0:
+            out = es_spmm_run_ex(rp, ci, v, B, s_, strat, seed_, reduce, F=F, workspace=workspace,
+                                 reuse_sampled=sampled[0])
+            sampled[0] = True
+            return out
+        return es_spmm_run(rp, ci, v, B, s_, strat, seed_, reduce, F=F)
+
     try:
         h = X
         n = len(layers)
@@ -49,10 +69,10 @@ def forward(model: str, rowptr, colind, val, X, layers, s: int, strategy: int, s
             hv = h[:, :fi]
             if model == "gcn":
                 hw = (hv @ W).contiguous()
-                out = es_spmm_run(rowptr, colind, val, hw, s, strategy, seed, ES_REDUCE_SUM) + b
+                out = aggregate(rowptr, colind, val, hw, s, strategy, seed, ES_REDUCE_SUM) + b
             else:
                 Wn = torch.from_numpy(w["W_neigh"]).to(X.device)
-                agg = es_spmm_run(rowptr, colind, None, h.contiguous(), s, strategy, seed, ES_REDUCE_MEAN,
+                agg = aggregate(rowptr, colind, None, h.contiguous(), s, strategy, seed, ES_REDUCE_MEAN,
                                   F=fi)
                 out = hv @ W + agg @ Wn + b
             h = torch.relu(out) if li + 1 < n else out
