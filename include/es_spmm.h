@@ -113,8 +113,9 @@ typedef struct {
  * entries (nnz >= rowptr[row_end] - rowptr[row_begin] is a precondition like the CSR
  * invariants; the kernels never read or write past the workspace), sampling cap s, feature
  * width F, and B of n_cols rows with pitch ldb.  > 0 when the measured plan prefers the slab
- * path: F >= 128, a 64-float slab of B (n_cols x 256 B) fits L2, and rows sample >= 128 slots
- * on average (min(s, nnz / n_rows) >= 128).  0 otherwise: pass no workspace then.
+ * path: F >= 128, a 64-float slab of B (n_cols x 256 B) fits L2, and rows sample enough slots
+ * on average: min(s, nnz / n_rows) >= 128 for F > 128, >= 192 for F <= 128.  0 otherwise: pass
+ * no workspace then.
  * has_val = 0 when val will be NULL (no slot values are stored). */
 int64_t es_spmm_workspace_bytes(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t F, int64_t ldb,
                                 int32_t s, int32_t has_val);

@@ -83,17 +83,19 @@ bool slab_feasible(int64_t n_cols, int64_t F) {
 }
 
 // es_spmm_workspace_bytes's choice (measured, profiles/r01.md "Slab path" and the s-sweep in
-// BASELINE.md): feasible, F >= 128, and rows that sample >= 128 slots on average -- the bound
-// used is min(s, nnz / n_rows).  Reddit-shaped s=256: F=602 9.8 -> 7.8 ms, F=128 1.89 -> 1.65;
-// Proteins-shaped (B L2-resident) 1.21 -> 1.08.  Below ~128 slots per row the per-row start-up
-// of each slice pass outweighs the L2-resident gathers (Reddit F=602 s=16: 2.0 vs 4.9 TFLOP/s,
-// s=64: 5.0-5.2 vs 5.1-6.2), and short rows (Arxiv-shaped, mean degree 14) keep the fused kernel.
+// BASELINE.md): feasible, F >= 128, and rows that sample enough slots on average -- the bound
+// used is min(s, nnz / n_rows) >= 128 for F > 128 (several slices: Reddit-shaped F=602 s=128
+// 5.8 -> 4.95 ms, s=256 9.8 -> 7.8 ms) and >= 192 for F <= 128 (two slices; at s=128 the fused
+// two-slot ring is 1-6 % faster, at s=192 the slab path wins 1.50 -> 1.39 ms).  Below that each
+// slice pass's per-row start-up outweighs the L2-resident gathers (Reddit F=602 s=16: 2.0 vs
+// 4.5 TFLOP/s), and short rows (Arxiv-shaped, mean degree 14) keep the fused kernel.
 bool slab_wanted(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t F, int64_t s) {
     if (!slab_feasible(n_cols, F)) return false;
     if (env_i64("ES_SPMM_SLAB", -1) == 1) return true;
     const int64_t mean_deg = n_rows > 0 ? nnz / n_rows : 0;
     const int64_t k_est = s < mean_deg ? s : mean_deg;
-    return F >= env_i64("ES_SPMM_SLAB_MIN_F", 128) && k_est >= env_i64("ES_SPMM_SLAB_MIN_K", 128);
+    const int64_t min_k = env_i64("ES_SPMM_SLAB_MIN_K", F > 128 ? 128 : 192);
+    return F >= env_i64("ES_SPMM_SLAB_MIN_F", 128) && k_est >= min_k;
 }
 
 int64_t slab_align(int64_t x) { return (x + 255) & ~(int64_t)255; }
@@ -178,7 +180,7 @@ es_status_t run_rows_impl(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
     p.b_bf16 = o.bf16;
     p.c_peers = o.c_peers;
     p.n_peers = o.n_peers;
-    const es::Plan plan = o.bf16 ? es::make_plan_bf16(F, ldb, ldc, B, C) : es::make_plan(F, ldb, ldc, B, C);
+    const es::Plan plan = o.bf16 ? es::make_plan_bf16(F, ldb, ldc, B, C) : es::make_plan(F, ldb, ldc, B, C, s);
     if (plan.unsupported) return ES_ERR_UNSUPPORTED;
     const uintptr_t bu = reinterpret_cast<uintptr_t>(B), cu = reinterpret_cast<uintptr_t>(C);
     if (o.workspace && !o.bf16 && bu % 16 == 0 && ldb % 4 == 0 && cu % 16 == 0 &&

@@ -101,7 +101,7 @@ cudaError_t launch_backward(const BwdParams& p, cudaStream_t st);
 cudaError_t launch_backward_deterministic(const BwdParams& p, int64_t n_cols, cudaStream_t st, int* launches,
                                           bool* too_large);
 
-Plan make_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C);
+Plan make_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C, int32_t s = INT32_MAX);
 Plan make_plan_bf16(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C);
 cudaError_t launch_spmm(SpmmParams p, const Plan& plan, cudaStream_t st);
 cudaError_t launch_sample_count(const int64_t* rowptr, int64_t n, int32_t s, int64_t* s_rowptr,

@@ -1000,7 +1000,7 @@ Plan make_plan_bf16(int64_t F, int64_t ldb, int64_t ldc, const void* B, const vo
     return pl;
 }
 
-Plan make_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C) {
+Plan make_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C, int32_t s) {
     Plan pl{};
     const uintptr_t b = reinterpret_cast<uintptr_t>(B), c = reinterpret_cast<uintptr_t>(C);
     if (b % 16 == 0 && ldb % 4 == 0) pl.vec = 4;
@@ -1048,8 +1048,11 @@ Plan make_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C
         int stages = env_int("ES_SPMM_STAGES", 0);
         if (stages != 3 && stages != 8) stages = 4;
         pl.stages = stages;
+        // rows per warp: 4 when rows are short (s <= 64: the warp's slot stream then spans
+        // several rows and one CTA's start-up serves them; Reddit F=602 s=16 1.08 -> 0.94 ms,
+        // bitwise identical; profiles/r01.md), else 1 (s = 256: 1 is best)
         const int rpw = env_int("ES_SPMM_ROWS_PER_WARP", 0);
-        pl.rows_per_warp = (rpw >= 1 && rpw <= 32) ? rpw : 1;
+        pl.rows_per_warp = (rpw >= 1 && rpw <= 32) ? rpw : (s <= 64 ? 4 : 1);
         pl.minb = env_int("ES_SPMM_MINB", 1);
     }
     return pl;
