@@ -384,15 +384,16 @@ spmm_cpasync(const SpmmParams p) {
 // sums its slots in order with 32-slot-chunk partials; the halves are added at the end
 // (a + b in both halves, so every lane holds the same bits).  Deterministic; a different
 // (interleaved) order than spmm_cpasync, inside the same error bound.
-template <int D, int MINB>
-__global__ void __launch_bounds__(kThreads, MINB)
+// W warps per CTA (register cap as for MINB 256-thread CTAs).
+template <int D, int MINB, int W = kWarps>
+__global__ void __launch_bounds__(32 * W, MINB * kWarps / W)
 spmm_cpasync_hw(const SpmmParams p) {
     static_assert(D >= 1 && D <= 8, "ring depth (2D slots must fit one 32-slot chunk)");
-    extern __shared__ __align__(16) float4 ring_smem[];          // [kWarps][D][2][32]
+    extern __shared__ __align__(16) float4 ring_smem[];          // [W][D][2][32]
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int h = lane >> 4, sub = lane & 15;
-    const int64_t r = (int64_t)blockIdx.x * kWarps + warp;
+    const int64_t r = (int64_t)blockIdx.x * W + warp;
     if (r >= p.n_rows) return;
     const uint64_t pol_a = policy_evict_first();
     const uint64_t pol_b = policy_evict_last();
@@ -808,6 +809,11 @@ sample_materialize(const int64_t* __restrict__ rowptr, int64_t nnz_base,
 // ------------------------------------------------------------------ host launchers
 namespace {
 
+int env_int_k(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return e ? atoi(e) : dflt;
+}
+
 template <int NCH, int D, int MINB, typename TB = float>
 cudaError_t launch_cpasync_k(const SpmmParams& p, cudaStream_t st) {
     const int64_t blocks = (p.n_rows + kWarps - 1) / kWarps;
@@ -831,17 +837,25 @@ cudaError_t launch_cpasync_bf16(const SpmmParams& p, const Plan& plan, cudaStrea
     }
 }
 
-template <int D, int MINB>
-cudaError_t launch_cpasync_hw_k(const SpmmParams& p, cudaStream_t st) {
-    const int64_t blocks = (p.n_rows + kWarps - 1) / kWarps;
-    const size_t smem = (size_t)kWarps * D * 64 * 16;
-    auto k = spmm_cpasync_hw<D, MINB>;
+template <int D, int MINB, int W>
+cudaError_t launch_cpasync_hw_w(const SpmmParams& p, cudaStream_t st) {
+    const int64_t blocks = (p.n_rows + W - 1) / W;
+    const size_t smem = (size_t)W * D * 64 * 16;
+    auto k = spmm_cpasync_hw<D, MINB, W>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
-    k<<<(unsigned)blocks, kThreads, smem, st>>>(p);
+    k<<<(unsigned)blocks, 32 * W, smem, st>>>(p);
     return cudaGetLastError();
+}
+
+template <int D, int MINB>
+cudaError_t launch_cpasync_hw_k(const SpmmParams& p, cudaStream_t st) {
+    const int w = env_int_k("ES_SPMM_HW_CTA_WARPS", 8);      // tuning: warps per CTA
+    if (w == 4) return launch_cpasync_hw_w<D, MINB, 4>(p, st);
+    if (w == 2) return launch_cpasync_hw_w<D, MINB, 2>(p, st);
+    return launch_cpasync_hw_w<D, MINB, 8>(p, st);
 }
 
 cudaError_t launch_cpasync(const SpmmParams& p, const Plan& plan, cudaStream_t st) {

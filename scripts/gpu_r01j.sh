@@ -21,3 +21,5 @@ for spec in "reddit602:56:14:--config reddit" "reddit128:24:6:--config reddit --
   [ "$name" != "reddit602" ] && rm -f $OUT/step_$name.ncu-rep
 done
 du -sh $OUT
+timeout 1200 python scripts/s_sweep.py > $OUT/s_sweep.jsonl 2> $OUT/s_sweep.err
+timeout 600 python scripts/e2e_gnn.py > $OUT/e2e_gnn.jsonl 2> $OUT/e2e_gnn.err
