@@ -852,7 +852,9 @@ cudaError_t launch_cpasync_hw_w(const SpmmParams& p, cudaStream_t st) {
 
 template <int D, int MINB>
 cudaError_t launch_cpasync_hw_k(const SpmmParams& p, cudaStream_t st) {
-    const int w = env_int_k("ES_SPMM_HW_CTA_WARPS", 8);      // tuning: warps per CTA
+    // 2-warp CTAs: a CTA's slot frees as soon as its 2 rows are done (short, unequal rows:
+    // Arxiv-shaped F=128 s=64 0.177 -> 0.156 ms; Proteins s=64 -0.7 %; profiles/r01.md)
+    const int w = env_int_k("ES_SPMM_HW_CTA_WARPS", 2);      // tuning: warps per CTA
     if (w == 4) return launch_cpasync_hw_w<D, MINB, 4>(p, st);
     if (w == 2) return launch_cpasync_hw_w<D, MINB, 2>(p, st);
     return launch_cpasync_hw_w<D, MINB, 8>(p, st);
