@@ -90,7 +90,8 @@ typedef struct {
      * slots by column, one writer per dB row; takes stream-ordered scratch and synchronises the
      * stream once to size it; K and n_cols must be < 2^31, else ES_ERR_UNSUPPORTED). */
     int32_t deterministic;
-    /* Feature-sliced ("slab") path (es_spmm_run_ex only).  A caller-owned device
+    /* Feature-sliced ("slab") path (es_spmm_run_ex; es_spmm_backward_ex: see there; DESIGN.md §5
+     * "Feature-sliced path"; the reason is Alg. 1 l.13-15: C[:, c] needs only B[:, c]).  A caller-owned device
      * workspace of workspace_bytes >= es_spmm_workspace_bytes(...) bytes makes the call
      * materialise the sampled slots once (es_spmm_sample's layout) and run the gather-FMA one
      * 64-float feature slice at a time, each slice's B slab (n_cols x 256 B) L2-resident.  Pass
@@ -98,8 +99,9 @@ typedef struct {
      * the call takes the path whenever a workspace is given and the slab fits L2.  Same C as
      * the fused kernels within the parity bound; the fused all-gather (c_peers) applies to it as
      * well.  NULL, or a layout the path does not take (bf16 B, B or C not 16-B aligned,
-     * F <= 16) = the fused kernels.  The
-     * workspace must not be shared by calls in flight. */
+     * F <= 16) = the fused kernels.  The workspace must not be shared by calls in flight.
+     * Launches: count + scan + sample materialisation + one per 64-float slice, all on `stream`;
+     * no allocation, no synchronisation.  (Read only when struct_size covers them.) */
     void* workspace;
     int64_t workspace_bytes;
     /* Slab path only: 1 = skip the sampling stage (a1-a3) and reuse the sampled slots already in
