@@ -259,21 +259,16 @@ def main():
         peers = PeerBuffers(n, C_d.stride(0), device=dev)
     # the library's plan: a workspace (allocated once, outside the timed region) selects the
     # feature-sliced path when B does not fit L2 but a 64-float slab of it does
-    ws = None
-    if not a.bf16:
-        ws = es.es_spmm_workspace(r1 - r0, n, e1 - e0, F, ldb, a.s, True, device=dev)
+    ws = es.es_spmm_workspace(r1 - r0, n, e1 - e0, F, ldb, a.s, True, device=dev)
 
     def launch(st):
         if peers is not None:
             es.es_spmm_run_ex(rp_d, ci_d, va_d, B_d, a.s, strat_id, a.seed, red_id, F=F, C=peers.C,
                               row_begin=r0, row_end=r1, n_rows=n, nnz_base=e0, c_peers=peers.peers,
                               n_peers=peers.world, workspace=ws, stream=st)
-        elif ws is not None:
+        elif ws is not None or a.bf16:
             es.es_spmm_run_ex(rp_d, ci_d, va_d, B_d, a.s, strat_id, a.seed, red_id, F=F, C=C_d,
                               row_begin=r0, row_end=r1, n_rows=n, nnz_base=e0, workspace=ws, stream=st)
-        elif a.bf16:
-            es.es_spmm_run_ex(rp_d, ci_d, va_d, B_d, a.s, strat_id, a.seed, red_id, F=F, C=C_d,
-                              row_begin=r0, row_end=r1, n_rows=n, nnz_base=e0, stream=st)
         else:
             es.es_spmm_run_rows(n, rp_d, e0, ci_d, va_d, B_d, a.s, strat_id, a.seed, red_id, r0, r1,
                                 F=F, C=C_d, stream=st)
@@ -370,7 +365,8 @@ def main():
         # ncu: ~97 % of the step).  Its launches are timed alone here, live, on the launch stream
         # with the same L2 flush: the same call with reuse_sampled=1 runs exactly the slice passes
         # over the slots the timed steps sampled into the workspace.
-        n_sl = (F + 63) // 64
+        wsl = 128 if a.bf16 else 64                        # elements per 256-B slab row
+        n_sl = (F + wsl - 1) // wsl
         pe0 = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
         pe1 = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
         for i in range(a.steps):
@@ -384,19 +380,19 @@ def main():
         torch.cuda.synchronize(dev)
         t_passes = float(np.sum([x.elapsed_time(y) for x, y in zip(pe0, pe1)])) / 1e3 / a.steps   # s per step
         nr_ = r1 - r0
-        # per launch (slice of width w): 8k (compact col+val) + 8(N+1) + 4wK + 4wN -- summed over slices
-        bytes_passes = n_sl * (8 * K_rank + 8 * (nr_ + 1)) + 4 * F * K_rank + 4 * F * nr_
+        # per launch (slice of width w): 8k (compact col+val) + 8(N+1) + b*wK + 4wN -- summed over slices
+        bytes_passes = n_sl * (8 * K_rank + 8 * (nr_ + 1)) + b_elem * F * K_rank + 4 * F * nr_
         achieved = bytes_passes / t_passes / 1e9
         roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                     "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
                     "bytes_per_launch": int(bytes_passes / n_sl), "launch_ms": round(1e3 * t_passes / n_sl, 4),
                     "launches_per_step": n_sl,
-                    "bytes_model": "per slice launch (width w): 8K (compact sampled colind+val) + 8(N+1) + 4wK "
-                                   "(B-slab gathers) + 4wN (C slice); summed over the slices = " + bytes_model
-                                   + " + (slices-1)(8K + 8(N+1))",
-                    "kernel": f"es::spmm_slab (8 lanes x 2 pieces per slot, ring depth 4, 4-warp CTAs), one launch "
-                              f"per 64-float feature slice ({n_sl}/step); achieved = its algorithmic bytes / its "
-                              f"average launch time, timed live (reuse_sampled passes)",
+                    "bytes_model": f"per slice launch (width w): 8K (compact sampled colind+val) + 8(N+1) + "
+                                   f"{b_elem}wK (B-slab gathers) + 4wN (C slice); summed over the slices = "
+                                   + bytes_model + " + (slices-1)(8K + 8(N+1))",
+                    "kernel": f"es::spmm_slab{'<bf16>' if a.bf16 else ''} (8 lanes x 2 pieces per slot, ring depth 4, "
+                              f"4-warp CTAs), one launch per {wsl}-element feature slice ({n_sl}/step); achieved = its "
+                              f"algorithmic bytes / its average launch time, timed live (reuse_sampled passes)",
                     "limiter": "shared-memory/L1tex throughput (ncu: L1/TEX 79.8 % of peak, L2 hit 91.5 %, "
                                "DRAM 8.5 %); every B byte crosses smem twice",
                     "step": {"achieved": round(step_achieved, 1), "frac": round(step_achieved / peak, 4),

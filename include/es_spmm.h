@@ -98,8 +98,8 @@ typedef struct {
      * it only when es_spmm_workspace_bytes returned > 0 (that is where it was measured faster);
      * the call takes the path whenever a workspace is given and the slab fits L2.  Same C as
      * the fused kernels within the parity bound; the fused all-gather (c_peers) applies to it as
-     * well.  NULL, or a layout the path does not take (bf16 B, B or C not 16-B aligned,
-     * F <= 16) = the fused kernels.  The workspace must not be shared by calls in flight.
+     * well, and so does bf16 storage of B (128-element slices).  NULL, or a layout the path
+     * does not take (B or C not 16-B aligned, F <= 16) = the fused kernels.  The workspace must not be shared by calls in flight.
      * Launches: count + scan + sample materialisation + one per 64-float slice, all on `stream`;
      * no allocation, no synchronisation.  (Read only when struct_size covers them.) */
     void* workspace;

@@ -183,7 +183,7 @@ es_status_t run_rows_impl(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
     const es::Plan plan = o.bf16 ? es::make_plan_bf16(F, ldb, ldc, B, C) : es::make_plan(F, ldb, ldc, B, C, s);
     if (plan.unsupported) return ES_ERR_UNSUPPORTED;
     const uintptr_t bu = reinterpret_cast<uintptr_t>(B), cu = reinterpret_cast<uintptr_t>(C);
-    if (o.workspace && !o.bf16 && bu % 16 == 0 && ldb % 4 == 0 && cu % 16 == 0 &&
+    if (o.workspace && bu % 16 == 0 && ldb % (o.bf16 ? 8 : 4) == 0 && cu % 16 == 0 &&
         ldc % 4 == 0 && slab_feasible(n_cols, F)) {
         SlabSlots sl;
         int launches = 0;
@@ -194,7 +194,9 @@ es_status_t run_rows_impl(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
                                   &launches);
             const int stages = (int)env_i64("ES_SPMM_SLAB_STAGES", 4);
             const int lanes = (int)env_i64("ES_SPMM_SLAB_G", 8);
-            for (int64_t c0 = 0; err == cudaSuccess && c0 < F; c0 += kSlabF) {
+            // slices of 256-B slab rows: 64 fp32 or 128 bf16 elements
+            const int64_t wsl = o.bf16 ? 2 * kSlabF : kSlabF;
+            for (int64_t c0 = 0; err == cudaSuccess && c0 < F; c0 += wsl) {
                 es::SlabParams sp{};
                 sp.s_rowptr = sl.s_rowptr;
                 sp.slot_base = 0;
@@ -202,10 +204,12 @@ es_status_t run_rows_impl(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
                 sp.s_colind = sl.s_col;
                 sp.s_val = sl.s_val;
                 sp.rowptr = rowptr;
-                sp.B = static_cast<const float*>(B) + c0;
+                sp.b_bf16 = o.bf16;
+                sp.B = o.bf16 ? reinterpret_cast<const float*>(static_cast<const uint16_t*>(B) + c0)
+                              : static_cast<const float*>(B) + c0;
                 sp.ldb = ldb;
-                sp.w = (int32_t)(F - c0 < kSlabF ? F - c0 : kSlabF);
-                sp.nv = (sp.w + 3) / 4;
+                sp.w = (int32_t)(F - c0 < wsl ? F - c0 : wsl);
+                sp.nv = o.bf16 ? (sp.w + 7) / 8 : (sp.w + 3) / 4;
                 sp.C = C + c0;
                 sp.c_peers = o.c_peers;
                 sp.n_peers = o.n_peers;

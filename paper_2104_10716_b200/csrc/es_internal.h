@@ -86,6 +86,7 @@ struct SlabParams {
     int32_t n_peers;
     int64_t row_base;         // global id of local row 0 (peer stores)
     int64_t col0;             // the slice's first column (peer stores)
+    int32_t b_bf16;           // B holds bf16 (NEXT-4 storage variant): B points at uint16_t elements
 };
 
 cudaError_t launch_slab_pass(const SlabParams& p, int lanes_per_slot, int stages, cudaStream_t st);

@@ -35,6 +35,27 @@ __device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const void* src, 
                  : "memory");
 }
 
+// A 16-B piece of a B row: 4 fp32, or 8 bf16 widened exactly to fp32 (NEXT-4 storage variant).
+template <bool BF16> struct SlabPiece;
+template <> struct SlabPiece<false> {
+    static constexpr int kElems = 4;
+    __device__ __forceinline__ static void widen(const float4& raw, float* out) {
+        out[0] = raw.x; out[1] = raw.y; out[2] = raw.z; out[3] = raw.w;
+    }
+};
+template <> struct SlabPiece<true> {
+    static constexpr int kElems = 8;
+    __device__ __forceinline__ static void widen(const float4& raw, float* out) {
+        const uint32_t w[4] = {__float_as_uint(raw.x), __float_as_uint(raw.y), __float_as_uint(raw.z),
+                               __float_as_uint(raw.w)};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            out[2 * i] = __uint_as_float(w[i] << 16);
+            out[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+        }
+    }
+};
+
 __device__ __forceinline__ float4 lds128(uint32_t addr) {
     float4 v;
     asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr)
@@ -52,9 +73,10 @@ __device__ __forceinline__ float4 lds128(uint32_t addr) {
 // order, bitwise).
 // W warps per CTA (register cap as for MINB 256-thread CTAs per SM): small CTAs free their
 // slot as soon as their few rows are done instead of waiting for the longest of 8 rows.
-template <int G, int P, int D, int MINB, bool FULL, int W>
+template <int G, int P, int D, int MINB, bool FULL, int W, bool BF16 = false>
 __global__ void __launch_bounds__(32 * W, MINB * 8 / W)
 spmm_slab(const SlabParams p) {
+    constexpr int E = SlabPiece<BF16>::kElems;   // B elements (-> fp32 accumulators) per piece
     constexpr int S = 32 / G;            // slots per step
     constexpr int U = 32 / S;            // steps per 32-slot chunk (= G)
     static_assert((G == 2 || G == 4 || G == 8 || G == 16) && G * P <= 16, "lanes x pieces per slot");
@@ -72,7 +94,7 @@ spmm_slab(const SlabParams p) {
     const int32_t k = end > beg ? (int32_t)(end - beg) : 0;
     const uint32_t my_s = smem_u32(slab_ring + (size_t)warp * D * kStage + e * (P * G) + sub);
     const char* bl = reinterpret_cast<const char*>(p.B) + sub * 16;
-    const uint32_t row_bytes = (uint32_t)(p.ldb * 4);
+    const uint32_t row_bytes = (uint32_t)(p.ldb * (BF16 ? 2 : 4));
 
     // FULL: all 16 pieces of the slice exist (every slice but a narrower last one)
     auto copy = [&](int stage, int32_t col, bool valid) {
@@ -100,11 +122,11 @@ spmm_slab(const SlabParams p) {
         copy(t, __shfl_sync(kAll, c0, S * t + e), S * t + e < k);
         cp_async_commit();
     }
-    float part[P][4], tot[P][4];
+    float part[P][E], tot[P][E];
 #pragma unroll
     for (int q = 0; q < P; ++q)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) { part[q][c] = 0.0f; tot[q][c] = 0.0f; }
+        for (int c = 0; c < E; ++c) { part[q][c] = 0.0f; tot[q][c] = 0.0f; }
     for (int32_t j0 = 0; j0 < k; j0 += 32) {
 #pragma unroll 1
         for (int u0 = 0; u0 < U; u0 += D) {
@@ -115,11 +137,10 @@ spmm_slab(const SlabParams p) {
                 const float av = __shfl_sync(kAll, a0, S * u + e);
 #pragma unroll
                 for (int q = 0; q < P; ++q) {
-                    const float4 x = lds128(my_s + (d * kStage + q * G) * 16);
-                    part[q][0] = fmaf(av, x.x, part[q][0]);
-                    part[q][1] = fmaf(av, x.y, part[q][1]);
-                    part[q][2] = fmaf(av, x.z, part[q][2]);
-                    part[q][3] = fmaf(av, x.w, part[q][3]);
+                    float x[E];
+                    SlabPiece<BF16>::widen(lds128(my_s + (d * kStage + q * G) * 16), x);
+#pragma unroll
+                    for (int c = 0; c < E; ++c) part[q][c] = fmaf(av, x[c], part[q][c]);
                 }
                 const int tn = u + D;                            // refill: step u + D
                 const int32_t cn = __shfl_sync(kAll, tn < U ? c0 : c1, (S * tn + e) & 31);
@@ -130,7 +151,7 @@ spmm_slab(const SlabParams p) {
 #pragma unroll
         for (int q = 0; q < P; ++q)
 #pragma unroll
-            for (int c = 0; c < 4; ++c) { tot[q][c] += part[q][c]; part[q][c] = 0.0f; }
+            for (int c = 0; c < E; ++c) { tot[q][c] += part[q][c]; part[q][c] = 0.0f; }
         c0 = c1;
         a0 = a1;
         c1 = 0;
@@ -149,7 +170,7 @@ spmm_slab(const SlabParams p) {
 #pragma unroll
         for (int q = 0; q < P; ++q)
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 0; c < E; ++c) {
                 const float other = __shfl_xor_sync(kAll, tot[q][c], o);
                 tot[q][c] = (lane & o) ? other + tot[q][c] : tot[q][c] + other;
             }
@@ -158,34 +179,41 @@ spmm_slab(const SlabParams p) {
         for (int q = 0; q < P; ++q) {
             const int piece = sub + G * q;
             if (FULL || piece < p.nv) {
-                float res[4];
 #pragma unroll
-                for (int c = 0; c < 4; ++c)
-                    res[c] = p.reduce == kMean ? (div > 0 ? __fdiv_rn(tot[q][c], (float)div) : 0.0f) : tot[q][c];
-                const int rem = p.w - piece * 4;                 // valid floats of this piece
-                auto put = [&](float* dst) {
-                    if (p.c_vec && rem >= 4) st_stream4(dst, res, pol_a);
-                    else
+                for (int h4 = 0; h4 < E / 4; ++h4) {                 // 4 output floats at a time
+                    float res[4];
 #pragma unroll
-                        for (int c = 0; c < 4; ++c)
-                            if (c < rem) st_stream(dst + c, res[c], pol_a);
-                };
-                if (p.n_peers == 0) {
-                    put(p.C + r * p.ldc + piece * 4);
-                } else {                                         // fused all-gather: every rank's C
-                    const int64_t off = (p.row_base + r) * p.ldc + p.col0 + piece * 4;
-                    for (int q2 = 0; q2 < p.n_peers; ++q2) put(p.c_peers[q2] + off);
+                    for (int c = 0; c < 4; ++c) {
+                        const float t = tot[q][4 * h4 + c];
+                        res[c] = p.reduce == kMean ? (div > 0 ? __fdiv_rn(t, (float)div) : 0.0f) : t;
+                    }
+                    const int col = piece * E + 4 * h4;              // first output column
+                    const int rem = p.w - col;                       // valid floats from there
+                    auto put = [&](float* dst) {
+                        if (p.c_vec && rem >= 4) st_stream4(dst, res, pol_a);
+                        else
+#pragma unroll
+                            for (int c = 0; c < 4; ++c)
+                                if (c < rem) st_stream(dst + c, res[c], pol_a);
+                    };
+                    if (rem <= 0) continue;
+                    if (p.n_peers == 0) {
+                        put(p.C + r * p.ldc + col);
+                    } else {                                     // fused all-gather: every rank's C
+                        const int64_t off = (p.row_base + r) * p.ldc + p.col0 + col;
+                        for (int q2 = 0; q2 < p.n_peers; ++q2) put(p.c_peers[q2] + off);
+                    }
                 }
             }
         }
     }
 }
 
-template <int G, int P, int D, int MINB, int W>
+template <int G, int P, int D, int MINB, int W, bool BF16 = false>
 cudaError_t launch_slab_w(const SlabParams& p, cudaStream_t st) {
     const int64_t blocks = (p.n_rows + W - 1) / W;
     const size_t smem = (size_t)W * D * 32 * P * 16;
-    auto k = p.nv == G * P ? spmm_slab<G, P, D, MINB, true, W> : spmm_slab<G, P, D, MINB, false, W>;
+    auto k = p.nv == G * P ? spmm_slab<G, P, D, MINB, true, W, BF16> : spmm_slab<G, P, D, MINB, false, W, BF16>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -280,6 +308,12 @@ spmm_slab_bwd(const SlabParams p, const float* __restrict__ dC, float* __restric
 // all slower: profiles/r01.md "Slab path".
 cudaError_t launch_slab_pass(const SlabParams& p, int lanes_per_slot, int stages, cudaStream_t st) {
     if (p.n_rows <= 0) return cudaSuccess;
+    if (p.b_bf16) {                      // bf16 B (NEXT-4): 128-element slices, 8 elements per piece
+        if (p.nv <= 4) return launch_slab_w<2, 2, 2, 3, 4, true>(p, st);
+        if (p.nv <= 8) return launch_slab_w<4, 2, 4, 3, 4, true>(p, st);
+        return lanes_per_slot == 16 ? launch_slab_w<16, 1, 4, 4, 4, true>(p, st)
+                                    : launch_slab_w<8, 2, 4, 3, 4, true>(p, st);
+    }
     if (lanes_per_slot == 16) {
         switch (stages) {
             case 2: return launch_slab_k<16, 2, 5>(p, st);

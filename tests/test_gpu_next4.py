@@ -66,13 +66,19 @@ def test_mean_by_degree(graph):
 
 @pytest.mark.parametrize("F,ld", [(8, 8), (16, 16), (100, 104), (128, 128), (256, 256), (602, 608), (1100, 1104)])
 @pytest.mark.parametrize("strat", [1, 2])
-def test_bf16_storage(graph, F, ld, strat):
+@pytest.mark.parametrize("path", ["fused", "slab"])
+def test_bf16_storage(graph, F, ld, strat, path, monkeypatch):
     rowptr, colind, val = graph
     B32 = synth.dense(2300, F, seed=F + 7, ld=ld)
     Bh = t(B32).to(torch.bfloat16)
     Bq = Bh.float().cpu().numpy()          # the exact values the kernel reads
+    ws = None
+    if path == "slab":                     # 128-element bf16 slices (+ narrow tails)
+        monkeypatch.setenv("ES_SPMM_SLAB", "1")
+        ws = es.es_spmm_workspace(1100, 2300, len(colind), F, ld, 256, True, device=DEV)
     for s, reduce in [(16, 0), (256, 1)]:
-        g = es.es_spmm_run_ex(t(rowptr), t(colind), t(val), Bh, s, strat, 3, reduce, F=F).cpu().numpy()
+        g = es.es_spmm_run_ex(t(rowptr), t(colind), t(val), Bh, s, strat, 3, reduce, F=F,
+                              workspace=ws).cpu().numpy()
         o = oracle.spmm(rowptr, colind, val, Bq, s, strat, seed=3, reduce=reduce, F=F)
         ok, err = rel_ok(g, o)
         assert ok, (F, s, err)
