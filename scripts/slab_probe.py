@@ -71,6 +71,9 @@ def main():
         os.environ["ES_SPMM_SLAB"] = "1"
         os.environ["ES_SPMM_SLAB_STAGES"] = st
         os.environ["ES_SPMM_SLAB_G"] = g
+        for kv in filter(None, os.environ.get("SLAB_ENV", "").split(",")):   # extra knobs, e.g. ES_SPMM_SLAB_ROWS=8
+            k_, v_ = kv.split("=")
+            os.environ[k_] = v_
         if len(v) > 2:
             os.environ["ES_SPMM_SLAB_CTA_WARPS"] = v[2]
         if len(v) > 3:
