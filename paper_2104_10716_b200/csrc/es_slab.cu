@@ -3,15 +3,16 @@
 // Why: the gather-FMA touches every B row a row of A samples.  When B does not
 // fit the 126 MB L2 (Reddit-shaped, F=602: 566 MB), most gathers go to HBM although each B row
 // is gathered ~170 times per call.  C[:, c] depends only on B[:, c] (Alg. 1 l.13-15 is a
-// per-feature sum), so the call is split into feature slices of <= 64 floats whose B slab
-// (n_cols x 256 B = 60 MB for Reddit) stays L2-resident for the whole pass:
+// per-feature sum), so the call is split into feature slices of 64 fp32 (or 128 bf16) elements
+// whose B slab (n_cols x 256 B = 60 MB for Reddit) stays L2-resident for the whole pass:
 //   1. es::launch_sample_count + scan : k_i = min(d_i, s) and its prefix     (a1, Alg. 1 l.5-6)
 //   2. es::launch_sample_materialize   : the sampled (col, val) of every row, slot order, compact
 //                                        (a2 + a3, Alg. 1 l.7-11 / Eq. 2) -- read once per call
 //   3. spmm_slab, once per slice       : a4 + a5 over the compact slots   (Alg. 1 l.12-16)
-// Per element, slot j of a row is FMA'd (fp32) into the partial of half-warp (j mod 2); each
-// half adds its partial to its total every 32 slots; the two totals are added at the end --
-// the summation order of spmm_cpasync_hw, so results match that kernel bitwise.
+// Per element, slot j of a row is FMA'd (fp32) into the partial of lane group (j mod S); each
+// group adds its partial to its total every 32 slots; the group totals are added by an xor tree
+// (with S = 2 groups the order of spmm_cpasync_hw, bitwise; DESIGN.md §6 error bound).
+// Also here: the feature-sliced backward (spmm_slab_bwd, NEXT-2).
 #include <cstdint>
 #include <cstdlib>
 #include <cuda_runtime.h>
