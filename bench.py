@@ -33,6 +33,7 @@ sys.path.insert(0, ROOT)
 import synth  # noqa: E402
 
 FALLBACK_HBM_GBS = 6650.0      # /opt/skills/guides/B200_PROFILING.md fallback (only if no measured peak)
+L2_STREAM_GBS = 19777.9        # L2-resident streaming read rate (<= 96 MB footprint), scripts/l2bw.cu on B200
 
 DEFAULTS = {  # workload named in config.workload; BASELINE.json configs[3] (the graded target)
     "pubmed": dict(F=16, s=32, strategy="bucket", reduce="sum"),
@@ -395,6 +396,9 @@ def main():
                               f"algorithmic bytes / its average launch time, timed live (reuse_sampled passes)",
                     "limiter": "shared-memory/L1tex throughput (ncu: L1/TEX 79.8 % of peak, L2 hit 91.5 %, "
                                "DRAM 8.5 %); every B byte crosses smem twice",
+                    # the slabs are L2-resident, so the L2 streaming rate is the other ceiling:
+                    # measured on this B200 by scripts/l2bw.cu (profiles/r01_l2bw_probe.jsonl)
+                    "l2_peak": L2_STREAM_GBS, "l2_frac": round(achieved / L2_STREAM_GBS, 4),
                     "step": {"achieved": round(step_achieved, 1), "frac": round(step_achieved / peak, 4),
                              "launches": launches_per_step,
                              "what": "the whole step (count + scan + sample materialisation + the slice "
