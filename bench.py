@@ -404,6 +404,15 @@ def main():
                              "what": "the whole step (count + scan + sample materialisation + the slice "
                                      "passes): step algorithmic bytes / step time"}}
 
+    # ---------------- compulsory bytes: every B row the sample touches read once --
+    # the distinct sampled columns come from our own sampler (es_spmm_sample), outside the timing
+    compulsory = None
+    if world == 1:
+        _, s_col, _, _ = es.es_spmm_sample(rp_d, ci_d, None, a.s, strat_id, a.seed, row_base=r0, want_pos=False)
+        n_touched = int(torch.unique(s_col).numel())
+        del s_col
+        compulsory = 8 * K_rank + 8 * (n + 1) + b_elem * F * n_touched + 4 * F * n
+
     # ---------------- end to end through the public host API (pinned host buffers)
     e2e = None
     if not a.no_e2e and not a.bf16:
@@ -449,7 +458,12 @@ def main():
                        "step_ms_min": round(1e3 * float(per_step.min()), 4),
                        "step_ms_median": round(1e3 * float(np.median(per_step)), 4),
                        "wall_s_timed_region": round(wall, 4),
-                       "bytes_model_per_step_all_ranks": byte_model(K_all, n, F, b_elem)},
+                       "bytes_model_per_step_all_ranks": byte_model(K_all, n, F, b_elem),
+                       "compulsory_bytes_per_step": compulsory,
+                       "compulsory_model": "8K + 8(N+1) + 4F*N_touched + 4FN (each sampled B row read once; "
+                                           "N_touched = distinct sampled columns, from es_spmm_sample)",
+                       "ms_at_hbm_peak_for_compulsory_bytes": (round(1e3 * compulsory / (peak * 1e9), 4)
+                                                               if compulsory else None)},
         }
         print(json.dumps(out), flush=True)
     if peers is not None:
