@@ -46,6 +46,16 @@ def main():
                 es.es_spmm_run_ex(rp, ci, va, B, 64, 2, 5, 1, F=F, workspace=ws, reuse_sampled=True)
             torch.cuda.synchronize()
             print("ok slab", g, F, ldb, flush=True)
+    # bf16 storage on the slab path (128-element slices + narrow tails) and the slab backward
+    os.environ["ES_SPMM_SLAB_G"] = "8"
+    for F, ldb in ((602, 608), (200, 200), (40, 40)):
+        Bh = t(synth.dense(700, F, seed=F, ld=ldb)).to(torch.bfloat16)
+        ws = es.es_spmm_workspace(300, 700, len(colind), F, ldb, 64, True, device=dev)
+        es.es_spmm_run_ex(rp, ci, va, Bh, 64, 2, 5, 1, F=F, workspace=ws)
+        dC = t(synth.dense(300, F, seed=3, ld=ldb))
+        es.es_spmm_backward_ex(rp, ci, va, dC, 700, 64, 2, 5, 1, F=F, workspace=ws, reuse_sampled=True)
+        torch.cuda.synchronize()
+        print("ok slab bf16 + backward", F, ldb, flush=True)
     os.environ.pop("ES_SPMM_SLAB", None)
     os.environ.pop("ES_SPMM_SLAB_G", None)
     es.es_spmm_sample(rp, ci, va, 40, 2, 9)
