@@ -189,7 +189,10 @@ es_status_t run_rows_impl(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
         int launches = 0;
         cudaError_t err = cudaSuccess;
         if (slab_slots(o, n, val != nullptr, &sl)) {
-            if (!o.reuse_sampled)
+            // Bucket takes the first k_i entries of each row: they already lie contiguous in the
+            // CSR (Alg. 1 with p_j = j), so the passes read them in place -- no sampling pass
+            const bool direct = strategy == ES_BUCKET;
+            if (!o.reuse_sampled && !direct)
                 err = slab_sample(sl, rowptr, nnz_base, colind, val, n, s, strategy, seed, row_begin, o.prime, st,
                                   &launches);
             const int stages = (int)env_i64("ES_SPMM_SLAB_STAGES", 4);
@@ -198,11 +201,12 @@ es_status_t run_rows_impl(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
             const int64_t wsl = o.bf16 ? 2 * kSlabF : kSlabF;
             for (int64_t c0 = 0; err == cudaSuccess && c0 < F; c0 += wsl) {
                 es::SlabParams sp{};
-                sp.s_rowptr = sl.s_rowptr;
-                sp.slot_base = 0;
-                sp.cap = sl.cap;
-                sp.s_colind = sl.s_col;
-                sp.s_val = sl.s_val;
+                sp.s_rowptr = direct ? rowptr : sl.s_rowptr;
+                sp.slot_base = direct ? nnz_base : 0;
+                sp.cap = direct ? INT64_MAX : sl.cap;
+                sp.s_colind = direct ? colind : sl.s_col;
+                sp.s_val = direct ? val : sl.s_val;
+                sp.direct_s = direct ? s : 0;
                 sp.rowptr = rowptr;
                 sp.b_bf16 = o.bf16;
                 sp.B = o.bf16 ? reinterpret_cast<const float*>(static_cast<const uint16_t*>(B) + c0)
@@ -392,15 +396,18 @@ es_status_t es_spmm_backward_ex(int64_t n_rows, int64_t n_cols, const int64_t* r
         cudaStream_t st = as_stream(stream);
         int launches = 0;
         cudaError_t err = cudaSuccess;
-        if (!o.reuse_sampled)
+        const bool direct = strategy == ES_BUCKET;               // first k_i entries, in place
+        if (!o.reuse_sampled && !direct)
             err = slab_sample(sl, rowptr, nnz_base, colind, val, n, s, strategy, seed, row_begin, o.prime, st,
                               &launches);
         for (int64_t c0 = 0; err == cudaSuccess && c0 < F; c0 += kSlabF) {
             es::SlabParams sp{};
-            sp.s_rowptr = sl.s_rowptr;
-            sp.cap = sl.cap;
-            sp.s_colind = sl.s_col;
-            sp.s_val = sl.s_val;
+            sp.s_rowptr = direct ? rowptr : sl.s_rowptr;
+            sp.slot_base = direct ? nnz_base : 0;
+            sp.cap = direct ? INT64_MAX : sl.cap;
+            sp.s_colind = direct ? colind : sl.s_col;
+            sp.s_val = direct ? val : sl.s_val;
+            sp.direct_s = direct ? s : 0;
             sp.rowptr = rowptr;
             sp.ldb = ldb;
             sp.w = (int32_t)(F - c0 < kSlabF ? F - c0 : kSlabF);

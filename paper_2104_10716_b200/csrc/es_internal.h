@@ -87,6 +87,8 @@ struct SlabParams {
     int64_t row_base;         // global id of local row 0 (peer stores)
     int64_t col0;             // the slice's first column (peer stores)
     int32_t b_bf16;           // B holds bf16 (NEXT-4 storage variant): B points at uint16_t elements
+    int32_t direct_s;         // > 0 (Bucket): the slots are the CSR itself -- s_rowptr/s_colind/s_val
+                              // are rowptr/colind/val, k_i = min(d_i, direct_s); no sampling pass
 };
 
 cudaError_t launch_slab_pass(const SlabParams& p, int lanes_per_slot, int stages, cudaStream_t st);

@@ -92,6 +92,7 @@ spmm_slab(const SlabParams p) {
     const int64_t beg = ld_stream(p.s_rowptr + r, policy_evict_first()) - p.slot_base;
     int64_t end = ld_stream(p.s_rowptr + r + 1, policy_evict_first()) - p.slot_base;
     if (end > p.cap) end = p.cap;                                // workspace bound (never read past)
+    if (p.direct_s > 0 && end - beg > p.direct_s) end = beg + p.direct_s;   // Bucket: first s of the row
     const int32_t k = end > beg ? (int32_t)(end - beg) : 0;
     const uint32_t my_s = smem_u32(slab_ring + (size_t)warp * D * kStage + e * (P * G) + sub);
     const char* bl = reinterpret_cast<const char*>(p.B) + sub * 16;
@@ -252,6 +253,7 @@ spmm_slab_bwd(const SlabParams p, const float* __restrict__ dC, float* __restric
     const int64_t beg = ld_stream(p.s_rowptr + r, pol_a) - p.slot_base;
     int64_t end = ld_stream(p.s_rowptr + r + 1, pol_a) - p.slot_base;
     if (end > p.cap) end = p.cap;
+    if (p.direct_s > 0 && end - beg > p.direct_s) end = beg + p.direct_s;
     const int32_t k = end > beg ? (int32_t)(end - beg) : 0;
     if (k == 0) return;
     float div = (float)k;
