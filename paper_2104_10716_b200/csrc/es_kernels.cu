@@ -1105,7 +1105,7 @@ cudaError_t launch_sample_count(const int64_t* rowptr, int64_t n, int32_t s, int
     err = cudaMallocAsync(&temp, temp_bytes, st);
     if (err != cudaSuccess) return err;
     err = cub::DeviceScan::InclusiveSum(temp, temp_bytes, s_rowptr + 1, s_rowptr + 1, n, st);
-    ++*launches;
+    *launches += 2;                      // CUB's scan: DeviceScanInitKernel + DeviceScanKernel (ncu)
     cudaError_t err2 = cudaFreeAsync(temp, st);
     return err != cudaSuccess ? err : err2;
 }

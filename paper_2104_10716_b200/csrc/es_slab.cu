@@ -354,7 +354,7 @@ cudaError_t launch_slab_count(const int64_t* rowptr, int64_t n, int32_t s, int64
     ++*launches;
     if (err != cudaSuccess || n == 0) return err;
     err = cub::DeviceScan::InclusiveSum(temp, temp_bytes, s_rowptr + 1, s_rowptr + 1, n, st);
-    ++*launches;
+    *launches += 2;                      // CUB's scan: DeviceScanInitKernel + DeviceScanKernel (ncu)
     return err;
 }
 

@@ -155,3 +155,19 @@ def test_reuse_sampled_slots(graph, lanes):
     assert np.array_equal(g2.cpu().numpy(), full2)
     o = oracle.spmm(rowptr, colind, val, B2, 96, 2, seed=13, reduce=1, F=300)
     assert rel_ok(full2, o)[0]
+
+
+def test_slab_launch_count(graph, monkeypatch):
+    """The launches es_launch_count reports (bench.py's gpu_launches) match the kernels the slab
+    path runs: count + CUB scan (2 kernels) + materialise + one per 64-float slice; Bucket reads
+    its slots in place (slices only); reuse_sampled runs the slices only."""
+    monkeypatch.setenv("ES_SPMM_SLAB", "1")
+    rowptr, colind, val = graph
+    B = synth.dense(2300, 602, seed=1, ld=608)
+    ws = es.es_spmm_workspace(1301, 2300, len(colind), 602, 608, 256, True, device=DEV)
+    for strat, reuse, want in ((2, False, 4 + 10), (1, False, 10), (2, True, 10)):
+        n0 = es.es_launch_count()
+        es.es_spmm_run_ex(t(rowptr), t(colind), t(val), t(B), 256, strat, 0, 1, F=602, workspace=ws,
+                          reuse_sampled=reuse)
+        torch.cuda.synchronize()
+        assert es.es_launch_count() - n0 == want, (strat, reuse)
