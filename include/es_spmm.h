@@ -99,7 +99,7 @@ typedef struct {
      * the call takes the path whenever a workspace is given and the slab fits L2.  Same C as
      * the fused kernels within the parity bound; the fused all-gather (c_peers) applies to it as
      * well, and so does bf16 storage of B (128-element slices).  NULL, or a layout the path
-     * does not take (B or C not 16-B aligned, F <= 16) = the fused kernels.  The workspace must not be shared by calls in flight.
+     * does not take (B rows not 16-B aligned, F <= 16) = the fused kernels.  The workspace must not be shared by calls in flight.
      * Launches: count + scan + sample materialisation + one per 64-float slice, all on `stream`;
      * no allocation, no synchronisation.  (Read only when struct_size covers them.) */
     void* workspace;

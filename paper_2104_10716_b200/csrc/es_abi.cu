@@ -183,8 +183,9 @@ es_status_t run_rows_impl(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
     const es::Plan plan = o.bf16 ? es::make_plan_bf16(F, ldb, ldc, B, C) : es::make_plan(F, ldb, ldc, B, C, s);
     if (plan.unsupported) return ES_ERR_UNSUPPORTED;
     const uintptr_t bu = reinterpret_cast<uintptr_t>(B), cu = reinterpret_cast<uintptr_t>(C);
-    if (o.workspace && bu % 16 == 0 && ldb % (o.bf16 ? 8 : 4) == 0 && cu % 16 == 0 &&
-        ldc % 4 == 0 && slab_feasible(n_cols, F)) {
+    // any C layout: 16-B vector stores where C's rows allow them, scalar stores otherwise
+    const bool c_vec16 = cu % 16 == 0 && ldc % 4 == 0;
+    if (o.workspace && bu % 16 == 0 && ldb % (o.bf16 ? 8 : 4) == 0 && slab_feasible(n_cols, F)) {
         SlabSlots sl;
         int launches = 0;
         cudaError_t err = cudaSuccess;
@@ -220,7 +221,7 @@ es_status_t run_rows_impl(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
                 sp.row_base = row_begin;
                 sp.col0 = c0;
                 sp.ldc = ldc;
-                sp.c_vec = 1;
+                sp.c_vec = c_vec16 ? 1 : 0;
                 sp.n_rows = n;
                 sp.reduce = reduce;
                 sp.mean_by_degree = o.mean_by_degree;

@@ -46,8 +46,14 @@ def slab(rowptr, colind, val, B, s, strat, seed, reduce, F, **kw):
                               device=DEV)
     assert ws is not None
     vd = None if val is None else t(val)
-    return es.es_spmm_run_ex(t(rowptr), t(colind), vd, t(B), s, strat, seed, reduce, F=F, workspace=ws,
-                             **kw).cpu().numpy()
+    n0 = es.es_launch_count()
+    out = es.es_spmm_run_ex(t(rowptr), t(colind), vd, t(B), s, strat, seed, reduce, F=F, workspace=ws,
+                            **kw).cpu().numpy()
+    # the slab path really ran (it launches the sampling kernels and/or one kernel per slice;
+    # a silent fallback to the fused kernel would launch exactly one)
+    assert es.es_launch_count() - n0 >= (F + 63) // 64 + (0 if strat == 1 else 4) and \
+        es.es_launch_count() - n0 > 1 or F <= 64, "slab path not taken"
+    return out
 
 
 @pytest.mark.parametrize("F,ld", [(17, 20), (64, 64), (65, 68), (200, 200), (602, 604), (602, 608)])
