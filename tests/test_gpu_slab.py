@@ -61,7 +61,7 @@ def slab(rowptr, colind, val, B, s, strat, seed, reduce, F, **kw):
 def test_slab_parity(graph, lanes, F, ld, strat):
     rowptr, colind, val = graph
     B = synth.dense(2300, F, seed=F + 1, ld=ld)
-    for s, seed, reduce in [(32, 0, 0), (256, 5, 1), (1000, 0, 1), (1, 3, 0)]:
+    for s, seed, reduce in [(32, 0, 0), (256, 5, 1), (1000, 0, 1), (1, 3, 0), (100000, 2, 1)]:
         g = slab(rowptr, colind, val, B, s, strat, seed, reduce, F)
         o = oracle.spmm(rowptr, colind, val, B, s, strat, seed=seed, reduce=reduce, F=F)
         ok, err = rel_ok(g, o)
