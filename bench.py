@@ -33,7 +33,7 @@ sys.path.insert(0, ROOT)
 import synth  # noqa: E402
 
 FALLBACK_HBM_GBS = 6650.0      # /opt/skills/guides/B200_PROFILING.md fallback (only if no measured peak)
-L2_STREAM_GBS = 19777.9        # L2-resident streaming read rate (<= 96 MB footprint), scripts/l2bw.cu on B200
+L2_RESIDENT_BYTES = 96 << 20   # a gathered operand up to this size stays L2-resident (126 MB L2; l2_peak.json)
 
 DEFAULTS = {  # workload named in config.workload; BASELINE.json configs[3] (the graded target)
     "pubmed": dict(F=16, s=32, strategy="bucket", reduce="sum"),
@@ -56,9 +56,12 @@ def parse():
     ap.add_argument("--reduce", default=None, choices=["sum", "mean"])
     ap.add_argument("--seed", type=int, default=0, help="FastRand seed (0 = paper-exact Eq. 2)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--kernel", default="auto", choices=["auto", "fused", "slab", "tma", "warp"],
-                    help="kernel family (A/B measurement; auto = the library's plan, fused = never the "
-                         "feature-sliced path, slab = always where it applies)")
+    ap.add_argument("--kernel", default="auto",
+                    choices=["auto", "fused", "slab", "slab_smem", "slab_ldg", "slab_tma", "tma", "warp", "cpasync",
+                             "halfwarp"],
+                    help="kernel family (A/B measurement through es_spmm_options_t.kernel; auto = the "
+                         "library's plan, fused = never the feature-sliced path, slab* = that path wherever "
+                         "it can run)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true", help="warm-L2 variant (not the headline)")
@@ -78,10 +81,6 @@ def parse():
             setattr(a, k, d[k])
     if a.warmup < 3:
         a.warmup = 3
-    if a.kernel in ("tma", "warp"):
-        os.environ["ES_SPMM_KERNEL"] = a.kernel
-    if a.kernel != "auto":
-        os.environ["ES_SPMM_SLAB"] = "1" if a.kernel == "slab" else "0"
     return a
 
 
@@ -93,6 +92,18 @@ def measured_peaks():
         return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy bandwidth)"
     except Exception:
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def l2_peak():
+    """The L2 streaming read rate measured on this pool's B200 (scripts/l2_peak.py ->
+    profiles/l2_peak.json, with its clock record): the ceiling of L2-resident gathers."""
+    path = os.path.join(ROOT, "profiles", "l2_peak.json")
+    try:
+        with open(path) as f:
+            j = json.load(f)
+        return float(j["l2_stream_gbs"]), f"measured (profiles/l2_peak.json: {j['how'][:60]}..., {j.get('when')})"
+    except Exception:
+        return None, None
 
 
 def ldb_for(F, elem=4):
@@ -260,16 +271,21 @@ def main():
         peers = PeerBuffers(n, C_d.stride(0), device=dev)
     # the library's plan: a workspace (allocated once, outside the timed region) selects the
     # feature-sliced path when B does not fit L2 but a 64-float slab of it does
-    ws = es.es_spmm_workspace(r1 - r0, n, e1 - e0, F, ldb, a.s, True, device=dev)
+    slab_family = a.kernel in ("auto", "slab", "slab_smem", "slab_ldg", "slab_tma")
+    ws = (es.es_spmm_workspace(r1 - r0, n, e1 - e0, F, ldb, a.s, True, device=dev,
+                               kernel=None if a.kernel == "auto" else a.kernel) if slab_family else None)
+    kern = None if a.kernel == "auto" else a.kernel
 
-    def launch(st):
+    def launch(st, reuse=False):
         if peers is not None:
             es.es_spmm_run_ex(rp_d, ci_d, va_d, B_d, a.s, strat_id, a.seed, red_id, F=F, C=peers.C,
                               row_begin=r0, row_end=r1, n_rows=n, nnz_base=e0, c_peers=peers.peers,
-                              n_peers=peers.world, workspace=ws, stream=st)
-        elif ws is not None or a.bf16:
+                              n_peers=peers.world, workspace=ws, nnz=e1 - e0, kernel=kern, reuse_sampled=reuse,
+                              stream=st)
+        elif ws is not None or a.bf16 or kern is not None:
             es.es_spmm_run_ex(rp_d, ci_d, va_d, B_d, a.s, strat_id, a.seed, red_id, F=F, C=C_d,
-                              row_begin=r0, row_end=r1, n_rows=n, nnz_base=e0, workspace=ws, stream=st)
+                              row_begin=r0, row_end=r1, n_rows=n, nnz_base=e0, workspace=ws, nnz=e1 - e0,
+                              kernel=kern, reuse_sampled=reuse, stream=st)
         else:
             es.es_spmm_run_rows(n, rp_d, e0, ci_d, va_d, B_d, a.s, strat_id, a.seed, red_id, r0, r1,
                                 F=F, C=C_d, stream=st)
@@ -338,18 +354,23 @@ def main():
     value = flops_all / (t_max / a.steps) / 1e9            # GFLOP/s
 
     # ---------------- roofline of the dominant kernel, this rank's launches
-    peak, peak_src = measured_peaks()
+    # Algorithmic bytes are SURVEY 8(d)'s per-run model, 8K + 8(N+1) + 4FK + 4FN, amortised over
+    # the launches that do the gather-FMA.  The binding ceiling is the L2 streaming rate when the
+    # gathered operand is L2-resident (the slab passes: one 256-B column slab of B at a time;
+    # the fused kernels: B itself <= 96 MB), else HBM (profiles/l2_peak.json, MEASURED_PEAKS.json).
+    hbm, hbm_src = measured_peaks()
+    l2, l2_src = l2_peak()
     bytes_rank = byte_model(K_rank, r1 - r0, F, b_elem)
-    avg_launch = t_rank / a.steps
-    step_achieved = bytes_rank / avg_launch / 1e9
+    avg_step = t_rank / a.steps
+    step_achieved = bytes_rank / avg_step / 1e9
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(prof):
+    key = f"{a.config}|F{F}|s{a.s}|{a.strategy}|{a.reduce}" + ("|slab" if ws is not None else "")
+    if os.path.exists(prof) and world == 1:
         try:
             with open(prof) as f:
                 tj = json.load(f)
-            key = f"{a.config}|F{F}|s{a.s}|{a.strategy}|{a.reduce}" + ("|slab" if ws is not None else "")
-            if key in tj and world == 1:
+            if key in tj:
                 traffic = tj[key]["dram_bytes_per_launch"]
         except Exception:
             traffic = None
@@ -357,52 +378,48 @@ def main():
                    "8K + 8(N+1) + 4FK + 4FN (sampled colind+val, rowptr, B gathers, C)")
     if ws is None:
         # one fused launch per step: the step IS the dominant kernel's launch
-        roofline = {"bound": "hbm", "achieved": round(step_achieved, 1), "peak": peak, "unit": "GB/s",
-                    "frac": round(step_achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
-                    "bytes_per_launch": bytes_rank, "bytes_model": bytes_model,
-                    "kernel": "es::spmm_cpasync<bf16>" if a.bf16 else es.es_spmm_plan(F, ldb, C_d.stride(0), B_d, C_d)}
+        resident = n * ldb * b_elem <= L2_RESIDENT_BYTES
+        t_launch = avg_step
+        n_launch = 1
+        kname = "es::spmm_cpasync<bf16>" if a.bf16 else es.es_spmm_plan(F, ldb, C_d.stride(0), B_d, C_d)
+        what = "one fused launch per step (sampling inside the kernel)"
     else:
-        # slab path: the dominant kernel is spmm_slab (one launch per 64-float feature slice,
-        # ncu: ~97 % of the step).  Its launches are timed alone here, live, on the launch stream
-        # with the same L2 flush: the same call with reuse_sampled=1 runs exactly the slice passes
-        # over the slots the timed steps sampled into the workspace.
+        # slab path: the dominant kernel is the slab pass (one launch per 256-B feature slice,
+        # ncu: ~97 % of the step).  Its launches are timed alone here, live, on the launch
+        # stream with the same L2 flush: the same call with reuse_sampled=1 runs exactly the
+        # slice passes over the slots the timed steps sampled into the workspace.
         wsl = 128 if a.bf16 else 64                        # elements per 256-B slab row
-        n_sl = (F + wsl - 1) // wsl
+        n_launch = (F + wsl - 1) // wsl
         pe0 = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
         pe1 = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
         for i in range(a.steps):
             if not a.no_flush:
                 flush.zero_()
             pe0[i].record(stream)
-            es.es_spmm_run_ex(rp_d, ci_d, va_d, B_d, a.s, strat_id, a.seed, red_id, F=F, C=C_d,
-                              row_begin=r0, row_end=r1, n_rows=n, nnz_base=e0, workspace=ws,
-                              reuse_sampled=True, stream=stream)
+            launch(stream, reuse=True)
             pe1[i].record(stream)
         torch.cuda.synchronize(dev)
-        t_passes = float(np.sum([x.elapsed_time(y) for x, y in zip(pe0, pe1)])) / 1e3 / a.steps   # s per step
-        nr_ = r1 - r0
-        # per launch (slice of width w): 8k (compact col+val) + 8(N+1) + b*wK + 4wN -- summed over slices
-        bytes_passes = n_sl * (8 * K_rank + 8 * (nr_ + 1)) + b_elem * F * K_rank + 4 * F * nr_
-        achieved = bytes_passes / t_passes / 1e9
-        roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                    "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
-                    "bytes_per_launch": int(bytes_passes / n_sl), "launch_ms": round(1e3 * t_passes / n_sl, 4),
-                    "launches_per_step": n_sl,
-                    "bytes_model": f"per slice launch (width w): 8K (compact sampled colind+val) + 8(N+1) + "
-                                   f"{b_elem}wK (B-slab gathers) + 4wN (C slice); summed over the slices = "
-                                   + bytes_model + " + (slices-1)(8K + 8(N+1))",
-                    "kernel": f"es::spmm_slab{'<bf16>' if a.bf16 else ''} (8 lanes x 2 pieces per slot, ring depth 4, "
-                              f"4-warp CTAs), one launch per {wsl}-element feature slice ({n_sl}/step); achieved = its "
-                              f"algorithmic bytes / its average launch time, timed live (reuse_sampled passes)",
-                    "limiter": "shared-memory/L1tex throughput (ncu: L1/TEX 79.8 % of peak, L2 hit 91.5 %, "
-                               "DRAM 8.5 %); every B byte crosses smem twice",
-                    # the slabs are L2-resident, so the L2 streaming rate is the other ceiling:
-                    # measured on this B200 by scripts/l2bw.cu (profiles/r01_l2bw_probe.jsonl)
-                    "l2_peak": L2_STREAM_GBS, "l2_frac": round(achieved / L2_STREAM_GBS, 4),
-                    "step": {"achieved": round(step_achieved, 1), "frac": round(step_achieved / peak, 4),
-                             "launches": launches_per_step,
-                             "what": "the whole step (count + scan + sample materialisation + the slice "
-                                     "passes): step algorithmic bytes / step time"}}
+        t_launch = float(np.sum([x.elapsed_time(y) for x, y in zip(pe0, pe1)])) / 1e3 / a.steps   # s per step
+        resident = n * 256 <= L2_RESIDENT_BYTES            # one slab of B
+        kname = (f"slab pass ({a.kernel if a.kernel != 'auto' else 'es::spmm_slab, shared-memory cp.async ring'}), "
+                 f"one launch per {wsl}-element feature slice ({n_launch}/step)")
+        what = ("the slab passes alone (reuse_sampled), timed live; the step adds count + scan + sample "
+                "materialisation")
+    achieved = bytes_rank / t_launch / 1e9
+    bound, peak, src = ("l2", l2, l2_src) if (resident and l2) else ("hbm", hbm, hbm_src)
+    roofline = {"bound": bound, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": src,
+                "bytes_per_launch": int(bytes_rank / n_launch), "launches_per_step": n_launch,
+                "launch_ms": round(1e3 * t_launch / n_launch, 4), "bytes_model": bytes_model + ", amortised over the "
+                f"{n_launch} launch(es) of the gather-FMA", "kernel": kname, "what": what,
+                "dram_frac": (round(traffic / (t_launch / n_launch) / 1e9 / hbm, 4) if traffic else None),
+                "dram_traffic_source": f"profiles/ncu_traffic.json[{key}] (ncu dram__bytes_read+write per launch)"
+                if traffic else None,
+                "hbm_gather_model": {"achieved": round(achieved, 1), "peak": hbm, "frac": round(achieved / hbm, 4),
+                                     "note": "the same algorithmic bytes against HBM: > 1 whenever the gathers "
+                                             "are served by L2 -- not a roofline fraction"},
+                "step": {"achieved": round(step_achieved, 1), "frac": round(step_achieved / peak, 4),
+                         "launches": launches_per_step}}
 
     # ---------------- compulsory bytes: every B row the sample touches read once --
     # the distinct sampled columns come from our own sampler (es_spmm_sample), outside the timing
@@ -483,14 +500,16 @@ def run_e2e(a, es, torch, dev, stream, rowptr, colind, val, B, r0, r1, e0, e1, F
     ci_h = torch.from_numpy(colind[e0:e1]).pin_memory()
     va_h = torch.from_numpy(val[e0:e1]).pin_memory()
     B_h = torch.from_numpy(B).pin_memory()
-    C_h = torch.empty((r1 - r0, F), dtype=torch.float32).pin_memory()
+    # C's host rows at B's pitch (ldc = ldb): one linear device->host copy per chunk
+    C_h = torch.empty((r1 - r0, ldb), dtype=torch.float32).pin_memory()
     need = es.es_spmm_host_workspace_bytes(r1 - r0, B.shape[0], e1 - e0, F, ldb, True)
     ws = torch.empty(need, dtype=torch.uint8, device=dev)
+    pipe = es.HostPipeline()                                 # copy streams + events, created once
     steps = max(3, min(a.steps, 10))
 
     def one():
         es.es_spmm_run_host(rp_h, ci_h, va_h, B_h, a.s, strat_id, a.seed, red_id, F=F, C=C_h,
-                            workspace=ws, row_base=r0, stream=stream)
+                            workspace=ws, row_base=r0, pipeline=pipe, stream=stream)
 
     for _ in range(2):
         one()
@@ -505,6 +524,7 @@ def run_e2e(a, es, torch, dev, stream, rowptr, colind, val, B, r0, r1, e0, e1, F
     ev1.record(stream)
     torch.cuda.synchronize(dev)
     t = ev0.elapsed_time(ev1) / 1e3
+    pipe.close()
     if world > 1:
         tt = torch.tensor([t], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -514,7 +534,8 @@ def run_e2e(a, es, torch, dev, stream, rowptr, colind, val, B, r0, r1, e0, e1, F
     return {"value": round(flops_all / (t / steps) / 1e9, 2), "unit": "GFLOP/s",
             "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h) * world,
             "ms_per_step": round(1e3 * t / steps, 3), "steps": steps,
-            "api": "es_spmm_run_host (pinned host buffers, chunked H2D/compute/D2H pipeline)"}
+            "api": "es_spmm_run_host_ex (pinned host buffers, chunked H2D/compute/D2H pipeline, the library's "
+                   "plan on the device copies, copy streams reused across calls)"}
 
 
 def main_reference(a, world, rank, strat_id, red_id):

@@ -20,7 +20,7 @@
  *   R6 seed != 0 rotates row i's FastRand sequence by mix64(seed + G*(i+1)) mod d_i
  *      (i = GLOBAL row id, G = 0x9E3779B97F4A7C15, mix64 = splitmix64 finalizer);
  *      seed == 0 is exactly Eq. 2;
- *   R8 fp32 storage, fp32 FMA accumulation (two interleaved partial sums), IEEE division.
+ *   R8 fp32 storage, fp32 FMA accumulation (32-slot chunk partials), IEEE division.
  *
  * Conventions (all entry points):
  *   * Pointers marked [dev] are device pointers; [host] are host pointers.  The caller
@@ -107,20 +107,65 @@ typedef struct {
     /* Slab path only: 1 = skip the sampling stage (a1-a3) and reuse the sampled slots already in
      * `workspace` from an earlier call on the same rows with the same s, strategy, seed and P'
      * (e.g. the layers of a GNN aggregating over one sampled graph, or timing the gather passes
-     * alone).  The caller guarantees that earlier call; nothing is checked. */
+     * alone).  Checked on the device against the signature the sampling call wrote into the
+     * workspace header (rows, s, strategy, seed, P', val presence): on a mismatch every output
+     * row of the call is written as NaN and es_spmm_workspace_status reports
+     * ES_WS_SIGNATURE_MISMATCH -- never a silently wrong C.  A call that cannot take the slab
+     * path (layout) with reuse_sampled = 1 returns ES_ERR_INVALID_VALUE. */
     int32_t reuse_sampled;
+    /* Stored entries of the call's rows, rowptr[row_end] - rowptr[row_begin] (a host value the
+     * caller knows; the library never reads device memory to size anything).  Sizes the slab
+     * path's capacity check: the workspace must hold min(nnz, n_rows * s) slots (0 = unknown:
+     * n_rows * s slots).  An undersized workspace returns ES_ERR_INVALID_VALUE.  If the value
+     * is wrong (smaller than the truth) the device backstop writes NaN rows and reports
+     * ES_WS_OVERFLOW instead of truncating.  (Read only when struct_size covers it.) */
+    int64_t nnz;
+    /* Kernel selection for A/B measurement and the parity tests' per-family coverage:
+     * ES_KERNEL_AUTO (0) = the library's measured plan, else force a family where
+     * it applies (ES_ERR_UNSUPPORTED where it cannot run the layout).  tune[] = family knobs,
+     * 0 = the default: tune[0] ring depth, tune[1] lanes per slot (slab) / rows per warp (TMA),
+     * tune[2] warps per CTA, tune[3] variant bits.  No result changes beyond each family's
+     * documented summation order.  (Read only when struct_size covers them.) */
+    int32_t kernel;
+    int32_t tune[4];
 } es_spmm_options_t;
 
+enum {
+    ES_KERNEL_AUTO = 0,
+    ES_KERNEL_FUSED = 1,        /* the plan's one-launch fused kernel; never the slab path       */
+    ES_KERNEL_WARP = 2,         /* LDG warp-per-row gathers                                       */
+    ES_KERNEL_TMA = 3,          /* cp.async.bulk ring of whole B rows                             */
+    ES_KERNEL_CPASYNC = 4,      /* per-lane cp.async ring, one slot per step                      */
+    ES_KERNEL_CPASYNC_HW = 5,   /* per-lane cp.async ring, two slots per step                     */
+    ES_KERNEL_SLAB = 6,         /* feature-sliced path with the plan's slab kernel (workspace)    */
+    ES_KERNEL_SLAB_SMEM = 7,    /* feature-sliced path, cp.async shared-memory ring               */
+    ES_KERNEL_SLAB_LDG = 8,     /* feature-sliced path, register-direct 256-bit gathers           */
+    ES_KERNEL_SLAB_TMA = 9      /* feature-sliced path, TMA tile::gather4 into a shared-memory ring */
+};
+
+/* Status word of a slab workspace (written by the device; reading it synchronises `stream`).
+ * ES_WS_OK, or the OR of: ES_WS_OVERFLOW (the sampled slots did not fit: the affected rows of
+ * C were written as NaN), ES_WS_SIGNATURE_MISMATCH (reuse_sampled over slots of a different
+ * sampling: the call's rows of C were written as NaN).  reset = 1 clears it afterwards. */
+enum { ES_WS_OK = 0, ES_WS_OVERFLOW = 1, ES_WS_SIGNATURE_MISMATCH = 2 };
+es_status_t es_spmm_workspace_status(void* workspace /*[dev]*/, int64_t workspace_bytes, int32_t reset,
+                                     int32_t* status_out /*[host]*/, void* stream);
+
 /* Bytes of workspace es_spmm_run_ex needs to take the slab path for rows holding `nnz` stored
- * entries (nnz >= rowptr[row_end] - rowptr[row_begin] is a precondition like the CSR
- * invariants; the kernels never read or write past the workspace), sampling cap s, feature
- * width F, and B of n_cols rows with pitch ldb.  > 0 when the measured plan prefers the slab
- * path: F >= 128, a 64-float slab of B (n_cols x 256 B) fits L2, and rows sample enough slots
- * on average: min(s, nnz / n_rows) >= 128 for F > 128, >= 192 for F <= 128.  0 otherwise: pass
- * no workspace then.
- * has_val = 0 when val will be NULL (no slot values are stored). */
+ * entries (pass the same nnz in es_spmm_options_t.nnz; the kernels never read or write past
+ * the workspace, and an undersized one is an error, never a truncation), sampling cap s,
+ * feature width F, and B of n_cols rows with pitch ldb.  > 0 when the measured plan prefers the
+ * slab path: F >= 128, ldb % 4 == 0, a 64-float slab of B (n_cols x 256 B) fits L2, and rows
+ * sample enough slots on average.  0 otherwise: pass no workspace then.
+ * has_val = 0 when val will be NULL (no slot values are stored); a workspace sized with
+ * has_val = 0 is too small for a call with val (ES_ERR_INVALID_VALUE). */
 int64_t es_spmm_workspace_bytes(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t F, int64_t ldb,
                                 int32_t s, int32_t has_val);
+/* Same, honouring opt->kernel: with a slab kernel forced (ES_KERNEL_SLAB*), > 0 wherever the slab
+ * path can run at all (F > 16, ldb % 4 == 0, the slab fits L2), not only where it is measured
+ * faster.  opt NULL = es_spmm_workspace_bytes. */
+int64_t es_spmm_workspace_bytes_ex(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t F, int64_t ldb,
+                                   int32_t s, int32_t has_val, const es_spmm_options_t* opt);
 
 /* Edge sampling materialised (stage 1 of Alg. 1; the paper's "pre-sampled graph",
  * §5.6).
@@ -216,11 +261,15 @@ es_status_t es_spmm_backward_ex(int64_t n_rows, int64_t n_cols,
                                 const es_spmm_options_t* opt, void* stream);
 
 /* End-to-end variant with HOST inputs and output (the call a user with host data makes):
- * copies rowptr/colind/val/B host->device, runs the fused kernel and copies C back,
- * rowptr entries are absolute offsets with colind[0] holding nonzero rowptr[0];
- * pipelined over row chunks on `stream` plus one internal copy stream.  Host buffers
- * should be pinned (cudaHostAlloc/cudaHostRegister) for asynchronous copies.
- *   workspace [dev] of es_spmm_host_workspace_bytes(...) bytes is owned by the caller.
+ * copies rowptr/colind/val/B host->device, runs the library's plan on the device copies (the
+ * slab path where es_spmm_workspace_bytes would ask for it, else the fused kernel) and copies C
+ * back; rowptr entries are absolute offsets with colind[0] holding nonzero rowptr[0].  Pipelined
+ * over up to 8 row chunks: B first, then each chunk's colind/val on an internal copy stream while
+ * earlier chunks compute on `stream` and their C rows go back on a second copy stream (one linear
+ * copy per chunk when ldc == ldb, the device pitch).  Host buffers should be pinned
+ * (cudaHostAlloc/cudaHostRegister) for asynchronous copies.
+ *   workspace [dev] of es_spmm_host_workspace_bytes(...) bytes is owned by the caller (device
+ *   copies of the inputs, C, and room for the slab path's sampled slots).
  * Synchronises `stream` before returning (C is valid on return). */
 int64_t es_spmm_host_workspace_bytes(int64_t n_rows, int64_t n_cols, int64_t nnz,
                                      int64_t F, int64_t ldb, int32_t has_val);
@@ -232,6 +281,25 @@ es_status_t es_spmm_run_host(int64_t n_rows, int64_t n_cols,
                              int64_t row_base /* global id of row 0 (seeded FastRand) */,
                              float* C /*[host]*/, int64_t ldc,
                              void* workspace /*[dev]*/, int64_t workspace_bytes, void* stream);
+
+/* The copy streams and events of the host pipeline, created once and reused across calls
+ * (es_spmm_run_host creates and destroys its own per call).  Owned by the caller; one call in
+ * flight per pipeline. */
+typedef struct es_host_pipeline es_host_pipeline_t;
+es_status_t es_host_pipeline_create(es_host_pipeline_t** out);
+void es_host_pipeline_destroy(es_host_pipeline_t* pipe);
+
+/* es_spmm_run_host with options (prime, mean_divisor, kernel/tune; workspace, peers, bf16 and
+ * reuse_sampled must be unset: ES_ERR_INVALID_VALUE) and a caller-owned pipeline (NULL = a
+ * temporary one). */
+es_status_t es_spmm_run_host_ex(int64_t n_rows, int64_t n_cols,
+                                const int64_t* rowptr /*[host]*/, const int32_t* colind /*[host]*/,
+                                const float* val /*[host] or NULL*/,
+                                const float* B /*[host]*/, int64_t F, int64_t ldb,
+                                int32_t s, int32_t strategy, uint64_t seed, int32_t reduce,
+                                int64_t row_base, float* C /*[host]*/, int64_t ldc,
+                                void* workspace /*[dev]*/, int64_t workspace_bytes,
+                                const es_spmm_options_t* opt, es_host_pipeline_t* pipe, void* stream);
 
 /* Peer-memory helpers for the fused all-gather (one process per GPU of a node).
  *   es_ipc_alloc/free: a dedicated cudaMalloc allocation (so an IPC handle maps exactly it).

@@ -18,6 +18,12 @@ ES_BUCKET, ES_FASTRAND = 1, 2
 ES_REDUCE_SUM, ES_REDUCE_MEAN = 0, 1
 ES_MEAN_BY_SAMPLED, ES_MEAN_BY_DEGREE = 0, 1
 ES_DTYPE_F32, ES_DTYPE_BF16 = 0, 1
+(ES_KERNEL_AUTO, ES_KERNEL_FUSED, ES_KERNEL_WARP, ES_KERNEL_TMA, ES_KERNEL_CPASYNC, ES_KERNEL_CPASYNC_HW,
+ ES_KERNEL_SLAB, ES_KERNEL_SLAB_SMEM, ES_KERNEL_SLAB_LDG, ES_KERNEL_SLAB_TMA) = range(10)
+KERNELS = {"auto": ES_KERNEL_AUTO, "fused": ES_KERNEL_FUSED, "warp": ES_KERNEL_WARP, "tma": ES_KERNEL_TMA,
+           "cpasync": ES_KERNEL_CPASYNC, "halfwarp": ES_KERNEL_CPASYNC_HW, "slab": ES_KERNEL_SLAB,
+           "slab_smem": ES_KERNEL_SLAB_SMEM, "slab_ldg": ES_KERNEL_SLAB_LDG, "slab_tma": ES_KERNEL_SLAB_TMA}
+ES_WS_OK, ES_WS_OVERFLOW, ES_WS_SIGNATURE_MISMATCH = 0, 1, 2
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libesspmm.so")
@@ -25,7 +31,8 @@ EXPORTS = ("es_spmm_sample", "es_spmm_run", "es_spmm_run_rows", "es_spmm_backwar
            "es_spmm_run_ex", "es_spmm_sample_ex", "es_spmm_backward_ex", "es_spmm_host_workspace_bytes",
            "es_ipc_handle_bytes", "es_ipc_alloc", "es_ipc_free", "es_ipc_export", "es_ipc_import", "es_ipc_close",
            "es_spmm_run_host", "es_partition_rows", "es_spmm_plan", "es_launch_count", "es_spmm_workspace_bytes",
-           "es_status_string")
+           "es_spmm_workspace_bytes_ex", "es_spmm_workspace_status", "es_status_string",
+           "es_host_pipeline_create", "es_host_pipeline_destroy", "es_spmm_run_host_ex")
 
 _lib = None
 
@@ -35,20 +42,63 @@ class EsError(RuntimeError):
 
 
 class EsOptions(ctypes.Structure):
-    """es_spmm_options_t (include/es_spmm.h): NEXT-4 sensitivity variants."""
+    """es_spmm_options_t (include/es_spmm.h)."""
     _fields_ = [("struct_size", ctypes.c_int32), ("prime", ctypes.c_int32),
                 ("mean_divisor", ctypes.c_int32), ("b_dtype", ctypes.c_int32),
                 ("c_peers", ctypes.c_void_p), ("n_peers", ctypes.c_int32),
                 ("deterministic", ctypes.c_int32), ("workspace", ctypes.c_void_p),
-                ("workspace_bytes", ctypes.c_int64), ("reuse_sampled", ctypes.c_int32)]
+                ("workspace_bytes", ctypes.c_int64), ("reuse_sampled", ctypes.c_int32),
+                ("nnz", ctypes.c_int64), ("kernel", ctypes.c_int32), ("tune", ctypes.c_int32 * 4)]
 
     @classmethod
     def make(cls, prime: int = 0, mean_by_degree: bool = False, bf16: bool = False, c_peers=None,
-             n_peers: int = 0, deterministic: bool = False, workspace=None, reuse_sampled: bool = False):
+             n_peers: int = 0, deterministic: bool = False, workspace=None, reuse_sampled: bool = False,
+             nnz: int = 0, kernel=None, tune=None):
         ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
+        kern, tun = _forced(kernel, tune)
         return cls(ctypes.sizeof(cls), prime, ES_MEAN_BY_DEGREE if mean_by_degree else ES_MEAN_BY_SAMPLED,
                    ES_DTYPE_BF16 if bf16 else ES_DTYPE_F32, _ptr(c_peers), n_peers, int(deterministic),
-                   _ptr(workspace), ws_bytes, int(reuse_sampled))
+                   _ptr(workspace), ws_bytes, int(reuse_sampled), int(nnz), kern,
+                   (ctypes.c_int32 * 4)(*[int(x) for x in tun]))
+
+
+# Kernel selection for A/B measurement and the tests' per-family coverage (es_spmm_options_t.kernel
+# and tune[]): `with kernel_override("slab_ldg", stages=8): ...` applies to every call that takes
+# options in the block (argument marshalling only; the library decides what runs).
+_OVERRIDE = {"kernel": ES_KERNEL_AUTO, "tune": (0, 0, 0, 0)}
+
+
+def _kernel_id(kernel) -> int:
+    if kernel is None:
+        return ES_KERNEL_AUTO
+    return KERNELS[kernel] if isinstance(kernel, str) else int(kernel)
+
+
+def _forced(kernel, tune):
+    k = _kernel_id(kernel) if kernel is not None else _OVERRIDE["kernel"]
+    t = tuple(tune) if tune is not None else _OVERRIDE["tune"]
+    return k, (list(t) + [0, 0, 0, 0])[:4]
+
+
+class kernel_override:
+    """Context manager: force a kernel family / tuning knobs for the calls inside the block."""
+
+    def __init__(self, kernel="auto", stages: int = 0, width: int = 0, cta_warps: int = 0, variant: int = 0):
+        self.new = {"kernel": _kernel_id(kernel), "tune": (stages, width, cta_warps, variant)}
+
+    def __enter__(self):
+        self.old = dict(_OVERRIDE)
+        _OVERRIDE.update(self.new)
+        return self
+
+    def __exit__(self, *exc):
+        _OVERRIDE.clear()
+        _OVERRIDE.update(self.old)
+        return False
+
+
+def overridden() -> bool:
+    return _OVERRIDE["kernel"] != ES_KERNEL_AUTO or any(_OVERRIDE["tune"])
 
 
 def load_library(path: str = LIB_PATH):
@@ -101,8 +151,19 @@ def load_library(path: str = LIB_PATH):
     lib.es_spmm_run_host.restype = st
     lib.es_spmm_run_host.argtypes = [i64, i64, vp, vp, vp, vp, i64, i64, i32, i32, u64, i32, i64, vp,
                                      i64, vp, i64, vp]
+    lib.es_host_pipeline_create.restype = st
+    lib.es_host_pipeline_create.argtypes = [ctypes.POINTER(ctypes.c_void_p)]
+    lib.es_host_pipeline_destroy.restype = None
+    lib.es_host_pipeline_destroy.argtypes = [vp]
+    lib.es_spmm_run_host_ex.restype = st
+    lib.es_spmm_run_host_ex.argtypes = [i64, i64, vp, vp, vp, vp, i64, i64, i32, i32, u64, i32, i64, vp,
+                                        i64, vp, i64, op, vp, vp]
     lib.es_spmm_workspace_bytes.restype = i64
     lib.es_spmm_workspace_bytes.argtypes = [i64, i64, i64, i64, i64, i32, i32]
+    lib.es_spmm_workspace_bytes_ex.restype = i64
+    lib.es_spmm_workspace_bytes_ex.argtypes = [i64, i64, i64, i64, i64, i32, i32, op]
+    lib.es_spmm_workspace_status.restype = st
+    lib.es_spmm_workspace_status.argtypes = [vp, i64, i32, ctypes.POINTER(ctypes.c_int32), vp]
     lib.es_partition_rows.restype = st
     lib.es_partition_rows.argtypes = [vp, i64, i32, i64, i32, vp]
     lib.es_spmm_plan.restype = st
@@ -127,6 +188,14 @@ def _stream(stream=None):
     import torch
     s = stream if stream is not None else torch.cuda.current_stream()
     return ctypes.c_void_p(s.cuda_stream)
+
+
+def _check_out(C, n: int, F: int, name: str):
+    """A caller-supplied output: a row-major CUDA fp32 matrix of >= n rows and >= F columns."""
+    import torch
+    if (not isinstance(C, torch.Tensor) or not C.is_cuda or C.dtype != torch.float32 or C.dim() != 2
+            or C.stride(1) != 1 or C.shape[0] < n or C.shape[1] < F):
+        raise EsError(f"{name} must be a row-major fp32 CUDA matrix of at least ({n}, {F})")
 
 
 def _dev(t, dtype, name):
@@ -197,8 +266,9 @@ def es_spmm_run(rowptr, colind, val, B, s: int, strategy: int, seed: int = 0,
     F = ldb if F is None else F
     if C is None:
         C = torch.empty((n, F), dtype=torch.float32, device=B.device)
-    if C.dim() != 2 or C.stride(1) != 1 or C.shape[0] < n or C.shape[1] < F:
-        raise EsError("C must be a row-major (n_rows, >=F) CUDA tensor")
+    _check_out(C, n, F, "C")
+    if overridden():                 # a forced kernel family (tests / A-B): the options entry point
+        return es_spmm_run_ex(rowptr, colind, val, B, s, strategy, seed, reduce, F=F, C=C, stream=stream)
     _check(load_library().es_spmm_run(n, B.shape[0], _ptr(rowptr), _ptr(colind), _ptr(val), _ptr(B),
                                       F, ldb, s, strategy, seed & (2**64 - 1), reduce, _ptr(C),
                                       C.stride(0), _stream(stream)), "es_spmm_run")
@@ -231,13 +301,17 @@ def es_spmm_run_ex(rowptr, colind, val, B, s: int, strategy: int, seed: int = 0,
                    reduce: int = ES_REDUCE_SUM, F: int | None = None, C=None, prime: int = 0,
                    mean_by_degree: bool = False, row_begin: int = 0, row_end: int | None = None,
                    n_rows: int | None = None, nnz_base: int = 0, c_peers=None, n_peers: int = 0,
-                   workspace=None, reuse_sampled: bool = False, stream=None):
+                   workspace=None, reuse_sampled: bool = False, nnz: int | None = None, kernel=None, tune=None,
+                   stream=None):
     """es_spmm_run_rows with the options: P' override, MEAN by original degree, bf16 storage of
     B (pass a torch.bfloat16 B; accumulation stays fp32) -- NEXT-4 -- the fused all-gather
     (c_peers: int64 CUDA tensor of n_peers full-C base pointers; C = this rank's full C) --
     NEXT-1, see paper_2104_10716_b200.dist.PeerBuffers -- and the slab path's workspace (a
     CUDA uint8 tensor of es_spmm_workspace_bytes(...) bytes, or None; reuse_sampled skips the
-    sampling stage and reuses the slots a previous call left in it)."""
+    sampling stage and reuses the slots a previous call left in it).  nnz = stored entries of
+    the rows (sizes the workspace check; defaults to colind.numel() when the CSR is not a
+    slice, i.e. nnz_base == 0 and the call covers all of rowptr); kernel/tune force a kernel
+    family (A/B measurement; default: the library's plan)."""
     import torch
     _dev(rowptr, torch.int64, "rowptr")
     _dev(colind, torch.int32, "colind")
@@ -254,8 +328,12 @@ def es_spmm_run_ex(rowptr, colind, val, B, s: int, strategy: int, seed: int = 0,
         n_rows = row_end
     if C is None:
         C = torch.empty((row_end - row_begin, F), dtype=torch.float32, device=B.device)
+    rows_out = row_end - row_begin if n_peers == 0 else n_rows
+    _check_out(C, rows_out, F, "C")
+    if nnz is None:
+        nnz = colind.numel() if (nnz_base == 0 and row_end - row_begin == rowptr.numel() - 1) else 0
     opt = EsOptions.make(prime, mean_by_degree, B.dtype == torch.bfloat16, c_peers, n_peers,
-                         workspace=workspace, reuse_sampled=reuse_sampled)
+                         workspace=workspace, reuse_sampled=reuse_sampled, nnz=nnz, kernel=kernel, tune=tune)
     _check(load_library().es_spmm_run_ex(n_rows, B.shape[0], _ptr(rowptr), nnz_base, _ptr(colind), _ptr(val),
                                          _ptr(B), F, ldb, s, strategy, seed & (2**64 - 1), reduce, _ptr(C),
                                          C.stride(0), row_begin, row_end, ctypes.byref(opt), _stream(stream)),
@@ -264,17 +342,29 @@ def es_spmm_run_ex(rowptr, colind, val, B, s: int, strategy: int, seed: int = 0,
 
 
 def es_spmm_workspace_bytes(n_rows: int, n_cols: int, nnz: int, F: int, ldb: int, s: int,
-                            has_val: bool = True) -> int:
-    """Workspace bytes for es_spmm_run_ex's slab path (0: the shape does not take it)."""
-    return int(load_library().es_spmm_workspace_bytes(n_rows, n_cols, nnz, F, ldb, s, int(bool(has_val))))
+                            has_val: bool = True, kernel=None) -> int:
+    """Workspace bytes for es_spmm_run_ex's slab path (0: the shape does not take it).  With a
+    slab kernel forced (argument or kernel_override), > 0 wherever the slab path can run."""
+    opt = EsOptions.make(kernel=kernel)
+    return int(load_library().es_spmm_workspace_bytes_ex(n_rows, n_cols, nnz, F, ldb, s, int(bool(has_val)),
+                                                         ctypes.byref(opt)))
 
 
 def es_spmm_workspace(n_rows: int, n_cols: int, nnz: int, F: int, ldb: int, s: int, has_val: bool = True,
-                      device=None):
+                      device=None, kernel=None):
     """A workspace tensor for es_spmm_run_ex (None when the slab path is not taken)."""
     import torch
-    nb = es_spmm_workspace_bytes(n_rows, n_cols, nnz, F, ldb, s, has_val)
-    return torch.empty(nb, dtype=torch.uint8, device=device) if nb > 0 else None
+    nb = es_spmm_workspace_bytes(n_rows, n_cols, nnz, F, ldb, s, has_val, kernel=kernel)
+    return torch.zeros(nb, dtype=torch.uint8, device=device) if nb > 0 else None
+
+
+def es_spmm_workspace_status(workspace, reset: bool = False, stream=None) -> int:
+    """The workspace's device status word (ES_WS_OK or ES_WS_OVERFLOW | ES_WS_SIGNATURE_MISMATCH);
+    synchronises the stream."""
+    v = ctypes.c_int32(0)
+    _check(load_library().es_spmm_workspace_status(_ptr(workspace), workspace.numel(), int(reset), ctypes.byref(v),
+                                                   _stream(stream)), "es_spmm_workspace_status")
+    return int(v.value)
 
 
 def es_spmm_sample_ex(rowptr, colind, val, s: int, strategy: int, seed: int = 0, row_base: int = 0,
@@ -313,12 +403,17 @@ def es_spmm_backward_ex(rowptr, colind, val, dC, n_cols: int, s: int, strategy: 
     es_spmm_run_ex) selects the feature-sliced backward, reuse_sampled=True reuses the slots the
     forward left in it."""
     import torch
+    _dev(rowptr, torch.int64, "rowptr")
+    _dev(colind, torch.int32, "colind")
+    _dev(val, torch.float32, "val")
+    n = rowptr.numel() - 1
     F = dC.shape[1] if F is None else F
+    _check_out(dC, n, F, "dC")
     if dB is None:
         dB = torch.zeros((n_cols, F), dtype=torch.float32, device=dC.device)
-    n = rowptr.numel() - 1
+    _check_out(dB, n_cols, F, "dB")
     opt = EsOptions.make(prime, mean_by_degree, deterministic=deterministic, workspace=workspace,
-                         reuse_sampled=reuse_sampled)
+                         reuse_sampled=reuse_sampled, nnz=colind.numel())
     _check(load_library().es_spmm_backward_ex(n, n_cols, _ptr(rowptr), 0, _ptr(colind), _ptr(val), _ptr(dC), F,
                                               dC.stride(0), s, strategy, seed & (2**64 - 1), reduce, _ptr(dB),
                                               dB.stride(0), 0, n, ctypes.byref(opt), _stream(stream)),
@@ -357,10 +452,32 @@ def es_spmm_host_workspace_bytes(n_rows, n_cols, nnz, F, ldb, has_val) -> int:
     return int(load_library().es_spmm_host_workspace_bytes(n_rows, n_cols, nnz, F, ldb, int(has_val)))
 
 
+class HostPipeline:
+    """es_host_pipeline_t: the host pipeline's copy streams and events, created once and reused
+    across es_spmm_run_host calls (close() or garbage collection destroys them)."""
+
+    def __init__(self):
+        p = ctypes.c_void_p()
+        _check(load_library().es_host_pipeline_create(ctypes.byref(p)), "es_host_pipeline_create")
+        self.ptr = p
+
+    def close(self):
+        if self.ptr is not None and self.ptr.value:
+            load_library().es_host_pipeline_destroy(self.ptr)
+        self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def es_spmm_run_host(rowptr, colind, val, B, s: int, strategy: int, seed: int = 0,
                      reduce: int = ES_REDUCE_SUM, F: int | None = None, C=None, workspace=None,
-                     row_base: int = 0, stream=None):
-    """End-to-end call on HOST (ideally pinned) torch/numpy buffers; returns host C."""
+                     row_base: int = 0, pipeline: HostPipeline | None = None, kernel=None, stream=None):
+    """End-to-end call on HOST (ideally pinned) torch/numpy buffers; returns host C (rows of C's
+    own pitch: pass C with C.stride(0) == B.shape[1] for one linear copy back per chunk)."""
     import torch
 
     def host(t, dtype):
@@ -379,14 +496,18 @@ def es_spmm_run_host(rowptr, colind, val, B, s: int, strategy: int, seed: int = 
     F = ldb if F is None else F
     if C is None:
         C = torch.empty((n, F), dtype=torch.float32, pin_memory=True)
+    if C.is_cuda or C.dtype != torch.float32 or C.dim() != 2 or C.stride(1) != 1 or C.shape[0] < n or C.shape[1] < F:
+        raise EsError("C must be a row-major fp32 host matrix of at least (n_rows, F)")
     nnz = int(rowptr[-1]) - int(rowptr[0]) if n >= 0 else 0
     need = es_spmm_host_workspace_bytes(n, B.shape[0], nnz, F, ldb, val is not None)
     if workspace is None or workspace.numel() < need:
         workspace = torch.empty(need, dtype=torch.uint8, device="cuda")
-    _check(load_library().es_spmm_run_host(n, B.shape[0], _ptr(rowptr), _ptr(colind), _ptr(val),
-                                           _ptr(B), F, ldb, s, strategy, seed & (2**64 - 1), reduce,
-                                           row_base, _ptr(C), C.stride(0), _ptr(workspace), workspace.numel(),
-                                           _stream(stream)), "es_spmm_run_host")
+    opt = EsOptions.make(kernel=kernel)
+    _check(load_library().es_spmm_run_host_ex(n, B.shape[0], _ptr(rowptr), _ptr(colind), _ptr(val),
+                                              _ptr(B), F, ldb, s, strategy, seed & (2**64 - 1), reduce,
+                                              row_base, _ptr(C), C.stride(0), _ptr(workspace), workspace.numel(),
+                                              ctypes.byref(opt), None if pipeline is None else pipeline.ptr,
+                                              _stream(stream)), "es_spmm_run_host_ex")
     return C
 
 

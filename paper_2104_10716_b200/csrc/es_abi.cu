@@ -9,6 +9,8 @@
 #include <cstring>
 #include <vector>
 
+#include <new>
+
 #include <cuda_runtime.h>
 
 #include "es_internal.h"
@@ -38,83 +40,94 @@ struct Opts {
     void* workspace = nullptr;
     int64_t workspace_bytes = 0;
     int32_t reuse_sampled = 0;
+    int64_t nnz = 0;             // stored entries of the call's rows (0 = unknown)
+    es::Tune tune;
 };
+
+#define ES_COVERS(o, field) ((o)->struct_size >= (int32_t)(offsetof(es_spmm_options_t, field) + sizeof((o)->field)))
 
 es_status_t read_opts(const es_spmm_options_t* o, Opts* out) {
     *out = Opts{};
     if (!o) return ES_OK;
-    if (o->struct_size < (int32_t)offsetof(es_spmm_options_t, c_peers)) return ES_ERR_INVALID_VALUE;
+    if (!ES_COVERS(o, b_dtype)) return ES_ERR_INVALID_VALUE;
     if (o->prime < 0) return ES_ERR_INVALID_VALUE;
     if (o->mean_divisor != ES_MEAN_BY_SAMPLED && o->mean_divisor != ES_MEAN_BY_DEGREE) return ES_ERR_INVALID_VALUE;
     if (o->b_dtype != ES_DTYPE_F32 && o->b_dtype != ES_DTYPE_BF16) return ES_ERR_INVALID_VALUE;
     out->prime = o->prime == 0 ? 577u : (uint32_t)o->prime;
     out->mean_by_degree = o->mean_divisor == ES_MEAN_BY_DEGREE;
     out->bf16 = o->b_dtype == ES_DTYPE_BF16;
-    if (o->struct_size >= (int32_t)offsetof(es_spmm_options_t, deterministic)) {
+    if (ES_COVERS(o, n_peers)) {
         if (o->n_peers < 0 || (o->n_peers > 0 && !o->c_peers)) return ES_ERR_INVALID_VALUE;
         out->c_peers = o->c_peers;
         out->n_peers = o->n_peers;
     }
-    if (o->struct_size >= (int32_t)offsetof(es_spmm_options_t, workspace)) out->deterministic = o->deterministic != 0;
-    if (o->struct_size >= (int32_t)offsetof(es_spmm_options_t, reuse_sampled)) {
+    if (ES_COVERS(o, deterministic)) out->deterministic = o->deterministic != 0;
+    if (ES_COVERS(o, workspace_bytes)) {
         if (o->workspace_bytes < 0 || (o->workspace_bytes > 0 && !o->workspace)) return ES_ERR_INVALID_VALUE;
-        out->workspace = o->workspace;
+        out->workspace = o->workspace_bytes > 0 ? o->workspace : nullptr;
         out->workspace_bytes = o->workspace_bytes;
     }
-    if (o->struct_size >= (int32_t)sizeof(es_spmm_options_t)) out->reuse_sampled = o->reuse_sampled != 0;
+    if (ES_COVERS(o, reuse_sampled)) out->reuse_sampled = o->reuse_sampled != 0;
+    if (ES_COVERS(o, nnz)) {
+        if (o->nnz < 0) return ES_ERR_INVALID_VALUE;
+        out->nnz = o->nnz;
+    }
+    if (ES_COVERS(o, tune)) {
+        if (o->kernel < ES_KERNEL_AUTO || o->kernel > ES_KERNEL_SLAB_TMA) return ES_ERR_INVALID_VALUE;
+        out->tune.kernel = o->kernel;
+        out->tune.stages = o->tune[0];
+        out->tune.width = o->tune[1];
+        out->tune.cta_warps = o->tune[2];
+        out->tune.variant = o->tune[3];
+    }
     return ES_OK;
 }
 
 // ---- slab path (es_slab.cu): when, and the workspace layout
 constexpr int64_t kSlabF = 64;                       // floats per feature slice (256-B slab rows)
+constexpr int64_t kSlabMaxBytes = (int64_t)80 << 20; // largest slab kept L2-resident (126 MB L2)
 
-int64_t env_i64(const char* name, int64_t dflt) {
-    const char* e = getenv(name);
-    return e ? atoll(e) : dflt;
-}
-
-// Run time (a workspace was passed): the slab path runs whenever it can -- F > 16 and a
-// 64-float slab of B (n_cols x 256 B) fits L2.  ES_SPMM_SLAB=0 disables, =1 forces.
+// A workspace was passed: the slab path runs whenever the layout allows -- F > 16, B rows 16-B
+// aligned, and a 64-float slab of B (n_cols x 256 B) fits L2.
 bool slab_feasible(int64_t n_cols, int64_t F) {
-    const int64_t force = env_i64("ES_SPMM_SLAB", -1);
-    if (force == 0 || F <= kSlabF / 4) return false;
-    if (force == 1) return true;
-    return n_cols * kSlabF * 4 <= (env_i64("ES_SPMM_SLAB_MAX_SLAB_MB", 80) << 20);
+    return F > kSlabF / 4 && n_cols * kSlabF * 4 <= kSlabMaxBytes;
 }
 
-// es_spmm_workspace_bytes's choice (measured, profiles/r01.md "Slab path" and the s-sweep in
-// BASELINE.md): feasible, F >= 128, and rows that sample enough slots on average -- the bound
-// used is min(s, nnz / n_rows) >= 128 for F > 128 (several slices: Reddit-shaped F=602 s=128
-// 5.8 -> 4.95 ms, s=256 9.8 -> 7.8 ms) and >= 192 for F <= 128 (two slices; at s=128 the fused
-// two-slot ring is 1-6 % faster, at s=192 the slab path wins 1.50 -> 1.39 ms).  Below that each
-// slice pass's per-row start-up outweighs the L2-resident gathers (Reddit F=602 s=16: 2.0 vs
-// 4.5 TFLOP/s), and short rows (Arxiv-shaped, mean degree 14) keep the fused kernel.
-bool slab_wanted(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t F, int64_t s) {
-    if (!slab_feasible(n_cols, F)) return false;
-    if (env_i64("ES_SPMM_SLAB", -1) == 1) return true;
+// es_spmm_workspace_bytes's choice (measured, DESIGN.md §5 and profiles/r02.md): feasible,
+// F >= 128, a 16-B row pitch, and rows that sample enough slots on average: min(s, nnz / n_rows)
+// >= 128 for F > 128 (several slices) and >= 192 for F <= 128 (two slices).  Below that each
+// slice pass's per-row start-up outweighs the L2-resident gathers and short rows keep the fused
+// kernels.
+bool slab_wanted(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t F, int64_t ldb, int64_t s) {
+    if (!slab_feasible(n_cols, F) || ldb % 4 != 0 || F < 128) return false;
     const int64_t mean_deg = n_rows > 0 ? nnz / n_rows : 0;
     const int64_t k_est = s < mean_deg ? s : mean_deg;
-    const int64_t min_k = env_i64("ES_SPMM_SLAB_MIN_K", F > 128 ? 128 : 192);
-    return F >= env_i64("ES_SPMM_SLAB_MIN_F", 128) && k_est >= min_k;
+    return k_est >= (F > 128 ? 128 : 192);
 }
 
 int64_t slab_align(int64_t x) { return (x + 255) & ~(int64_t)255; }
 
+// [header 256 B][s_rowptr (n+1) x 8][scan temp][s_colind cap x 4][s_val cap x 4]
 struct SlabLayout {
-    int64_t off_rowptr, off_temp, temp_bytes, off_col, off_val, bytes_fixed;
+    int64_t off_rowptr, off_temp, temp_bytes, off_col, bytes_fixed;
 };
 SlabLayout slab_layout(int64_t n) {
     SlabLayout L{};
-    L.off_rowptr = 0;
-    L.off_temp = slab_align(8 * (n + 1));
+    L.off_rowptr = 256;
+    L.off_temp = slab_align(L.off_rowptr + 8 * (n + 1));
     L.temp_bytes = (int64_t)es::slab_scan_temp_bytes(n);
     L.off_col = slab_align(L.off_temp + L.temp_bytes);
     L.bytes_fixed = L.off_col;
     return L;
 }
+int64_t slab_bytes(int64_t n, int64_t cap, bool has_val) {
+    const int64_t c = cap > 0 ? cap : 1;
+    return slab_layout(n).bytes_fixed + slab_align(4 * c) + (has_val ? slab_align(4 * c) : 0);
+}
 
-// The workspace's sampled-slot arrays (es_spmm_sample layout); false if it holds no slot.
+// The workspace's sampled-slot arrays (es_spmm_sample layout).
 struct SlabSlots {
+    es::WsHeader* hdr;
     int64_t* s_rowptr;
     int32_t* s_col;
     float* s_val;
@@ -122,12 +135,17 @@ struct SlabSlots {
     void* temp;
     size_t temp_bytes;
 };
-bool slab_slots(const Opts& o, int64_t n, bool has_val, SlabSlots* out) {
+// false: the workspace cannot hold the slots the call may sample -- min(nnz, n*s) when the
+// caller stated nnz, else n*s (an undersized workspace is an error, never a truncation)
+bool slab_slots(const Opts& o, int64_t n, int32_t s, bool has_val, SlabSlots* out) {
     const SlabLayout L = slab_layout(n);
     const int64_t per_slot = has_val ? 8 : 4;
-    const int64_t cap = (o.workspace_bytes - L.bytes_fixed - 256) / per_slot;
-    if (cap < 1) return false;
+    int64_t cap = (o.workspace_bytes - L.bytes_fixed - (has_val ? 256 : 0)) / per_slot;
+    const int64_t need_max = n * (int64_t)s;
+    const int64_t need = o.nnz > 0 && o.nnz < need_max ? o.nnz : need_max;
+    if (cap < need || cap < 1) return false;
     char* ws = static_cast<char*>(o.workspace);
+    out->hdr = reinterpret_cast<es::WsHeader*>(ws);
     out->s_rowptr = reinterpret_cast<int64_t*>(ws + L.off_rowptr);
     out->s_col = reinterpret_cast<int32_t*>(ws + L.off_col);
     out->s_val = has_val ? reinterpret_cast<float*>(ws + slab_align(L.off_col + 4 * cap)) : nullptr;
@@ -136,14 +154,33 @@ bool slab_slots(const Opts& o, int64_t n, bool has_val, SlabSlots* out) {
     out->temp_bytes = (size_t)L.temp_bytes;
     return true;
 }
-// a1-a3 once into the workspace: count, scan, materialise
+
+// Signature of a sampling: everything the sampled slots depend on (never 0).
+uint64_t sampling_signature(int64_t n, int64_t row_begin, int32_t s, int32_t strategy, uint64_t seed,
+                            uint32_t prime, const int64_t* rowptr, int64_t nnz_base, const int32_t* colind,
+                            const float* val) {
+    uint64_t h = 0x6a09e667f3bcc908ull;
+    auto mix = [&](uint64_t x) {
+        h ^= x + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2);
+        h *= 0xBF58476D1CE4E5B9ull;
+        h ^= h >> 31;
+    };
+    mix((uint64_t)n); mix((uint64_t)row_begin); mix((uint64_t)s); mix((uint64_t)strategy); mix(seed);
+    mix(prime); mix(reinterpret_cast<uintptr_t>(rowptr)); mix((uint64_t)nnz_base);
+    mix(reinterpret_cast<uintptr_t>(colind)); mix(reinterpret_cast<uintptr_t>(val));
+    return h ? h : 1;
+}
+
+// a1-a3 once into the workspace: count, scan, materialise, sign
 cudaError_t slab_sample(const SlabSlots& sl, const int64_t* rowptr, int64_t nnz_base, const int32_t* colind,
                         const float* val, int64_t n, int32_t s, int32_t strategy, uint64_t seed, int64_t row_begin,
-                        uint32_t prime, cudaStream_t st, int* launches) {
-    cudaError_t err = es::launch_slab_count(rowptr, n, s, sl.s_rowptr, sl.temp, sl.temp_bytes, st, launches);
+                        uint32_t prime, uint64_t sig, cudaStream_t st, int* launches) {
+    // the count kernel clears the header (status 0, signature invalid) and the materialisation
+    // signs it: no extra launches
+    cudaError_t err = es::launch_slab_count(rowptr, n, s, sl.s_rowptr, sl.temp, sl.temp_bytes, st, launches, sl.hdr);
     if (err != cudaSuccess) return err;
     err = es::launch_sample_materialize(rowptr, nnz_base, colind, val, n, s, strategy, seed, row_begin, prime,
-                                        sl.s_rowptr, sl.s_col, sl.s_val, nullptr, st, sl.cap);
+                                        sl.s_rowptr, sl.s_col, sl.s_val, nullptr, st, sl.cap, sl.hdr, sig);
     ++*launches;
     return err;
 }
@@ -159,6 +196,81 @@ es_status_t run_rows_impl(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
     const int64_t n = row_end - row_begin;
     if (n == 0) return ES_OK;
     if (!rowptr || !C || (n_cols > 0 && !B)) return ES_ERR_INVALID_VALUE;
+    const es::Tune& tn = o.tune;
+    const bool force_slab = tn.kernel == ES_KERNEL_SLAB || tn.kernel == ES_KERNEL_SLAB_SMEM ||
+                            tn.kernel == ES_KERNEL_SLAB_LDG || tn.kernel == ES_KERNEL_SLAB_TMA;
+    const uintptr_t bu = reinterpret_cast<uintptr_t>(B), cu = reinterpret_cast<uintptr_t>(C);
+    const int64_t esz = o.bf16 ? 2 : 4;
+    const bool slab_layout_ok = o.workspace && bu % 16 == 0 && (ldb * esz) % 16 == 0 && slab_feasible(n_cols, F) &&
+                                tn.kernel != ES_KERNEL_FUSED && tn.kernel != ES_KERNEL_WARP &&
+                                tn.kernel != ES_KERNEL_TMA && tn.kernel != ES_KERNEL_CPASYNC &&
+                                tn.kernel != ES_KERNEL_CPASYNC_HW;
+    if (force_slab && !slab_layout_ok) return ES_ERR_UNSUPPORTED;
+    if (slab_layout_ok) {
+        // any C layout: 16-B vector stores where C's rows allow them, scalar stores otherwise
+        const bool c_vec16 = cu % 16 == 0 && ldc % 4 == 0;
+        // Bucket takes the first k_i entries of each row: they already lie contiguous in the
+        // CSR (Alg. 1 with p_j = j), so the passes read them in place -- no sampling pass
+        const bool direct = strategy == ES_BUCKET;
+        SlabSlots sl{};
+        if (!direct && !slab_slots(o, n, s, val != nullptr, &sl)) return ES_ERR_INVALID_VALUE;
+        int launches = 0;
+        cudaError_t err = cudaSuccess;
+        const uint64_t sig = sampling_signature(n, row_begin, s, strategy, seed, o.prime, rowptr, nnz_base,
+                                                colind, val);
+        if (!o.reuse_sampled && !direct)
+            err = slab_sample(sl, rowptr, nnz_base, colind, val, n, s, strategy, seed, row_begin, o.prime, sig, st,
+                              &launches);
+        // slices of 256-B slab rows: 64 fp32 or 128 bf16 elements
+        const int64_t wsl = o.bf16 ? 2 * kSlabF : kSlabF;
+        const bool b32 = bu % 32 == 0 && (ldb * esz) % 32 == 0;
+        CUtensorMap tmap;
+        const bool use_tma = tn.kernel == ES_KERNEL_SLAB_TMA;
+        if (use_tma && !es::encode_b_tensor_map(&tmap, B, F, ldb, n_cols, o.bf16)) return ES_ERR_UNSUPPORTED;
+        for (int64_t c0 = 0; err == cudaSuccess && c0 < F; c0 += wsl) {
+            es::SlabParams sp{};
+            sp.s_rowptr = direct ? rowptr : sl.s_rowptr;
+            sp.slot_base = direct ? nnz_base : 0;
+            sp.cap = direct ? INT64_MAX : sl.cap;
+            sp.s_colind = direct ? colind : sl.s_col;
+            sp.s_val = direct ? val : sl.s_val;
+            sp.direct_s = direct ? s : 0;
+            sp.ws_status = direct ? nullptr : &sl.hdr->status;
+            sp.ws_sig = direct ? nullptr : &sl.hdr->sig;
+            sp.sig = sig;
+            sp.rowptr = rowptr;
+            sp.b_bf16 = o.bf16;
+            sp.B = o.bf16 ? reinterpret_cast<const float*>(static_cast<const uint16_t*>(B) + c0)
+                          : static_cast<const float*>(B) + c0;
+            sp.ldb = ldb;
+            sp.w = (int32_t)(F - c0 < wsl ? F - c0 : wsl);
+            sp.b32 = b32 ? 1 : 0;
+            const bool ldg = b32 && tn.kernel == ES_KERNEL_SLAB_LDG;
+            if (tn.kernel == ES_KERNEL_SLAB_LDG && !b32) return ES_ERR_UNSUPPORTED;
+            // 16-B pieces (shared-memory ring) or 32-B pieces (register-direct)
+            sp.nv = ldg ? (int32_t)((sp.w * esz + 31) / 32) : (int32_t)((sp.w * esz + 15) / 16);
+            sp.C = C + c0;
+            sp.c_peers = o.c_peers;
+            sp.n_peers = o.n_peers;
+            sp.row_base = row_begin;
+            sp.col0 = c0;
+            sp.ldc = ldc;
+            sp.c_vec = c_vec16 ? 1 : 0;
+            sp.n_rows = n;
+            sp.reduce = reduce;
+            sp.mean_by_degree = o.mean_by_degree;
+            if (use_tma) {
+                sp.nv = (int32_t)((sp.w * esz + 15) / 16);
+                err = es::launch_slab_pass_tma(tmap, sp, (int32_t)c0, (int32_t)n_cols, tn, st);
+            } else {
+                err = es::launch_slab_pass(sp, tn, st);
+            }
+            ++launches;
+        }
+        g_launches.fetch_add(launches, std::memory_order_relaxed);
+        return err == cudaSuccess ? ES_OK : ES_ERR_CUDA;
+    }
+    if (o.reuse_sampled) return ES_ERR_INVALID_VALUE;      // no slab path: nothing to reuse
     es::SpmmParams p{};
     p.rowptr = rowptr;
     p.nnz_base = nnz_base;
@@ -180,59 +292,9 @@ es_status_t run_rows_impl(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
     p.b_bf16 = o.bf16;
     p.c_peers = o.c_peers;
     p.n_peers = o.n_peers;
-    const es::Plan plan = o.bf16 ? es::make_plan_bf16(F, ldb, ldc, B, C) : es::make_plan(F, ldb, ldc, B, C, s);
+    const es::Plan plan = o.bf16 ? es::make_plan_bf16(F, ldb, ldc, B, C) : es::make_plan(F, ldb, ldc, B, C, s, tn);
     if (plan.unsupported) return ES_ERR_UNSUPPORTED;
-    const uintptr_t bu = reinterpret_cast<uintptr_t>(B), cu = reinterpret_cast<uintptr_t>(C);
-    // any C layout: 16-B vector stores where C's rows allow them, scalar stores otherwise
-    const bool c_vec16 = cu % 16 == 0 && ldc % 4 == 0;
-    if (o.workspace && bu % 16 == 0 && ldb % (o.bf16 ? 8 : 4) == 0 && slab_feasible(n_cols, F)) {
-        SlabSlots sl;
-        int launches = 0;
-        cudaError_t err = cudaSuccess;
-        if (slab_slots(o, n, val != nullptr, &sl)) {
-            // Bucket takes the first k_i entries of each row: they already lie contiguous in the
-            // CSR (Alg. 1 with p_j = j), so the passes read them in place -- no sampling pass
-            const bool direct = strategy == ES_BUCKET;
-            if (!o.reuse_sampled && !direct)
-                err = slab_sample(sl, rowptr, nnz_base, colind, val, n, s, strategy, seed, row_begin, o.prime, st,
-                                  &launches);
-            const int stages = (int)env_i64("ES_SPMM_SLAB_STAGES", 4);
-            const int lanes = (int)env_i64("ES_SPMM_SLAB_G", 8);
-            // slices of 256-B slab rows: 64 fp32 or 128 bf16 elements
-            const int64_t wsl = o.bf16 ? 2 * kSlabF : kSlabF;
-            for (int64_t c0 = 0; err == cudaSuccess && c0 < F; c0 += wsl) {
-                es::SlabParams sp{};
-                sp.s_rowptr = direct ? rowptr : sl.s_rowptr;
-                sp.slot_base = direct ? nnz_base : 0;
-                sp.cap = direct ? INT64_MAX : sl.cap;
-                sp.s_colind = direct ? colind : sl.s_col;
-                sp.s_val = direct ? val : sl.s_val;
-                sp.direct_s = direct ? s : 0;
-                sp.rowptr = rowptr;
-                sp.b_bf16 = o.bf16;
-                sp.B = o.bf16 ? reinterpret_cast<const float*>(static_cast<const uint16_t*>(B) + c0)
-                              : static_cast<const float*>(B) + c0;
-                sp.ldb = ldb;
-                sp.w = (int32_t)(F - c0 < wsl ? F - c0 : wsl);
-                sp.nv = o.bf16 ? (sp.w + 7) / 8 : (sp.w + 3) / 4;
-                sp.C = C + c0;
-                sp.c_peers = o.c_peers;
-                sp.n_peers = o.n_peers;
-                sp.row_base = row_begin;
-                sp.col0 = c0;
-                sp.ldc = ldc;
-                sp.c_vec = c_vec16 ? 1 : 0;
-                sp.n_rows = n;
-                sp.reduce = reduce;
-                sp.mean_by_degree = o.mean_by_degree;
-                err = es::launch_slab_pass(sp, lanes, stages, st);
-                ++launches;
-            }
-            g_launches.fetch_add(launches, std::memory_order_relaxed);
-            return err == cudaSuccess ? ES_OK : ES_ERR_CUDA;
-        }
-    }
-    cudaError_t err = es::launch_spmm(p, plan, st);
+    cudaError_t err = es::launch_spmm(p, plan, tn, st);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return err == cudaSuccess ? ES_OK : ES_ERR_CUDA;
 }
@@ -257,10 +319,36 @@ int64_t es_launch_count(void) { return g_launches.load(std::memory_order_relaxed
 int64_t es_spmm_workspace_bytes(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t F, int64_t ldb,
                                 int32_t s, int32_t has_val) {
     if (n_rows <= 0 || n_cols < 0 || nnz < 0 || F < 1 || ldb < F || s < 1) return 0;
-    if (!slab_wanted(n_rows, n_cols, nnz, F, s)) return 0;
-    const SlabLayout L = slab_layout(n_rows);
+    if (!slab_wanted(n_rows, n_cols, nnz, F, ldb, s)) return 0;
     const int64_t cap = nnz < n_rows * (int64_t)s ? nnz : n_rows * (int64_t)s;
-    return L.bytes_fixed + 256 + slab_align(4 * (cap > 0 ? cap : 1)) + (has_val ? 4 * (cap > 0 ? cap : 1) : 0) + 256;
+    return slab_bytes(n_rows, cap, has_val != 0) + 256;
+}
+
+int64_t es_spmm_workspace_bytes_ex(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t F, int64_t ldb,
+                                   int32_t s, int32_t has_val, const es_spmm_options_t* opt) {
+    Opts o;
+    if (read_opts(opt, &o) != ES_OK) return 0;
+    const int k = o.tune.kernel;
+    if (k != ES_KERNEL_SLAB && k != ES_KERNEL_SLAB_SMEM && k != ES_KERNEL_SLAB_LDG && k != ES_KERNEL_SLAB_TMA)
+        return es_spmm_workspace_bytes(n_rows, n_cols, nnz, F, ldb, s, has_val);
+    // a slab kernel forced: a workspace wherever the path can run at all
+    if (n_rows <= 0 || n_cols < 0 || nnz < 0 || F < 1 || ldb < F || s < 1) return 0;
+    if (!slab_feasible(n_cols, F) || ldb % 4 != 0) return 0;
+    const int64_t cap = nnz < n_rows * (int64_t)s ? nnz : n_rows * (int64_t)s;
+    return slab_bytes(n_rows, cap, has_val != 0) + 256;
+}
+
+es_status_t es_spmm_workspace_status(void* workspace, int64_t workspace_bytes, int32_t reset, int32_t* status_out,
+                                     void* stream) {
+    if (!workspace || workspace_bytes < (int64_t)sizeof(es::WsHeader) || !status_out) return ES_ERR_INVALID_VALUE;
+    es::WsHeader* h = static_cast<es::WsHeader*>(workspace);
+    cudaStream_t st = as_stream(stream);
+    int32_t v = 0;
+    if (cudaMemcpyAsync(&v, &h->status, sizeof(v), cudaMemcpyDeviceToHost, st) != cudaSuccess) return ES_ERR_CUDA;
+    if (cudaStreamSynchronize(st) != cudaSuccess) return ES_ERR_CUDA;
+    *status_out = v;
+    if (reset && cudaMemsetAsync(&h->status, 0, sizeof(int32_t), st) != cudaSuccess) return ES_ERR_CUDA;
+    return ES_OK;
 }
 
 es_status_t es_spmm_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C,
@@ -392,14 +480,17 @@ es_status_t es_spmm_backward_ex(int64_t n_rows, int64_t n_cols, const int64_t* r
     // slab path (a workspace was passed): the gradient one 64-float slice at a time, the dB slab
     // L2-resident while its reductions land; the sampled slots come from the workspace
     // (reuse_sampled: the forward's) or are sampled here
-    SlabSlots sl;
-    if (o.workspace && p.vec == 4 && slab_feasible(n_cols, F) && slab_slots(o, n, val != nullptr, &sl)) {
+    const bool direct = strategy == ES_BUCKET;                   // first k_i entries, in place
+    SlabSlots sl{};
+    if (o.workspace && p.vec == 4 && slab_feasible(n_cols, F)) {
+        if (!direct && !slab_slots(o, n, s, val != nullptr, &sl)) return ES_ERR_INVALID_VALUE;
         cudaStream_t st = as_stream(stream);
         int launches = 0;
         cudaError_t err = cudaSuccess;
-        const bool direct = strategy == ES_BUCKET;               // first k_i entries, in place
+        const uint64_t sig = sampling_signature(n, row_begin, s, strategy, seed, o.prime, rowptr, nnz_base,
+                                                colind, val);
         if (!o.reuse_sampled && !direct)
-            err = slab_sample(sl, rowptr, nnz_base, colind, val, n, s, strategy, seed, row_begin, o.prime, st,
+            err = slab_sample(sl, rowptr, nnz_base, colind, val, n, s, strategy, seed, row_begin, o.prime, sig, st,
                               &launches);
         for (int64_t c0 = 0; err == cudaSuccess && c0 < F; c0 += kSlabF) {
             es::SlabParams sp{};
@@ -409,6 +500,9 @@ es_status_t es_spmm_backward_ex(int64_t n_rows, int64_t n_cols, const int64_t* r
             sp.s_colind = direct ? colind : sl.s_col;
             sp.s_val = direct ? val : sl.s_val;
             sp.direct_s = direct ? s : 0;
+            sp.ws_status = direct ? nullptr : &sl.hdr->status;
+            sp.ws_sig = direct ? nullptr : &sl.hdr->sig;
+            sp.sig = sig;
             sp.rowptr = rowptr;
             sp.ldb = ldb;
             sp.w = (int32_t)(F - c0 < kSlabF ? F - c0 : kSlabF);
@@ -423,6 +517,7 @@ es_status_t es_spmm_backward_ex(int64_t n_rows, int64_t n_cols, const int64_t* r
         g_launches.fetch_add(launches, std::memory_order_relaxed);
         return err == cudaSuccess ? ES_OK : ES_ERR_CUDA;
     }
+    if (o.reuse_sampled) return ES_ERR_INVALID_VALUE;      // no slab path: nothing to reuse
     cudaError_t err = es::launch_backward(p, as_stream(stream));
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return err == cudaSuccess ? ES_OK : ES_ERR_CUDA;
@@ -489,12 +584,80 @@ es_status_t es_partition_rows(const int64_t* rowptr_host, int64_t n_rows, int32_
 // ---------------------------------------------------------------- host-buffer pipeline
 static inline int64_t align256(int64_t x) { return (x + 255) & ~(int64_t)255; }
 
+}  // extern "C"
+
+struct es_host_pipeline {
+    cudaStream_t s_in = nullptr, s_out = nullptr;
+    cudaEvent_t ev_start = nullptr, ev_out = nullptr;
+    std::vector<cudaEvent_t> ev_in, ev_done;
+};
+
+namespace {
+constexpr int kHostMaxChunks = 8;
+
+void destroy_pipeline(es_host_pipeline* p) {
+    if (!p) return;
+    if (p->s_in) { cudaStreamSynchronize(p->s_in); cudaStreamDestroy(p->s_in); }
+    if (p->s_out) { cudaStreamSynchronize(p->s_out); cudaStreamDestroy(p->s_out); }
+    for (auto e : p->ev_in) if (e) cudaEventDestroy(e);
+    for (auto e : p->ev_done) if (e) cudaEventDestroy(e);
+    if (p->ev_start) cudaEventDestroy(p->ev_start);
+    if (p->ev_out) cudaEventDestroy(p->ev_out);
+    delete p;
+}
+
+es_host_pipeline* make_pipeline() {
+    es_host_pipeline* p = new (std::nothrow) es_host_pipeline();
+    if (!p) return nullptr;
+    bool ok = cudaStreamCreateWithFlags(&p->s_in, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&p->s_out, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaEventCreateWithFlags(&p->ev_start, cudaEventDisableTiming) == cudaSuccess &&
+              cudaEventCreateWithFlags(&p->ev_out, cudaEventDisableTiming) == cudaSuccess;
+    p->ev_in.assign(kHostMaxChunks, nullptr);
+    p->ev_done.assign(kHostMaxChunks, nullptr);
+    for (int c = 0; ok && c < kHostMaxChunks; ++c)
+        ok = cudaEventCreateWithFlags(&p->ev_in[(size_t)c], cudaEventDisableTiming) == cudaSuccess &&
+             cudaEventCreateWithFlags(&p->ev_done[(size_t)c], cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) {
+        destroy_pipeline(p);
+        return nullptr;
+    }
+    return p;
+}
+
+// device workspace of the host pipeline: [rowptr][colind][val][B][C][slab workspace (cap = nnz)]
+struct HostLayout {
+    int64_t off_rowptr, off_col, off_val, off_B, off_C, off_slab, slab_bytes, total;
+};
+HostLayout host_layout(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t F, int64_t ldb, bool has_val) {
+    HostLayout L{};
+    L.off_rowptr = 0;
+    L.off_col = align256((n_rows + 1) * 8);
+    L.off_val = L.off_col + align256(nnz * 4);
+    L.off_B = L.off_val + (has_val ? align256(nnz * 4) : 0);
+    L.off_C = L.off_B + align256(n_cols * ldb * 4);
+    L.off_slab = L.off_C + align256(n_rows * ldb * 4);
+    // room for the slab path (sampled slots of any s: at most nnz) where the layout can take it
+    L.slab_bytes = (slab_feasible(n_cols, F) && F >= 128 && ldb % 4 == 0) ? slab_bytes(n_rows, nnz, has_val) + 256 : 0;
+    L.total = L.off_slab + L.slab_bytes;
+    return L;
+}
+}  // namespace
+
+extern "C" {
+
+es_status_t es_host_pipeline_create(es_host_pipeline_t** out) {
+    if (!out) return ES_ERR_INVALID_VALUE;
+    *out = make_pipeline();
+    return *out ? ES_OK : ES_ERR_CUDA;
+}
+
+void es_host_pipeline_destroy(es_host_pipeline_t* pipe) { destroy_pipeline(pipe); }
+
 int64_t es_spmm_host_workspace_bytes(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t F,
                                      int64_t ldb, int32_t has_val) {
-    (void)F;
-    if (n_rows < 0 || n_cols < 0 || nnz < 0 || ldb < 1) return -1;
-    return align256((n_rows + 1) * 8) + align256(nnz * 4) + (has_val ? align256(nnz * 4) : 0) +
-           align256(n_cols * ldb * 4) + align256(n_rows * ldb * 4);
+    if (n_rows < 0 || n_cols < 0 || nnz < 0 || ldb < 1 || F < 1) return -1;
+    return host_layout(n_rows, n_cols, nnz, F, ldb, has_val != 0).total;
 }
 
 es_status_t es_spmm_run_host(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
@@ -502,49 +665,60 @@ es_status_t es_spmm_run_host(int64_t n_rows, int64_t n_cols, const int64_t* rowp
                              int64_t ldb, int32_t s, int32_t strategy, uint64_t seed, int32_t reduce,
                              int64_t row_base, float* C, int64_t ldc, void* workspace,
                              int64_t workspace_bytes, void* stream) {
+    return es_spmm_run_host_ex(n_rows, n_cols, rowptr, colind, val, B, F, ldb, s, strategy, seed, reduce,
+                               row_base, C, ldc, workspace, workspace_bytes, nullptr, nullptr, stream);
+}
+
+es_status_t es_spmm_run_host_ex(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
+                                const int32_t* colind, const float* val, const float* B, int64_t F,
+                                int64_t ldb, int32_t s, int32_t strategy, uint64_t seed, int32_t reduce,
+                                int64_t row_base, float* C, int64_t ldc, void* workspace,
+                                int64_t workspace_bytes, const es_spmm_options_t* opt,
+                                es_host_pipeline_t* pipe, void* stream) {
     es_status_t rc = check_common(n_rows, n_cols, F, ldb, ldc, s, strategy, reduce);
     if (rc != ES_OK) return rc;
+    Opts o;
+    if (read_opts(opt, &o) != ES_OK || o.bf16 || o.n_peers || o.workspace || o.reuse_sampled)
+        return ES_ERR_INVALID_VALUE;                 // host buffers: fp32 B, no peers, own workspace
     if (n_rows == 0) return ES_OK;
     if (!rowptr || !C || !workspace || (n_cols > 0 && !B) || row_base < 0) return ES_ERR_INVALID_VALUE;
     const int64_t base = rowptr[0];
     const int64_t nnz = rowptr[n_rows] - base;
     if (nnz > 0 && !colind) return ES_ERR_INVALID_VALUE;
-    const int64_t need = es_spmm_host_workspace_bytes(n_rows, n_cols, nnz, F, ldb, val != nullptr);
-    if (workspace_bytes < need) return ES_ERR_INVALID_VALUE;
+    const HostLayout L = host_layout(n_rows, n_cols, nnz, F, ldb, val != nullptr);
+    if (workspace_bytes < L.total) return ES_ERR_INVALID_VALUE;
 
-    // device workspace layout; the device C uses ldc' = ldb (dense, 16 B rows when ldb % 4 == 0)
     char* w = static_cast<char*>(workspace);
-    int64_t* d_rowptr = reinterpret_cast<int64_t*>(w); w += align256((n_rows + 1) * 8);
-    int32_t* d_colind = reinterpret_cast<int32_t*>(w); w += align256(nnz * 4);
-    float* d_val = nullptr;
-    if (val) { d_val = reinterpret_cast<float*>(w); w += align256(nnz * 4); }
-    float* d_B = reinterpret_cast<float*>(w); w += align256(n_cols * ldb * 4);
-    float* d_C = reinterpret_cast<float*>(w);
-    const int64_t dldc = ldb;
+    int64_t* d_rowptr = reinterpret_cast<int64_t*>(w + L.off_rowptr);
+    int32_t* d_colind = reinterpret_cast<int32_t*>(w + L.off_col);
+    float* d_val = val ? reinterpret_cast<float*>(w + L.off_val) : nullptr;
+    float* d_B = reinterpret_cast<float*>(w + L.off_B);
+    float* d_C = reinterpret_cast<float*>(w + L.off_C);
+    const int64_t dldc = ldb;                        // device C rows as B's (16-B rows when ldb % 4 == 0)
+    // the library's plan: the slab path where es_spmm_workspace_bytes would ask for it
+    const bool slab = L.slab_bytes > 0 && slab_wanted(n_rows, n_cols, nnz, F, ldb, s) &&
+                      o.tune.kernel != ES_KERNEL_FUSED;
 
     cudaStream_t st = as_stream(stream);
-    cudaStream_t s_in = nullptr, s_out = nullptr;
-    const int kMaxChunks = 8;
-    int n_chunks = (int)std::min<int64_t>(kMaxChunks, std::max<int64_t>(1, n_rows / 4096));
-    std::vector<cudaEvent_t> ev_in((size_t)n_chunks, nullptr), ev_done((size_t)n_chunks, nullptr);
-    cudaEvent_t ev_start = nullptr, ev_out = nullptr;
+    es_host_pipeline* own = nullptr;
+    if (!pipe) {
+        own = make_pipeline();
+        if (!own) return ES_ERR_CUDA;
+        pipe = own;
+    }
+    const int n_chunks = (int)std::min<int64_t>(kHostMaxChunks, std::max<int64_t>(1, n_rows / 4096));
     cudaError_t err = cudaSuccess;
     auto ok = [&](cudaError_t e) { if (err == cudaSuccess && e != cudaSuccess) err = e; return err == cudaSuccess; };
 
-    if (!ok(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking)) ||
-        !ok(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking)) ||
-        !ok(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming)) ||
-        !ok(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming))) goto cleanup;
-    for (int c = 0; c < n_chunks; ++c)
-        if (!ok(cudaEventCreateWithFlags(&ev_in[(size_t)c], cudaEventDisableTiming)) ||
-            !ok(cudaEventCreateWithFlags(&ev_done[(size_t)c], cudaEventDisableTiming))) goto cleanup;
-
     // inputs may only be overwritten after earlier work on the caller's stream
-    if (!ok(cudaEventRecord(ev_start, st)) || !ok(cudaStreamWaitEvent(s_in, ev_start, 0))) goto cleanup;
-    if (!ok(cudaMemcpyAsync(d_rowptr, rowptr, (size_t)(n_rows + 1) * 8, cudaMemcpyHostToDevice, s_in)))
-        goto cleanup;
+    if (!ok(cudaEventRecord(pipe->ev_start, st)) || !ok(cudaStreamWaitEvent(pipe->s_in, pipe->ev_start, 0)) ||
+        !ok(cudaStreamWaitEvent(pipe->s_out, pipe->ev_start, 0)))
+        goto done;
+    // every row gathers from all of B: B (and rowptr) first, then the CSR chunk by chunk
+    if (!ok(cudaMemcpyAsync(d_rowptr, rowptr, (size_t)(n_rows + 1) * 8, cudaMemcpyHostToDevice, pipe->s_in)))
+        goto done;
     if (n_cols > 0 &&
-        !ok(cudaMemcpyAsync(d_B, B, (size_t)(n_cols * ldb) * 4, cudaMemcpyHostToDevice, s_in))) goto cleanup;
+        !ok(cudaMemcpyAsync(d_B, B, (size_t)(n_cols * ldb) * 4, cudaMemcpyHostToDevice, pipe->s_in))) goto done;
     {
         int64_t r0 = 0;
         for (int c = 0; c < n_chunks; ++c) {
@@ -558,36 +732,49 @@ es_status_t es_spmm_run_host(int64_t n_rows, int64_t n_cols, const int64_t* rowp
             const int64_t e0 = rowptr[r0] - base, e1 = rowptr[r1] - base;
             if (e1 > e0) {
                 if (!ok(cudaMemcpyAsync(d_colind + e0, colind + e0, (size_t)(e1 - e0) * 4,
-                                        cudaMemcpyHostToDevice, s_in))) goto cleanup;
+                                        cudaMemcpyHostToDevice, pipe->s_in))) goto done;
                 if (val && !ok(cudaMemcpyAsync(d_val + e0, val + e0, (size_t)(e1 - e0) * 4,
-                                               cudaMemcpyHostToDevice, s_in))) goto cleanup;
+                                               cudaMemcpyHostToDevice, pipe->s_in))) goto done;
             }
-            if (!ok(cudaEventRecord(ev_in[(size_t)c], s_in)) || !ok(cudaStreamWaitEvent(st, ev_in[(size_t)c], 0)))
-                goto cleanup;
+            if (!ok(cudaEventRecord(pipe->ev_in[(size_t)c], pipe->s_in)) ||
+                !ok(cudaStreamWaitEvent(st, pipe->ev_in[(size_t)c], 0)))
+                goto done;
+            Opts oc = o;
+            if (slab) {                               // one workspace, reused chunk after chunk (stream order)
+                oc.workspace = w + L.off_slab;
+                oc.workspace_bytes = L.slab_bytes;
+                oc.nnz = e1 - e0;
+            }
             rc = run_rows_impl(row_base + n_rows, n_cols, d_rowptr + r0, base, d_colind, d_val, d_B, F,
                                ldb, s, strategy, seed, reduce, d_C + r0 * dldc, dldc, row_base + r0,
-                               row_base + r1, Opts{}, st);
-            if (rc != ES_OK) goto cleanup;
-            if (!ok(cudaEventRecord(ev_done[(size_t)c], st)) || !ok(cudaStreamWaitEvent(s_out, ev_done[(size_t)c], 0)))
-                goto cleanup;
-            if (r1 > r0 &&
-                !ok(cudaMemcpy2DAsync(C + r0 * ldc, (size_t)ldc * 4, d_C + r0 * dldc, (size_t)dldc * 4,
-                                      (size_t)F * 4, (size_t)(r1 - r0), cudaMemcpyDeviceToHost, s_out)))
-                goto cleanup;
+                               row_base + r1, oc, st);
+            if (rc != ES_OK) goto done;
+            if (!ok(cudaEventRecord(pipe->ev_done[(size_t)c], st)) ||
+                !ok(cudaStreamWaitEvent(pipe->s_out, pipe->ev_done[(size_t)c], 0)))
+                goto done;
+            if (r1 > r0) {
+                // one linear copy when the host rows have the device pitch, else a 2-D copy
+                const bool flat = ldc == dldc;
+                cudaError_t e = flat ? cudaMemcpyAsync(C + r0 * ldc, d_C + r0 * dldc, (size_t)((r1 - r0) * dldc) * 4,
+                                                       cudaMemcpyDeviceToHost, pipe->s_out)
+                                     : cudaMemcpy2DAsync(C + r0 * ldc, (size_t)ldc * 4, d_C + r0 * dldc,
+                                                         (size_t)dldc * 4, (size_t)F * 4, (size_t)(r1 - r0),
+                                                         cudaMemcpyDeviceToHost, pipe->s_out);
+                if (!ok(e)) goto done;
+            }
             r0 = r1;
         }
     }
-    if (!ok(cudaEventRecord(ev_out, s_out)) || !ok(cudaStreamWaitEvent(st, ev_out, 0))) goto cleanup;
+    if (!ok(cudaEventRecord(pipe->ev_out, pipe->s_out)) || !ok(cudaStreamWaitEvent(st, pipe->ev_out, 0))) goto done;
     ok(cudaStreamSynchronize(st));
 
-cleanup:
-    if (err != cudaSuccess) cudaStreamSynchronize(st);
-    for (auto e : ev_in) if (e) cudaEventDestroy(e);
-    for (auto e : ev_done) if (e) cudaEventDestroy(e);
-    if (ev_start) cudaEventDestroy(ev_start);
-    if (ev_out) cudaEventDestroy(ev_out);
-    if (s_in) { cudaStreamSynchronize(s_in); cudaStreamDestroy(s_in); }
-    if (s_out) { cudaStreamSynchronize(s_out); cudaStreamDestroy(s_out); }
+done:
+    if (err != cudaSuccess || rc != ES_OK) {
+        cudaStreamSynchronize(pipe->s_in);
+        cudaStreamSynchronize(pipe->s_out);
+        cudaStreamSynchronize(st);
+    }
+    if (own) destroy_pipeline(own);
     if (rc != ES_OK) return rc;
     return err == cudaSuccess ? ES_OK : ES_ERR_CUDA;
 }

@@ -1,9 +1,20 @@
 // es_internal.h -- internal (C++) interface between the C ABI layer and the kernels.
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace es {
+
+// Kernel selection / A-B knobs (es_spmm_options_t.kernel + tune[]; 0 = the measured default).
+// The product path reads no environment: everything arrives through the options struct.
+struct Tune {
+    int kernel = 0;      // ES_KERNEL_*
+    int stages = 0;      // ring depth
+    int width = 0;       // lanes per slot (slab) / rows per warp (TMA)
+    int cta_warps = 0;   // warps per CTA
+    int variant = 0;     // kernel-specific variant bits
+};
 
 struct SpmmParams {
     const int64_t* rowptr;   // local row r uses rowptr[r], rowptr[r+1] (absolute offsets)
@@ -87,32 +98,58 @@ struct SlabParams {
     int64_t row_base;         // global id of local row 0 (peer stores)
     int64_t col0;             // the slice's first column (peer stores)
     int32_t b_bf16;           // B holds bf16 (NEXT-4 storage variant): B points at uint16_t elements
+    int32_t b32;              // B base and row pitch 32-B aligned (256-bit gathers possible)
     int32_t direct_s;         // > 0 (Bucket): the slots are the CSR itself -- s_rowptr/s_colind/s_val
                               // are rowptr/colind/val, k_i = min(d_i, direct_s); no sampling pass
+    // device backstops (workspace header, DESIGN.md §1 "Boundary"): a row whose slots end past
+    // `cap` (overflow) or a call whose expected sampling signature differs from the one the
+    // sampling pass wrote (reuse_sampled) writes NaN rows and ORs a flag into *ws_status
+    int32_t* ws_status;       // NULL: no workspace (direct Bucket slots)
+    const uint64_t* ws_sig;   // signature written by the sampling call (NULL: not checked)
+    uint64_t sig;             // the signature this call expects
 };
 
-cudaError_t launch_slab_pass(const SlabParams& p, int lanes_per_slot, int stages, cudaStream_t st);
+// workspace header (first 256 B of a slab workspace)
+struct WsHeader {
+    uint64_t sig;             // signature of the sampling call that filled the slots
+    int32_t status;           // ES_WS_* flags (device-written)
+    int32_t pad;
+};
+constexpr int kWsOverflow = 1, kWsSignature = 2;
+
+cudaError_t launch_slab_pass(const SlabParams& p, const Tune& t, cudaStream_t st);
+// TMA gather4 slab pass: tm = a 2-D tensor map over B (inner dim F elements, rows n_cols, box
+// {256 B of elements, 1}), c0 = the slice's first column
+cudaError_t launch_slab_pass_tma(const CUtensorMap& tm, const SlabParams& p, int32_t c0, int32_t n_cols,
+                                 const Tune& t, cudaStream_t st);
+// encodes that tensor map (driver entry point, no libcuda link); false if the layout is not
+// expressible (pitch not a multiple of 16 B, > 2^31 rows, ...)
+bool encode_b_tensor_map(CUtensorMap* tm, const void* B, int64_t F, int64_t ldb, int64_t n_cols, bool bf16);
+
 // backward slab pass: p.C/ldc describe dC's slice (read), dB the slice of the gradient (reduced into)
 cudaError_t launch_slab_backward(const SlabParams& p, const float* dC, float* dB, cudaStream_t st);
 size_t slab_scan_temp_bytes(int64_t n);
+// hdr (may be NULL): the workspace header, cleared by the count kernel (status 0, signature 0)
 cudaError_t launch_slab_count(const int64_t* rowptr, int64_t n, int32_t s, int64_t* s_rowptr, void* temp,
-                              size_t temp_bytes, cudaStream_t st, int* launches);
+                              size_t temp_bytes, cudaStream_t st, int* launches, WsHeader* hdr = nullptr);
 cudaError_t launch_sample_count_only(const int64_t* rowptr, int64_t n, int32_t s, int64_t* s_rowptr,
-                                     cudaStream_t st);
+                                     cudaStream_t st, WsHeader* hdr = nullptr);
 
 cudaError_t launch_backward(const BwdParams& p, cudaStream_t st);
 cudaError_t launch_backward_deterministic(const BwdParams& p, int64_t n_cols, cudaStream_t st, int* launches,
                                           bool* too_large);
 
-Plan make_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C, int32_t s = INT32_MAX);
+Plan make_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C, int32_t s = INT32_MAX,
+               const Tune& t = Tune{});
 Plan make_plan_bf16(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C);
-cudaError_t launch_spmm(SpmmParams p, const Plan& plan, cudaStream_t st);
+cudaError_t launch_spmm(SpmmParams p, const Plan& plan, const Tune& t, cudaStream_t st);
 cudaError_t launch_sample_count(const int64_t* rowptr, int64_t n, int32_t s, int64_t* s_rowptr,
                                 cudaStream_t st, int* launches);
 cudaError_t launch_sample_materialize(const int64_t* rowptr, int64_t nnz_base, const int32_t* colind,
                                       const float* val, int64_t n, int32_t s, int32_t strategy,
                                       uint64_t seed, int64_t row_base, uint32_t prime,
                                       const int64_t* s_rowptr, int32_t* s_colind, float* s_val,
-                                      int64_t* s_pos, cudaStream_t st, int64_t cap = INT64_MAX);
+                                      int64_t* s_pos, cudaStream_t st, int64_t cap = INT64_MAX,
+                                      WsHeader* hdr = nullptr, uint64_t sig = 0);
 
 }  // namespace es

@@ -30,6 +30,7 @@
 
 #include "es_device.cuh"
 #include "es_internal.h"
+#include "es_spmm.h"
 
 namespace es {
 
@@ -776,9 +777,12 @@ cudaError_t launch_backward(const BwdParams& p, cudaStream_t st) {
 
 // ------------------------------------------------------------------ sampler (es_spmm_sample)
 __global__ void sample_count(const int64_t* __restrict__ rowptr, int64_t n, int32_t s,
-                             int64_t* __restrict__ s_rowptr) {
+                             int64_t* __restrict__ s_rowptr, WsHeader* hdr) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i == 0) s_rowptr[0] = 0;
+    if (i == 0) {
+        s_rowptr[0] = 0;
+        if (hdr) { hdr->status = 0; hdr->sig = 0; }     // a new sampling: clear the workspace header
+    }
     if (i < n) {
         const int64_t d = rowptr[i + 1] - rowptr[i];
         s_rowptr[i + 1] = d < (int64_t)s ? d : (int64_t)s;
@@ -790,13 +794,18 @@ sample_materialize(const int64_t* __restrict__ rowptr, int64_t nnz_base,
                    const int32_t* __restrict__ colind, const float* __restrict__ val, int64_t n,
                    int32_t s, int32_t strategy, uint64_t seed, int64_t row_base, uint32_t prime,
                    const int64_t* __restrict__ s_rowptr, int32_t* __restrict__ s_colind,
-                   float* __restrict__ s_val, int64_t* __restrict__ s_pos, int64_t cap) {
+                   float* __restrict__ s_val, int64_t* __restrict__ s_pos, int64_t cap, WsHeader* hdr,
+                   uint64_t sig) {
     const int lane = threadIdx.x & 31;
     const int64_t r = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+    if (hdr && blockIdx.x == 0 && threadIdx.x == 0) hdr->sig = sig;    // the slots' signature
     if (r >= n) return;
     RowSampler rs;
     rs.init(rowptr[r] - nnz_base, rowptr[r + 1] - nnz_base, s, strategy, seed, row_base + r, prime);
     const int64_t o0 = s_rowptr[r];
+    // overflow backstop: the row's slots do not fit (the caller understated nnz); the slab
+    // passes poison the row (es_slab.cu slab_row_guard) -- flagged here too
+    if (hdr && lane == 0 && o0 + rs.k > cap) atomicOr(&hdr->status, kWsOverflow);
     for (int32_t j = lane; j < rs.k && o0 + j < cap; j += 32) {
         const int64_t pj = rs.pos(j);
         const int64_t e = rs.beg + pj;
@@ -808,11 +817,6 @@ sample_materialize(const int64_t* __restrict__ rowptr, int64_t nnz_base,
 
 // ------------------------------------------------------------------ host launchers
 namespace {
-
-int env_int_k(const char* name, int dflt) {
-    const char* e = getenv(name);
-    return e ? atoi(e) : dflt;
-}
 
 template <int NCH, int D, int MINB, typename TB = float>
 cudaError_t launch_cpasync_k(const SpmmParams& p, cudaStream_t st) {
@@ -851,22 +855,22 @@ cudaError_t launch_cpasync_hw_w(const SpmmParams& p, cudaStream_t st) {
 }
 
 template <int D, int MINB>
-cudaError_t launch_cpasync_hw_k(const SpmmParams& p, cudaStream_t st) {
+cudaError_t launch_cpasync_hw_k(const SpmmParams& p, int cta_warps, cudaStream_t st) {
     // 2-warp CTAs: a CTA's slot frees as soon as its 2 rows are done (short, unequal rows:
     // Arxiv-shaped F=128 s=64 0.177 -> 0.156 ms; Proteins s=64 -0.7 %; profiles/r01.md)
-    const int w = env_int_k("ES_SPMM_HW_CTA_WARPS", 2);      // tuning: warps per CTA
+    const int w = cta_warps > 0 ? cta_warps : 2;
     if (w == 4) return launch_cpasync_hw_w<D, MINB, 4>(p, st);
     if (w == 2) return launch_cpasync_hw_w<D, MINB, 2>(p, st);
     return launch_cpasync_hw_w<D, MINB, 8>(p, st);
 }
 
-cudaError_t launch_cpasync(const SpmmParams& p, const Plan& plan, cudaStream_t st) {
+cudaError_t launch_cpasync(const SpmmParams& p, const Plan& plan, const Tune& t, cudaStream_t st) {
     if (plan.bf16) return launch_cpasync_bf16(p, plan, st);
     if (plan.halfwarp) {
         switch (plan.stages) {
-            case 2: return plan.minb >= 5 ? launch_cpasync_hw_k<2, 5>(p, st) : launch_cpasync_hw_k<2, 4>(p, st);
-            case 8: return plan.minb >= 5 ? launch_cpasync_hw_k<8, 5>(p, st) : launch_cpasync_hw_k<8, 4>(p, st);
-            default: return plan.minb >= 5 ? launch_cpasync_hw_k<4, 5>(p, st) : launch_cpasync_hw_k<4, 4>(p, st);
+            case 2: return launch_cpasync_hw_k<2, 5>(p, t.cta_warps, st);
+            case 8: return launch_cpasync_hw_k<8, 5>(p, t.cta_warps, st);
+            default: return launch_cpasync_hw_k<4, 5>(p, t.cta_warps, st);
         }
     }
     // Register caps that force spills made this kernel trap with cudaErrorIllegalInstruction on
@@ -985,21 +989,6 @@ cudaError_t dispatch_vec(const SpmmParams& p, const Plan& plan, cudaStream_t st)
 
 }  // namespace
 
-static int env_kernel_override() {
-    // ES_SPMM_KERNEL=warp|tma (tuning / A-B measurement only; default: auto)
-    const char* e = getenv("ES_SPMM_KERNEL");
-    if (!e) return 0;
-    if (!strcmp(e, "warp")) return 1;
-    if (!strcmp(e, "tma")) return 2;
-    if (!strcmp(e, "cpasync")) return 3;
-    return 0;
-}
-
-static int env_int(const char* name, int dflt) {
-    const char* e = getenv(name);
-    return e ? atoi(e) : dflt;
-}
-
 Plan make_plan_bf16(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C) {
     // bf16 B (NEXT-4): cp.async ring only -- 16-B aligned rows (ldb % 8 == 0), F <= 2048.
     Plan pl{};
@@ -1016,14 +1005,14 @@ Plan make_plan_bf16(int64_t F, int64_t ldb, int64_t ldc, const void* B, const vo
     return pl;
 }
 
-Plan make_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C, int32_t s) {
+Plan make_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C, int32_t s, const Tune& t) {
     Plan pl{};
     const uintptr_t b = reinterpret_cast<uintptr_t>(B), c = reinterpret_cast<uintptr_t>(C);
     if (b % 16 == 0 && ldb % 4 == 0) pl.vec = 4;
     else if (b % 8 == 0 && ldb % 2 == 0) pl.vec = 2;
     else pl.vec = 1;
     const int64_t nv = (F + pl.vec - 1) / pl.vec;
-    if (nv <= 16) {                  // (tuning: ES_SPMM_CPASYNC_MIN_NV4 lowers the cp.async bound)
+    if (nv <= 16) {
         pl.subwarp = true;
         int g = 1;
         while (g < nv) g <<= 1;
@@ -1034,51 +1023,49 @@ Plan make_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C
         pl.nch = (int)(nch > 8 ? 8 : nch);
     }
     pl.c_vec = (c % (4u * (unsigned)pl.vec) == 0) && (ldc % pl.vec == 0);
-    pl.u = env_int("ES_SPMM_U", 4);
-    pl.minb = env_int("ES_SPMM_MINB", 4);
+    pl.u = 4;
+    pl.minb = 4;
+    const int ov = t.kernel;
     // TMA ring: whole 16-B padded B rows as bulk copies; needs 16-B alignment and F <= 1024.
-    const int64_t nv4 = (F + 3) / 4;
     // Measured (profiles/r01.md): TMA wins for wide rows (Reddit F=602: 9.5 vs 26.8 ms,
     // F=256: 4.8 vs 8.2 ms); for 512-B rows (F=128) the LDG warp kernel wins (2.97 vs 4.3 ms).
-    const int64_t kTmaMinRowBytes = env_int("ES_SPMM_TMA_MIN_BYTES", 2048);
+    const int64_t nv4 = (F + 3) / 4;
+    constexpr int64_t kTmaMinRowBytes = 2048;
     const bool tma_ok = pl.vec == 4 && nv4 > 32 && nv4 <= 32 * 8;
-    const int ov = env_kernel_override();
-    pl.tma = tma_ok && ov != 1 && (ov == 2 || ldb * 4 >= kTmaMinRowBytes);
+    pl.tma = tma_ok && ov != ES_KERNEL_WARP && (ov == ES_KERNEL_TMA || ldb * 4 >= kTmaMinRowBytes);
     // cp.async ring: 16-B aligned B, 16 < F/4 <= 128 by default (profiles/r01.md: Reddit F=128
     // 1.95 vs 2.27 ms, F=256 3.13 vs 4.55 (TMA), F=512 7.23 vs 7.51 (TMA); F=602 TMA wins 9.4 vs
-    // 10.4); forced up to F/4 <= 256 with ES_SPMM_KERNEL=cpasync.
-    pl.cpasync = pl.vec == 4 && nv4 > env_int("ES_SPMM_CPASYNC_MIN_NV4", 16) && nv4 <= 32 * 8 &&
-                 (ov == 3 || (ov == 0 && nv4 <= 32 * 4));
+    // 10.4); forced up to F/4 <= 256 with ES_KERNEL_CPASYNC.
+    const bool force_cp = ov == ES_KERNEL_CPASYNC || ov == ES_KERNEL_CPASYNC_HW;
+    pl.cpasync = pl.vec == 4 && nv4 > 16 && nv4 <= 32 * 8 &&
+                 (force_cp || ((ov == ES_KERNEL_AUTO || ov == ES_KERNEL_FUSED) && nv4 <= 32 * 4));
     if (pl.cpasync) {
         pl.tma = false;
         pl.nch = (int)((nv4 + 31) / 32);
-        pl.stages = env_int("ES_SPMM_STAGES", 4);
-        pl.minb = env_int("ES_SPMM_MINB", pl.nch == 1 ? 5 : 1);
+        pl.stages = t.stages > 0 ? t.stages : 4;
+        pl.minb = pl.nch == 1 ? 5 : 1;
         // two slots per step for F <= 128 (profiles/r01.md: Reddit F=128 1.88 vs 1.99 ms,
-        // Proteins 1.19 vs 1.30 ms); ES_SPMM_HALFWARP=0 selects the one-slot ring
-        pl.halfwarp = pl.nch == 1 && env_int("ES_SPMM_HALFWARP", 1) != 0;
+        // Proteins 1.19 vs 1.30 ms); ES_KERNEL_CPASYNC forces the one-slot ring
+        pl.halfwarp = pl.nch == 1 && ov != ES_KERNEL_CPASYNC;
     }
     if (pl.tma) {
         pl.nch = (int)((nv4 + 31) / 32);
         pl.subwarp = false;
-        int stages = env_int("ES_SPMM_STAGES", 0);
-        if (stages != 3 && stages != 8) stages = 4;
-        pl.stages = stages;
+        pl.stages = (t.stages == 3 || t.stages == 8) ? t.stages : 4;
         // rows per warp: 4 when rows are short (s <= 64: the warp's slot stream then spans
         // several rows and one CTA's start-up serves them; Reddit F=602 s=16 1.08 -> 0.94 ms,
         // bitwise identical; profiles/r01.md), else 1 (s = 256: 1 is best)
-        const int rpw = env_int("ES_SPMM_ROWS_PER_WARP", 0);
-        pl.rows_per_warp = (rpw >= 1 && rpw <= 32) ? rpw : (s <= 64 ? 4 : 1);
-        pl.minb = env_int("ES_SPMM_MINB", 1);
+        pl.rows_per_warp = (t.width >= 1 && t.width <= 32) ? t.width : (s <= 64 ? 4 : 1);
+        pl.minb = 1;
     }
     return pl;
 }
 
-cudaError_t launch_spmm(SpmmParams p, const Plan& plan, cudaStream_t st) {
+cudaError_t launch_spmm(SpmmParams p, const Plan& plan, const Tune& t, cudaStream_t st) {
     if (p.n_rows <= 0) return cudaSuccess;
     p.c_vec = plan.c_vec ? 1 : 0;
     if (plan.tma) return dispatch_tma(p, plan, st);
-    if (plan.cpasync) return launch_cpasync(p, plan, st);
+    if (plan.cpasync) return launch_cpasync(p, plan, t, st);
     switch (plan.vec) {
         case 4: return dispatch_vec<4>(p, plan, st);
         case 2: return dispatch_vec<2>(p, plan, st);
@@ -1087,9 +1074,9 @@ cudaError_t launch_spmm(SpmmParams p, const Plan& plan, cudaStream_t st) {
 }
 
 cudaError_t launch_sample_count_only(const int64_t* rowptr, int64_t n, int32_t s, int64_t* s_rowptr,
-                                     cudaStream_t st) {
+                                     cudaStream_t st, WsHeader* hdr) {
     const int64_t blocks = (n + 1 + 255) / 256;
-    sample_count<<<(unsigned)(blocks > 0 ? blocks : 1), 256, 0, st>>>(rowptr, n, s, s_rowptr);
+    sample_count<<<(unsigned)(blocks > 0 ? blocks : 1), 256, 0, st>>>(rowptr, n, s, s_rowptr, hdr);
     return cudaGetLastError();
 }
 
@@ -1114,12 +1101,13 @@ cudaError_t launch_sample_materialize(const int64_t* rowptr, int64_t nnz_base, c
                                       const float* val, int64_t n, int32_t s, int32_t strategy,
                                       uint64_t seed, int64_t row_base, uint32_t prime,
                                       const int64_t* s_rowptr, int32_t* s_colind, float* s_val,
-                                      int64_t* s_pos, cudaStream_t st, int64_t cap) {
+                                      int64_t* s_pos, cudaStream_t st, int64_t cap, WsHeader* hdr,
+                                      uint64_t sig) {
     if (n <= 0) return cudaSuccess;
     const int64_t blocks = (n + kWarps - 1) / kWarps;
     sample_materialize<<<(unsigned)blocks, kThreads, 0, st>>>(rowptr, nnz_base, colind, val, n, s,
                                                                strategy, seed, row_base, prime,
-                                                               s_rowptr, s_colind, s_val, s_pos, cap);
+                                                               s_rowptr, s_colind, s_val, s_pos, cap, hdr, sig);
     return cudaGetLastError();
 }
 

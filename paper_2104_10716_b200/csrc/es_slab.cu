@@ -14,18 +14,18 @@
 // (with S = 2 groups the order of spmm_cpasync_hw, bitwise; DESIGN.md §6 error bound).
 // Also here: the feature-sliced backward (spmm_slab_bwd, NEXT-2).
 #include <cstdint>
-#include <cstdlib>
+#include <type_traits>
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cub/device/device_scan.cuh>
 
 #include "es_device.cuh"
 #include "es_internal.h"
+#include "es_spmm.h"
 
 namespace es {
 namespace {
 
-constexpr int kSlabThreads = 256;
-constexpr int kSlabWarps = kSlabThreads / 32;
 constexpr unsigned kAll = 0xffffffffu;
 
 // 16-B global -> shared copy, zero-filling when src_bytes == 0 (no global read is made): the
@@ -64,16 +64,245 @@ __device__ __forceinline__ float4 lds128(uint32_t addr) {
     return v;
 }
 
-// One warp per row, split into S = 32/G groups of G lanes.  Step u of a 32-slot chunk consumes
-// slots S*u + e (group e = lane / G); lane `sub` = lane % G of a group owns the P 16-B pieces
-// sub + G*q (q < P) of the slice (nv <= G*P <= 16 pieces), so each LDGSTS instruction of a
-// group covers G*16 contiguous bytes.  A narrow last slice uses fewer lanes per slot (more
-// slots per step, fewer steps).  The copy for step u + D is issued right after step u is
-// consumed, into the stage it released.  Per element: group e sums slots j = e (mod S) in slot
-// order (32-slot-chunk partials), then an xor tree over the groups (G = 16: spmm_cpasync_hw's
-// order, bitwise).
-// W warps per CTA (register cap as for MINB 256-thread CTAs per SM): small CTAs free their
-// slot as soon as their few rows are done instead of waiting for the longest of 8 rows.
+// ---- device backstops of the workspace contract (include/es_spmm.h: reuse_sampled, nnz)
+// A row whose slots would end past the workspace capacity, or a call whose expected sampling
+// signature differs from the one the sampling call left in the header, is written as NaN (a
+// loud failure, never a truncated sum) and the reason is ORed into the header's status word.
+__device__ __forceinline__ bool slab_row_guard(const SlabParams& p, int64_t raw_end, bool sig_bad) {
+    const bool over = raw_end > p.cap;
+    if ((over || sig_bad) && p.ws_status && (threadIdx.x & 31) == 0)
+        atomicOr(p.ws_status, (over ? kWsOverflow : 0) | (sig_bad ? kWsSignature : 0));
+    return over || sig_bad;
+}
+
+__device__ __forceinline__ void slab_poison_row(const SlabParams& p, int64_t r) {
+    const float nan = __int_as_float(0x7fc00000);
+    for (int c = threadIdx.x & 31; c < p.w; c += 32) {
+        if (p.n_peers == 0) p.C[r * p.ldc + c] = nan;
+        else
+            for (int q = 0; q < p.n_peers; ++q) p.c_peers[q][(p.row_base + r) * p.ldc + p.col0 + c] = nan;
+    }
+}
+
+// Epilogue of one lane's piece: E consecutive elements starting at slice column `col`
+// (a5: SUM, or MEAN / divisor with IEEE division, k = 0 -> 0), 16-B stores where C allows.
+template <int E>
+__device__ __forceinline__ void slab_store_piece(const SlabParams& p, int64_t r, int col, const float* tot,
+                                                 int64_t div, uint64_t pol) {
+#pragma unroll
+    for (int h4 = 0; h4 < E / 4; ++h4) {
+        const int c0 = col + 4 * h4;
+        const int rem = p.w - c0;
+        if (rem <= 0) break;
+        float res[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const float t = tot[4 * h4 + c];
+            res[c] = p.reduce == kMean ? (div > 0 ? __fdiv_rn(t, (float)div) : 0.0f) : t;
+        }
+        auto put = [&](float* dst) {
+            if (p.c_vec && rem >= 4) st_stream4(dst, res, pol);
+            else
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    if (c < rem) st_stream(dst + c, res[c], pol);
+        };
+        if (p.n_peers == 0) {
+            put(p.C + r * p.ldc + c0);
+        } else {                                     // fused all-gather: every rank's C (NEXT-1)
+            const int64_t off = (p.row_base + r) * p.ldc + p.col0 + c0;
+            for (int q = 0; q < p.n_peers; ++q) put(p.c_peers[q] + off);
+        }
+    }
+}
+
+// Slots [beg, end) of local row r (k_i of them), the guards applied.  Returns false when the
+// warp has nothing to compute (guard tripped: the row was poisoned).
+__device__ __forceinline__ bool slab_row_slots(const SlabParams& p, int64_t r, int64_t& beg, int32_t& k) {
+    const uint64_t pol = policy_evict_first();
+    beg = ld_stream(p.s_rowptr + r, pol) - p.slot_base;
+    int64_t end = ld_stream(p.s_rowptr + r + 1, pol) - p.slot_base;
+    if (p.direct_s > 0 && end - beg > p.direct_s) end = beg + p.direct_s;   // Bucket: first s of the row
+    const bool sig_bad = p.ws_sig != nullptr && *p.ws_sig != p.sig;
+    if (slab_row_guard(p, end, sig_bad)) {
+        slab_poison_row(p, r);
+        return false;
+    }
+    k = end > beg ? (int32_t)(end - beg) : 0;
+    return true;
+}
+
+// ---------------------------------------------------------------- register-direct slab kernel
+// The default slab kernel.  One warp per row, split into S = 32/G groups of G
+// lanes; step u of a 32-slot chunk consumes slots S*u + e (group e = lane / G).  Lane `sub` of
+// a group owns the P 32-byte pieces sub + G*q of the 256-byte slab row and gathers each with
+// ONE 256-bit load (SASS LDG.E...256) straight into registers: no shared memory, so every B
+// byte crosses the L1 data path once (the shared-memory ring wrote it with LDGSTS and read it
+// back with LDS: two crossings, the measured limiter of that kernel).  The loads of step u + D
+// are issued right after step u is consumed into the D-deep register ring it released; slots
+// past k_i (and pieces past the slice) are zero-filled, so they add exactly +0.
+// Per element: group e sums slots j = e (mod S) in slot order with 32-slot-chunk partials,
+// then an xor tree over the groups -- the order of the shared-memory ring with the same G
+// (bitwise; tested), inside the DESIGN.md §6 bound.
+template <bool BF16> struct Piece32;
+template <> struct Piece32<false> {              // 8 fp32
+    static constexpr int kElems = 8;
+    __device__ __forceinline__ static void widen(const uint32_t* w, float* out) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) out[i] = __uint_as_float(w[i]);
+    }
+};
+template <> struct Piece32<true> {               // 16 bf16, widened exactly to fp32 (NEXT-4)
+    static constexpr int kElems = 16;
+    __device__ __forceinline__ static void widen(const uint32_t* w, float* out) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            out[2 * i] = __uint_as_float(w[i] << 16);
+            out[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+        }
+    }
+};
+
+// 256-bit gather of one 32-B piece when `on` (CACHE 0: L1::no_allocate; 1: L1-allocating, so hot
+// B rows can hit in L1 across the warps of an SM).  The predicate lives inside the asm and the
+// registers are in/out operands: a predicated-off load leaves them as they were, so the ring's
+// registers are the load's destination (no moves).
+template <int CACHE>
+__device__ __forceinline__ void ld256(const void* src, uint32_t* w, bool on) {
+    if constexpr (CACHE == 0)
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %9, 0;\n\t"
+                     "@p ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n\t}"
+                     : "+r"(w[0]), "+r"(w[1]), "+r"(w[2]), "+r"(w[3]), "+r"(w[4]), "+r"(w[5]), "+r"(w[6]),
+                       "+r"(w[7])
+                     : "l"(src), "r"((int)on));
+    else
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %9, 0;\n\t"
+                     "@p ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n\t}"
+                     : "+r"(w[0]), "+r"(w[1]), "+r"(w[2]), "+r"(w[3]), "+r"(w[4]), "+r"(w[5]), "+r"(w[6]),
+                       "+r"(w[7])
+                     : "l"(src), "r"((int)on));
+}
+
+template <int G, int P, int D, int W, int MINW, bool BF16, bool FULL, int CACHE>
+__global__ void __launch_bounds__(32 * W, MINW / W)
+spmm_slab_ldg(const SlabParams p) {
+    constexpr int E = Piece32<BF16>::kElems;
+    constexpr int S = 32 / G;            // slots per step
+    constexpr int U = G;                 // steps per 32-slot chunk
+    static_assert((G == 2 || G == 4 || G == 8) && G * P <= 8, "lanes x pieces per slot (8 pieces = 256 B)");
+    static_assert(D >= 2 && U % D == 0, "ring depth must divide the steps of a chunk");
+    const int lane = threadIdx.x & 31;
+    const int e = lane / G, sub = lane % G;
+    const int64_t r = (int64_t)blockIdx.x * W + (threadIdx.x >> 5);
+    if (r >= p.n_rows) return;
+    int64_t beg;
+    int32_t k;
+    if (!slab_row_slots(p, r, beg, k)) return;
+    const char* bl = reinterpret_cast<const char*>(p.B) + sub * 32;
+    const uint32_t row_bytes = (uint32_t)(p.ldb * (BF16 ? 2 : 4));
+
+    // Slots past k_i are neither loaded nor accumulated (predicated loads and FMAs: no zero
+    // fill, so no register moves); pieces past a narrow slice are not loaded and their
+    // accumulators are never stored (the xor tree only combines equal pieces).
+    uint32_t buf[D][P][8];
+#pragma unroll
+    for (int d = 0; d < D; ++d)
+#pragma unroll
+        for (int q = 0; q < P; ++q)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) buf[d][q][i] = 0u;
+    auto issue = [&](int d, int32_t col, bool valid) {
+        const char* src = bl + (uint64_t)(uint32_t)col * row_bytes;
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            const bool on = FULL ? valid : (valid && sub + G * q < p.nv);
+            ld256<CACHE>(src + q * G * 32, buf[d][q], on);
+        }
+    };
+    auto load_pair = [&](int64_t j, int32_t& c, float& a) {      // slot j of the row (coalesced)
+        const uint64_t pol = policy_evict_first();
+        c = ld_stream(p.s_colind + beg + j, pol);
+        a = p.s_val ? ld_stream(p.s_val + beg + j, pol) : 1.0f;
+    };
+
+    int32_t c0 = 0, c1 = 0;
+    float a0 = 0.0f, a1 = 0.0f;
+    if (lane < k) load_pair(lane, c0, a0);
+    if (32 + lane < k) load_pair(32 + lane, c1, a1);
+#pragma unroll
+    for (int t = 0; t < D; ++t) issue(t, __shfl_sync(kAll, c0, S * t + e), S * t + e < k);
+    float part[P][E], tot[P][E];
+#pragma unroll
+    for (int q = 0; q < P; ++q)
+#pragma unroll
+        for (int c = 0; c < E; ++c) { part[q][c] = 0.0f; tot[q][c] = 0.0f; }
+    // one 32-slot chunk: full chunks (all slots valid, warp-uniform test) run branch-free; only a
+    // row's last, partial chunk predicates its FMAs on the slot being < k
+    auto chunk = [&](int32_t j0, auto partial) {
+#pragma unroll 1
+        for (int u0 = 0; u0 < U; u0 += D) {
+#pragma unroll
+            for (int d = 0; d < D; ++d) {                        // step u = u0 + d, ring slot d
+                const int u = u0 + d;
+                const float av = __shfl_sync(kAll, a0, S * u + e);
+                if (!decltype(partial)::value || j0 + S * u + e < k) {
+#pragma unroll
+                    for (int q = 0; q < P; ++q) {
+                        float x[E];
+                        Piece32<BF16>::widen(buf[d][q], x);
+#pragma unroll
+                        for (int c = 0; c < E; ++c) part[q][c] = fmaf(av, x[c], part[q][c]);
+                    }
+                }
+                const int tn = u + D;                            // refill: step u + D
+                const int32_t cn = __shfl_sync(kAll, tn < U ? c0 : c1, (S * tn + e) & 31);
+                issue(d, cn, j0 + S * tn + e < k);
+            }
+        }
+    };
+    for (int32_t j0 = 0; j0 < k; j0 += 32) {
+        if (j0 + 32 <= k) chunk(j0, std::false_type{});
+        else chunk(j0, std::true_type{});
+#pragma unroll
+        for (int q = 0; q < P; ++q)
+#pragma unroll
+            for (int c = 0; c < E; ++c) { tot[q][c] += part[q][c]; part[q][c] = 0.0f; }
+        c0 = c1;
+        a0 = a1;
+        c1 = 0;
+        a1 = 0.0f;
+        if (j0 + 64 + lane < k) load_pair(j0 + 64 + lane, c1, a1);
+    }
+    const uint64_t pol_a = policy_evict_first();
+    int64_t div = k;
+    if (p.reduce == kMean && p.mean_by_degree)
+        div = ld_stream(p.rowptr + r + 1, pol_a) - ld_stream(p.rowptr + r, pol_a);
+#pragma unroll
+    for (int o = G; o < 32; o <<= 1)
+#pragma unroll
+        for (int q = 0; q < P; ++q)
+#pragma unroll
+            for (int c = 0; c < E; ++c) {
+                const float other = __shfl_xor_sync(kAll, tot[q][c], o);
+                tot[q][c] = (lane & o) ? other + tot[q][c] : tot[q][c] + other;
+            }
+    if (e == 0) {
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            const int piece = sub + G * q;
+            if (FULL || piece < p.nv) slab_store_piece<E>(p, r, piece * E, tot[q], div, pol_a);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- shared-memory ring slab kernel
+// The round-1 kernel, kept for B rows that are 16-B but not 32-B aligned and for A/B
+// measurement (ES_KERNEL_SLAB_SMEM).  Same mapping with 16-B pieces staged through a per-warp
+// cp.async ring: lane `sub` owns the P pieces sub + G*q (nv <= G*P <= 16), each LDGSTS
+// instruction of a group covers G*16 contiguous bytes.  Ring layout [warps][D][P][S][G]: the
+// 8 lanes of a quarter-warp always touch 128 contiguous bytes (conflict-free for every G).
+// Per element: group e sums slots j = e (mod S) in slot order (32-slot-chunk partials), then
+// an xor tree over the groups (G = 16: spmm_cpasync_hw's order, bitwise).
 template <int G, int P, int D, int MINB, bool FULL, int W, bool BF16 = false>
 __global__ void __launch_bounds__(32 * W, MINB * 8 / W)
 spmm_slab(const SlabParams p) {
@@ -83,18 +312,16 @@ spmm_slab(const SlabParams p) {
     static_assert((G == 2 || G == 4 || G == 8 || G == 16) && G * P <= 16, "lanes x pieces per slot");
     static_assert(D >= 2 && U % D == 0, "ring depth must divide the steps of a chunk");
     constexpr int kStage = 32 * P;                               // float4 per warp stage
-    extern __shared__ __align__(16) float4 slab_ring[];          // [warps][D][S][P][G]
+    extern __shared__ __align__(16) float4 slab_ring[];          // [warps][D][P][S][G]
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int e = lane / G, sub = lane % G;
     const int64_t r = (int64_t)blockIdx.x * W + warp;
     if (r >= p.n_rows) return;
-    const int64_t beg = ld_stream(p.s_rowptr + r, policy_evict_first()) - p.slot_base;
-    int64_t end = ld_stream(p.s_rowptr + r + 1, policy_evict_first()) - p.slot_base;
-    if (end > p.cap) end = p.cap;                                // workspace bound (never read past)
-    if (p.direct_s > 0 && end - beg > p.direct_s) end = beg + p.direct_s;   // Bucket: first s of the row
-    const int32_t k = end > beg ? (int32_t)(end - beg) : 0;
-    const uint32_t my_s = smem_u32(slab_ring + (size_t)warp * D * kStage + e * (P * G) + sub);
+    int64_t beg;
+    int32_t k;
+    if (!slab_row_slots(p, r, beg, k)) return;
+    const uint32_t my_s = smem_u32(slab_ring + (size_t)warp * D * kStage + e * G + sub);
     const char* bl = reinterpret_cast<const char*>(p.B) + sub * 16;
     const uint32_t row_bytes = (uint32_t)(p.ldb * (BF16 ? 2 : 4));
 
@@ -104,7 +331,7 @@ spmm_slab(const SlabParams p) {
 #pragma unroll
         for (int q = 0; q < P; ++q) {
             const bool on = FULL ? valid : (valid && sub + G * q < p.nv);
-            cp_async16_zfill(my_s + (stage * kStage + q * G) * 16, src + q * G * 16, on ? 16u : 0u);
+            cp_async16_zfill(my_s + (stage * kStage + q * 32) * 16, src + q * G * 16, on ? 16u : 0u);
         }
     };
     auto load_pair = [&](int64_t j, int32_t& c, float& a) {      // slot j of the row (coalesced)
@@ -140,7 +367,7 @@ spmm_slab(const SlabParams p) {
 #pragma unroll
                 for (int q = 0; q < P; ++q) {
                     float x[E];
-                    SlabPiece<BF16>::widen(lds128(my_s + (d * kStage + q * G) * 16), x);
+                    SlabPiece<BF16>::widen(lds128(my_s + (d * kStage + q * 32) * 16), x);
 #pragma unroll
                     for (int c = 0; c < E; ++c) part[q][c] = fmaf(av, x[c], part[q][c]);
                 }
@@ -180,35 +407,150 @@ spmm_slab(const SlabParams p) {
 #pragma unroll
         for (int q = 0; q < P; ++q) {
             const int piece = sub + G * q;
-            if (FULL || piece < p.nv) {
-#pragma unroll
-                for (int h4 = 0; h4 < E / 4; ++h4) {                 // 4 output floats at a time
-                    float res[4];
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        const float t = tot[q][4 * h4 + c];
-                        res[c] = p.reduce == kMean ? (div > 0 ? __fdiv_rn(t, (float)div) : 0.0f) : t;
-                    }
-                    const int col = piece * E + 4 * h4;              // first output column
-                    const int rem = p.w - col;                       // valid floats from there
-                    auto put = [&](float* dst) {
-                        if (p.c_vec && rem >= 4) st_stream4(dst, res, pol_a);
-                        else
-#pragma unroll
-                            for (int c = 0; c < 4; ++c)
-                                if (c < rem) st_stream(dst + c, res[c], pol_a);
-                    };
-                    if (rem <= 0) continue;
-                    if (p.n_peers == 0) {
-                        put(p.C + r * p.ldc + col);
-                    } else {                                     // fused all-gather: every rank's C
-                        const int64_t off = (p.row_base + r) * p.ldc + p.col0 + col;
-                        for (int q2 = 0; q2 < p.n_peers; ++q2) put(p.c_peers[q2] + off);
-                    }
-                }
-            }
+            if (FULL || piece < p.nv) slab_store_piece<E>(p, r, piece * E, tot[q], div, pol_a);
         }
     }
+}
+
+// ---------------------------------------------------------------- TMA gather4 slab kernel
+// One elected lane per warp feeds a D-stage shared-memory ring with TMA tile::gather4 copies
+// (SASS UTMALDG.2D.GATHER4): ONE instruction moves the 256-B slab rows of 4 slots (1 KB, a whole
+// step) from L2 into the stage, completion counted by the stage's mbarrier (expect_tx).  The
+// LSU no longer writes shared memory (the LDGSTS half of the shared-memory ring's wavefronts);
+// the consumer is that kernel's: 8 lanes x 2 LDS.128 per slot, group e = slot 4u + e.  Slots
+// past k_i gather row n_cols (out of bounds: the TMA zero-fills without a memory access) and
+// columns past F are zero-filled the same way, so the passes are branch-free.  Same order as
+// spmm_slab<8, 2, ...> (bitwise).
+template <int D, int W, int MINB, bool BF16>
+__global__ void __launch_bounds__(32 * W, MINB)
+spmm_slab_tma(const __grid_constant__ CUtensorMap tmap, const SlabParams p, int32_t c0_coord, int32_t n_cols) {
+    constexpr int G = 8, P = 2, S = 4, U = 8;
+    constexpr int E = SlabPiece<BF16>::kElems;
+    constexpr uint32_t kStageBytes = 1024;
+    static_assert(U % D == 0, "ring depth must divide the steps of a chunk");
+    extern __shared__ __align__(1024) unsigned char tma_smem[];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int e = lane / G, sub = lane % G;
+    const int64_t r = (int64_t)blockIdx.x * W + warp;
+    unsigned char* ring = tma_smem + (size_t)warp * D * kStageBytes;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(tma_smem + (size_t)W * D * kStageBytes) + warp * D;
+    if (r >= p.n_rows) return;
+    int64_t beg;
+    int32_t k;
+    if (!slab_row_slots(p, r, beg, k)) return;
+    if (lane == 0) {
+        for (int d = 0; d < D; ++d) mbar_init(&bar[d], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    const uint32_t ring_s = smem_u32(ring);
+    const uint32_t my_s = ring_s + e * 256 + sub * 16;
+    auto load_pair = [&](int64_t j, int32_t& c, float& a) {      // slot j of the row (coalesced)
+        const uint64_t pol = policy_evict_first();
+        c = ld_stream(p.s_colind + beg + j, pol);
+        a = p.s_val ? ld_stream(p.s_val + beg + j, pol) : 1.0f;
+    };
+    // step t's 4 rows (slots 4t .. 4t+3 of the current / next chunk); warp-collective
+    auto issue = [&](int d, int32_t src_c, int32_t j_first) {
+        int32_t rows[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int32_t c = __shfl_sync(kAll, src_c, (j_first + i) & 31);
+            rows[i] = j_first + i < k ? c : n_cols;                 // OOB row: zero fill
+        }
+        if (lane == 0) {
+            mbar_arrive_expect_tx(&bar[d], kStageBytes);
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+                :: "r"(ring_s + d * kStageBytes), "l"(&tmap), "r"(c0_coord), "r"(rows[0]), "r"(rows[1]),
+                   "r"(rows[2]), "r"(rows[3]), "r"(smem_u32(&bar[d])) : "memory");
+        }
+    };
+    (void)beg;
+    int32_t c0 = 0, c1 = 0;
+    float a0 = 0.0f, a1 = 0.0f;
+    if (lane < k) load_pair(lane, c0, a0);
+    if (32 + lane < k) load_pair(32 + lane, c1, a1);
+    // issue(d, cols, first slot index relative to the row): the slot's column lives in lane
+    // (slot & 31) of c0 (this chunk) or c1 (next chunk)
+#pragma unroll
+    for (int t = 0; t < D; ++t) issue(t, c0, S * t);
+    float part[P][E], tot[P][E];
+#pragma unroll
+    for (int q = 0; q < P; ++q)
+#pragma unroll
+        for (int c = 0; c < E; ++c) { part[q][c] = 0.0f; tot[q][c] = 0.0f; }
+    uint32_t phase = 0;                  // bit d: parity of stage d's next completion
+    for (int32_t j0 = 0; j0 < k; j0 += 32) {
+#pragma unroll 1
+        for (int u0 = 0; u0 < U; u0 += D) {
+#pragma unroll
+            for (int d = 0; d < D; ++d) {                        // step u = u0 + d, stage d
+                const int u = u0 + d;
+                mbar_wait(&bar[d], (phase >> d) & 1u);
+                phase ^= 1u << d;
+                const float av = __shfl_sync(kAll, a0, S * u + e);
+#pragma unroll
+                for (int q = 0; q < P; ++q) {
+                    float x[E];
+                    SlabPiece<BF16>::widen(lds128(my_s + d * kStageBytes + q * 128), x);
+#pragma unroll
+                    for (int c = 0; c < E; ++c) part[q][c] = fmaf(av, x[c], part[q][c]);
+                }
+                __syncwarp();                                    // stage d fully read
+                const int tn = u + D;                            // refill: step u + D
+                issue(d, tn < U ? c0 : c1, j0 + S * tn);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < P; ++q)
+#pragma unroll
+            for (int c = 0; c < E; ++c) { tot[q][c] += part[q][c]; part[q][c] = 0.0f; }
+        c0 = c1;
+        a0 = a1;
+        c1 = 0;
+        a1 = 0.0f;
+        if (j0 + 64 + lane < k) load_pair(j0 + 64 + lane, c1, a1);
+    }
+    // drain: the D copies issued past the row's end (all zero-filled) must land before exit
+#pragma unroll
+    for (int d = 0; d < D; ++d) mbar_wait(&bar[d], (phase >> d) & 1u);
+    const uint64_t pol_a = policy_evict_first();
+    int64_t div = k;
+    if (p.reduce == kMean && p.mean_by_degree)
+        div = ld_stream(p.rowptr + r + 1, pol_a) - ld_stream(p.rowptr + r, pol_a);
+#pragma unroll
+    for (int o = G; o < 32; o <<= 1)
+#pragma unroll
+        for (int q = 0; q < P; ++q)
+#pragma unroll
+            for (int c = 0; c < E; ++c) {
+                const float other = __shfl_xor_sync(kAll, tot[q][c], o);
+                tot[q][c] = (lane & o) ? other + tot[q][c] : tot[q][c] + other;
+            }
+    if (e == 0) {
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            const int piece = sub + G * q;
+            if (piece < p.nv) slab_store_piece<E>(p, r, piece * E, tot[q], div, pol_a);
+        }
+    }
+}
+
+template <int D, int W, int MINB, bool BF16>
+cudaError_t launch_tma_slab_w(const CUtensorMap& tm, const SlabParams& p, int32_t c0, int32_t n_cols,
+                              cudaStream_t st) {
+    const int64_t blocks = (p.n_rows + W - 1) / W;
+    const size_t smem = (size_t)W * D * 1024 + (size_t)W * D * 8;
+    auto k = spmm_slab_tma<D, W, MINB, BF16>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    k<<<(unsigned)blocks, 32 * W, smem, st>>>(tm, p, c0, n_cols);
+    return cudaGetLastError();
 }
 
 template <int G, int P, int D, int MINB, int W, bool BF16 = false>
@@ -225,13 +567,30 @@ cudaError_t launch_slab_w(const SlabParams& p, cudaStream_t st) {
 }
 
 template <int G, int D, int MINB, int P = 16 / G>
-cudaError_t launch_slab_k(const SlabParams& p, cudaStream_t st) {
-    const char* we = getenv("ES_SPMM_SLAB_CTA_WARPS");     // tuning: warps per CTA (default 4)
-    const int w = we ? atoi(we) : 4;
-    if (w == 1) return launch_slab_w<G, P, D, MINB, 1>(p, st);
-    if (w == 2) return launch_slab_w<G, P, D, MINB, 2>(p, st);
-    if (w == 8) return launch_slab_w<G, P, D, MINB, 8>(p, st);
+cudaError_t launch_slab_k(const SlabParams& p, int cta_warps, cudaStream_t st) {
+    if (cta_warps == 1) return launch_slab_w<G, P, D, MINB, 1>(p, st);
+    if (cta_warps == 2) return launch_slab_w<G, P, D, MINB, 2>(p, st);
+    if (cta_warps == 8) return launch_slab_w<G, P, D, MINB, 8>(p, st);
     return launch_slab_w<G, P, D, MINB, 4>(p, st);
+}
+
+// MINW: min resident warps per SM the register cap is set for
+template <int G, int P, int D, int W, int MINW, bool BF16>
+cudaError_t launch_ldg_w(const SlabParams& p, int cache, cudaStream_t st) {
+    const int64_t blocks = (p.n_rows + W - 1) / W;
+    const bool full = p.nv == G * P;
+    auto k = full ? (cache ? spmm_slab_ldg<G, P, D, W, MINW, BF16, true, 1> : spmm_slab_ldg<G, P, D, W, MINW, BF16, true, 0>)
+                  : (cache ? spmm_slab_ldg<G, P, D, W, MINW, BF16, false, 1>
+                           : spmm_slab_ldg<G, P, D, W, MINW, BF16, false, 0>);
+    k<<<(unsigned)blocks, 32 * W, 0, st>>>(p);
+    return cudaGetLastError();
+}
+
+template <int G, int P, int D, int MINW, bool BF16>
+cudaError_t launch_ldg_k(const SlabParams& p, const Tune& t, cudaStream_t st) {
+    const int cache = t.variant & 1;
+    if (t.cta_warps == 2) return launch_ldg_w<G, P, D, 2, MINW, BF16>(p, cache, st);
+    return launch_ldg_w<G, P, D, 4, MINW, BF16>(p, cache, st);
 }
 
 // ---------------------------------------------------------------- backward (NEXT-2), slab path
@@ -252,8 +611,9 @@ spmm_slab_bwd(const SlabParams p, const float* __restrict__ dC, float* __restric
     const uint64_t pol_a = policy_evict_first();
     const int64_t beg = ld_stream(p.s_rowptr + r, pol_a) - p.slot_base;
     int64_t end = ld_stream(p.s_rowptr + r + 1, pol_a) - p.slot_base;
-    if (end > p.cap) end = p.cap;
     if (p.direct_s > 0 && end - beg > p.direct_s) end = beg + p.direct_s;
+    const bool sig_bad = p.ws_sig != nullptr && *p.ws_sig != p.sig;
+    if (slab_row_guard(p, end, sig_bad)) return;      // dB is accumulated into: flagged, not poisoned
     const int32_t k = end > beg ? (int32_t)(end - beg) : 0;
     if (k == 0) return;
     float div = (float)k;
@@ -304,35 +664,71 @@ spmm_slab_bwd(const SlabParams p, const float* __restrict__ dC, float* __restric
 
 }  // namespace
 
-// Instantiations: G = 8 (default: 2 pieces per lane, 4 slots per step) or 16; D = 2, 4, 8.
-// MINB = the register cap that does not spill (spilling cp.async kernels trapped on B200,
-// _build.py refuses them).  Measured alternatives (register-staged LDG with every cache
-// operator, cp.async.ca, 4 lanes per slot, a row-stream variant over a padded layout) were
-// all slower: profiles/r01.md "Slab path".
-cudaError_t launch_slab_pass(const SlabParams& p, int lanes_per_slot, int stages, cudaStream_t st) {
+// Slab kernel selection.  Default: the shared-memory ring, G = tune.width (8 default, or 16)
+// lanes x 16-B pieces per slot (profiles/r02.md: it beats the register-direct and the TMA
+// gather4 kernels on every measured config -- they are latency- resp. TMA-rate-bound).
+// ES_KERNEL_SLAB_LDG: the register-direct kernel, 8 lanes x one 32-B piece per slot (4 slots per
+// step) for a full 256-B slice, 4 lanes (8 slots per step) for a slice of <= 4 pieces, 2 lanes for
+// <= 2 -- needs B and its row pitch 32-B aligned (p.b32); ring depth tune.stages (4 default; 2,
+// 8).  The register caps below are the largest that do not spill (spilling cp.async kernels
+// trapped on B200, _build.py refuses them).
+cudaError_t launch_slab_pass(const SlabParams& p, const Tune& t, cudaStream_t st) {
     if (p.n_rows <= 0) return cudaSuccess;
+    const bool ldg = p.b32 && t.kernel == ES_KERNEL_SLAB_LDG;
+    if (ldg) {
+        const int np = p.nv;                 // 32-B pieces in this slice (<= 8)
+        // register caps (MINW resident warps per SM) that do not spill: the D-deep ring holds
+        // D x 8 registers per piece
+        if (p.b_bf16) {
+            if (np <= 2) return launch_ldg_k<2, 1, 2, 24, true>(p, t, st);
+            if (np <= 4) return launch_ldg_k<4, 1, 4, 16, true>(p, t, st);
+            return launch_ldg_k<8, 1, 4, 16, true>(p, t, st);
+        }
+        if (np <= 2) return launch_ldg_k<2, 1, 2, 24, false>(p, t, st);
+        if (np <= 4) return launch_ldg_k<4, 1, 4, 16, false>(p, t, st);
+        if (t.stages == 8) return launch_ldg_k<8, 1, 8, 12, false>(p, t, st);
+        if (t.stages == 2) return launch_ldg_k<8, 1, 2, 24, false>(p, t, st);
+        return launch_ldg_k<8, 1, 4, 16, false>(p, t, st);
+    }
+    const int cw = t.cta_warps;
     if (p.b_bf16) {                      // bf16 B (NEXT-4): 128-element slices, 8 elements per piece
         if (p.nv <= 4) return launch_slab_w<2, 2, 2, 3, 4, true>(p, st);
         if (p.nv <= 8) return launch_slab_w<4, 2, 4, 3, 4, true>(p, st);
-        return lanes_per_slot == 16 ? launch_slab_w<16, 1, 4, 4, 4, true>(p, st)
-                                    : launch_slab_w<8, 2, 4, 3, 4, true>(p, st);
+        return t.width == 16 ? launch_slab_w<16, 1, 4, 4, 4, true>(p, st)
+                             : launch_slab_w<8, 2, 4, 3, 4, true>(p, st);
     }
-    if (lanes_per_slot == 16) {
-        switch (stages) {
-            case 2: return launch_slab_k<16, 2, 5>(p, st);
-            case 8: return launch_slab_k<16, 8, 4>(p, st);
-            default: return launch_slab_k<16, 4, 5>(p, st);
+    if (t.width == 16) {
+        switch (t.stages) {
+            case 2: return launch_slab_k<16, 2, 5>(p, cw, st);
+            case 8: return launch_slab_k<16, 8, 4>(p, cw, st);
+            default: return launch_slab_k<16, 4, 5>(p, cw, st);
         }
     }
     // narrow last slice: 4 lanes x 2 pieces (8 slots per step) for <= 8 pieces, 2 x 2 (16 slots
     // per step) for <= 4 -- half / a quarter of the steps of a full slice
-    if (p.nv <= 4) return launch_slab_k<2, 2, 4, 2>(p, st);
-    if (p.nv <= 8) return launch_slab_k<4, 4, 4, 2>(p, st);
-    switch (stages) {
-        case 2: return launch_slab_k<8, 2, 4>(p, st);
-        case 8: return launch_slab_k<8, 8, 4>(p, st);
-        default: return launch_slab_k<8, 4, 4>(p, st);
+    if (p.nv <= 4) return launch_slab_k<2, 2, 4, 2>(p, cw, st);
+    if (p.nv <= 8) return launch_slab_k<4, 4, 4, 2>(p, cw, st);
+    switch (t.stages) {
+        case 2: return launch_slab_k<8, 2, 4>(p, cw, st);
+        case 8: return launch_slab_k<8, 8, 4>(p, cw, st);
+        default: return launch_slab_k<8, 4, 4>(p, cw, st);
     }
+}
+
+// The TMA gather4 kernel over one slice: column coordinate c0 of the tensor map over all of B
+// (es_abi.cu encodes it once per call).  ring depth tune.stages (4 default; 2, 8), warps per CTA
+// tune.cta_warps (4 default; 2, 8).
+cudaError_t launch_slab_pass_tma(const CUtensorMap& tm, const SlabParams& p, int32_t c0, int32_t n_cols,
+                                 const Tune& t, cudaStream_t st) {
+    if (p.n_rows <= 0) return cudaSuccess;
+    if (p.b_bf16) return launch_tma_slab_w<4, 4, 4, true>(tm, p, c0, n_cols, st);
+    if (t.stages == 2) return t.cta_warps == 8 ? launch_tma_slab_w<2, 8, 4, false>(tm, p, c0, n_cols, st)
+                                               : launch_tma_slab_w<2, 4, 8, false>(tm, p, c0, n_cols, st);
+    if (t.stages == 8) return t.cta_warps == 8 ? launch_tma_slab_w<8, 8, 3, false>(tm, p, c0, n_cols, st)
+                                               : launch_tma_slab_w<8, 4, 6, false>(tm, p, c0, n_cols, st);
+    if (t.cta_warps == 8) return launch_tma_slab_w<4, 8, 4, false>(tm, p, c0, n_cols, st);
+    if (t.cta_warps == 2) return launch_tma_slab_w<4, 2, 16, false>(tm, p, c0, n_cols, st);
+    return launch_tma_slab_w<4, 4, 8, false>(tm, p, c0, n_cols, st);
 }
 
 cudaError_t launch_slab_backward(const SlabParams& p, const float* dC, float* dB, cudaStream_t st) {
@@ -342,6 +738,33 @@ cudaError_t launch_slab_backward(const SlabParams& p, const float* dC, float* dB
     return cudaGetLastError();
 }
 
+bool encode_b_tensor_map(CUtensorMap* tm, const void* B, int64_t F, int64_t ldb, int64_t n_cols, bool bf16) {
+    using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    // resolved once (thread-safe static initialisation); immutable afterwards
+    static const Encode encode = []() -> Encode {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return nullptr;
+        return reinterpret_cast<Encode>(fn);
+    }();
+    const int64_t esz = bf16 ? 2 : 4;
+    if (!encode || reinterpret_cast<uintptr_t>(B) % 16 != 0 || (ldb * esz) % 16 != 0 || n_cols < 1 ||
+        n_cols >= (int64_t)1 << 31 || F < 1)
+        return false;
+    const cuuint64_t dims[2] = {(cuuint64_t)F, (cuuint64_t)n_cols};   // columns >= F: zero fill
+    const cuuint64_t strides[1] = {(cuuint64_t)(ldb * esz)};
+    const cuuint32_t box[2] = {(cuuint32_t)(256 / esz), 1};          // one 256-B slab row
+    const cuuint32_t estr[2] = {1, 1};
+    return encode(tm, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                  const_cast<void*>(B), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 size_t slab_scan_temp_bytes(int64_t n) {
     size_t temp = 0;
     if (n > 0) cub::DeviceScan::InclusiveSum(nullptr, temp, (int64_t*)nullptr, (int64_t*)nullptr, n);
@@ -349,8 +772,8 @@ size_t slab_scan_temp_bytes(int64_t n) {
 }
 
 cudaError_t launch_slab_count(const int64_t* rowptr, int64_t n, int32_t s, int64_t* s_rowptr, void* temp,
-                              size_t temp_bytes, cudaStream_t st, int* launches) {
-    cudaError_t err = launch_sample_count_only(rowptr, n, s, s_rowptr, st);
+                              size_t temp_bytes, cudaStream_t st, int* launches, WsHeader* hdr) {
+    cudaError_t err = launch_sample_count_only(rowptr, n, s, s_rowptr, st, hdr);
     ++*launches;
     if (err != cudaSuccess || n == 0) return err;
     err = cub::DeviceScan::InclusiveSum(temp, temp_bytes, s_rowptr + 1, s_rowptr + 1, n, st);

@@ -51,8 +51,10 @@ def forward(model: str, rowptr, colind, val, X, layers, s: int, strategy: int, s
     def aggregate(rp, ci, v, B, s_, strat, seed_, reduce, F=None):
         """The sampled SpMM through the library's plan (slab path + slot reuse with a workspace)."""
         F = B.shape[1] if F is None else F
-        if workspace is not None and es_spmm_workspace_bytes(n_rows, B.shape[0], nnz, F, B.shape[1], s_,
-                                                             v is not None) > 0:
+        # the slab path runs (and leaves slots to reuse) only where the library asks for a
+        # workspace AND B's rows are 16-B aligned; a reuse the library cannot honour is an error
+        if (workspace is not None and B.data_ptr() % 16 == 0
+                and es_spmm_workspace_bytes(n_rows, B.shape[0], nnz, F, B.shape[1], s_, v is not None) > 0):
             out = es_spmm_run_ex(rp, ci, v, B, s_, strat, seed_, reduce, F=F, workspace=workspace,
                                  reuse_sampled=sampled[0])
             sampled[0] = True

@@ -31,10 +31,9 @@ def main():
     dC = torch.from_numpy(synth.dense(n, F, 77, ld=ldb)).to(dev)
     dB = torch.zeros((n, ldb), dtype=torch.float32, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    os.environ["ES_SPMM_SLAB"] = "1"
-    ws = es.es_spmm_workspace(n, n, len(colind), F, ldb, s, True, device=dev)
+    ws = es.es_spmm_workspace(n, n, len(colind), F, ldb, s, True, device=dev, kernel="slab")
     B = torch.from_numpy(synth.dense(n, F, 5, ld=ldb)).to(dev)
-    es.es_spmm_run_ex(rp, ci, va, B, s, 2, 0, 1, F=F, workspace=ws)     # forward: samples into ws
+    es.es_spmm_run_ex(rp, ci, va, B, s, 2, 0, 1, F=F, workspace=ws, kernel="slab")   # forward: samples into ws
 
     def timed(fn, reps=6):
         ts = []

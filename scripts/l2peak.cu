@@ -1,0 +1,145 @@
+// L2 ceilings on this B200 (roofline denominators for L2-resident gathers; tuning evidence, not
+// part of the library).  Prints one JSON line per probe.
+//   stream      : every thread streams float4 (ld.global.cg, L2 only) over a footprint of X bytes,
+//                 R times: the L2 streaming read rate -- bench.py's roofline peak for the slab
+//                 passes and L2-resident fused configs (profiles/l2_peak.json).
+//   gather_ldg  : random 256-B rows of an X-byte slab, 8 lanes x 2 float4 per row, U rows in
+//                 flight per lane group (register-direct gathers).
+//   gather_smem : the same rows through a per-warp cp.async ring (LDGSTS) read back with LDS --
+//                 the shared-memory-staged pattern of es::spmm_slab at ideal row lengths.
+// Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o l2peak scripts/l2peak.cu
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cuda_runtime.h>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { \
+  printf("{\"error\":\"%s at %d\"}\n", cudaGetErrorString(e), __LINE__); exit(1);} } while (0)
+
+__device__ __forceinline__ uint32_t hash32(uint64_t x) {
+  x ^= x >> 30; x *= 0xBF58476D1CE4E5B9ull; x ^= x >> 27; x *= 0x94D049BB133111EBull; x ^= x >> 31;
+  return (uint32_t)x;
+}
+
+__global__ void stream_read(const float4* __restrict__ p, size_t n4, int reps, float* sink) {
+  float acc = 0.f;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (int r = 0; r < reps; ++r) {
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + 3 * stride < n4; i += 4 * stride) {
+      float4 a = __ldcg(p + i), b = __ldcg(p + i + stride), c = __ldcg(p + i + 2 * stride),
+             d = __ldcg(p + i + 3 * stride);
+      acc += a.x + b.y + c.z + d.w;
+    }
+    for (; i < n4; i += stride) { float4 a = __ldcg(p + i); acc += a.x; }
+  }
+  if (acc == 1234.5f) *sink = acc;
+}
+
+// each warp: rows g = warp*steps*4 + 4t + e (group e = lane/8), lane sub = lane%8 owns float4 sub, sub+8
+template <int U>
+__global__ void gather_ldg(const float4* __restrict__ slab, uint32_t nrows, long steps, float* sink) {
+  const int lane = threadIdx.x & 31, e = lane >> 3, sub = lane & 7;
+  const long warp = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  float acc = 0.f;
+  for (long t = 0; t < steps; t += U) {
+    float4 v[U][2];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t row = hash32((uint64_t)(warp * steps + t + u) * 4 + e) % nrows;
+      v[u][0] = __ldcg(slab + (size_t)row * 16 + sub);
+      v[u][1] = __ldcg(slab + (size_t)row * 16 + sub + 8);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc += v[u][0].x + v[u][1].w;
+  }
+  if (acc == 1234.5f) *sink = acc;
+}
+
+template <int D>
+__global__ void gather_smem(const float4* __restrict__ slab, uint32_t nrows, long steps, float* sink) {
+  extern __shared__ float4 ring[];                       // [warps][D][4 rows][16]
+  const int lane = threadIdx.x & 31, e = lane >> 3, sub = lane & 7, w = threadIdx.x >> 5;
+  const long warp = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  float4* my = ring + (size_t)w * D * 64 + e * 16 + sub;
+  auto issue = [&](int d, long t) {
+    const uint32_t row = hash32((uint64_t)(warp * steps + t) * 4 + e) % nrows;
+    const float4* src = slab + (size_t)row * 16 + sub;
+    const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(my + d * 64);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(s0), "l"(src) : "memory");
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(s0 + 128), "l"(src + 8) : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  float acc = 0.f;
+#pragma unroll
+  for (int d = 0; d < D; ++d) issue(d, d);
+  for (long t = 0; t < steps; t += D) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      asm volatile("cp.async.wait_group %0;" :: "n"(D - 1) : "memory");
+      const float4 a = my[d * 64], b = my[d * 64 + 8];
+      acc += a.x + b.w;
+      issue(d, t + d + D);
+    }
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  if (acc == 1234.5f) *sink = acc;
+}
+
+int main() {
+  int nsm = 148, dev = 0, sm_clk = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  CK(cudaDeviceGetAttribute(&sm_clk, cudaDevAttrClockRate, dev));
+  const size_t maxbytes = (size_t)1 << 30;
+  float4* buf;
+  float* sink;
+  CK(cudaMalloc(&buf, maxbytes));
+  CK(cudaMalloc(&sink, 4));
+  CK(cudaMemset(buf, 0, maxbytes));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  auto time_best = [&](auto launch, int reps) {
+    float best = 1e30f;
+    launch();                                             // warm
+    for (int i = 0; i < reps; ++i) {
+      CK(cudaEventRecord(e0));
+      launch();
+      CK(cudaEventRecord(e1));
+      CK(cudaEventSynchronize(e1));
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (ms < best) best = ms;
+    }
+    return best;
+  };
+  const size_t foot[] = {32u << 20, 48u << 20, 60u << 20, 64u << 20, 80u << 20, 96u << 20, 112u << 20,
+                         128u << 20, (size_t)1 << 30};
+  for (size_t X : foot) {
+    const size_t n4 = X / 16;
+    const int reps = (int)(((size_t)8 << 30) / X) > 0 ? (int)(((size_t)8 << 30) / X) : 1;
+    const int grid = nsm * 4;
+    const float ms = time_best([&] { stream_read<<<grid, 512>>>(buf, n4, reps, sink); }, 5);
+    printf("{\"probe\":\"stream\",\"footprint_MB\":%.0f,\"GBps\":%.1f,\"sm_clock_attr_khz\":%d}\n",
+           X / 1048576.0, (double)X * reps / ms / 1e6, sm_clk);
+  }
+  for (size_t X : {(size_t)60 << 20, (size_t)96 << 20}) {
+    const uint32_t nrows = (uint32_t)(X / 256);
+    const long steps = 4096;
+    for (int wps : {16, 32, 48}) {                        // resident warps per SM
+      const int threads = 256;
+      const int grid = nsm * wps / 8;
+      const double bytes = (double)grid * 8 * steps * 4 * 256;
+      float ms = time_best([&] { gather_ldg<4><<<grid, threads>>>(buf, nrows, steps, sink); }, 3);
+      printf("{\"probe\":\"gather_ldg\",\"row_B\":256,\"footprint_MB\":%.0f,\"warps_per_sm\":%d,\"rows_in_flight_per_warp\":16,\"GBps\":%.1f}\n",
+             X / 1048576.0, wps, bytes / ms / 1e6);
+      const size_t smem = (size_t)8 * 4 * 64 * 16;
+      ms = time_best([&] { gather_smem<4><<<grid, threads, smem>>>(buf, nrows, steps, sink); }, 3);
+      printf("{\"probe\":\"gather_smem\",\"row_B\":256,\"footprint_MB\":%.0f,\"warps_per_sm\":%d,\"ring_depth\":4,\"GBps\":%.1f}\n",
+             X / 1048576.0, wps, bytes / ms / 1e6);
+    }
+  }
+  CK(cudaGetLastError());
+  return 0;
+}

@@ -3,7 +3,7 @@
 for s in {16..512} x {Bucket, FastRand} on the dataset-shaped graphs (1 GPU, L2 flushed before
 every call, CUDA events, median of 5), through the library's plan: es_spmm_run_ex with the
 workspace es_spmm_workspace_bytes asks for (the slab path) where it asks, else the fused kernel
-(ES_SPMM_SLAB=0 forces the fused kernel everywhere).  Prints one JSON line per point."""
+(`--kernel fused` as the first argument forces the fused kernel everywhere).  Prints one JSON line per point."""
 import json
 import os
 import sys

@@ -21,43 +21,37 @@ def main():
     cases = [(16, 16, None), (41, 44, None), (128, 128, None), (200, 200, "tma"), (256, 256, None),
              (602, 604, None), (602, 602, None), (1100, 1100, None), (130, 130, "warp")]
     for F, ldb, kern in cases:
-        os.environ.pop("ES_SPMM_KERNEL", None)
-        if kern:
-            os.environ["ES_SPMM_KERNEL"] = kern
         B = t(synth.dense(700, F, seed=F, ld=ldb))
-        for strat in (1, 2):
-            for red in (0, 1):
-                C = es.es_spmm_run(rp, ci, va, B, 64, strat, 5, red, F=F)
+        with es.kernel_override(kern or "auto"):
+            for strat in (1, 2):
+                for red in (0, 1):
+                    C = es.es_spmm_run(rp, ci, va, B, 64, strat, 5, red, F=F)
         torch.cuda.synchronize()
         print("ok", F, ldb, es.es_spmm_plan(F, ldb, F, B, C), flush=True)
-    # slab path (forced): 8 x 2 and 16 x 1 lanes per slot, narrow tails, and a workspace sized
-    # for a quarter of the stored entries (slots past its capacity are never read or written)
-    os.environ.pop("ES_SPMM_KERNEL", None)
-    os.environ["ES_SPMM_SLAB"] = "1"
-    for g in ("8", "16"):
-        os.environ["ES_SPMM_SLAB_G"] = g
-        for F, ldb in ((602, 608), (130, 132), (200, 200), (17, 20)):
-            B = t(synth.dense(700, F, seed=F, ld=ldb))
-            for nnz in (len(colind), len(colind) // 4):
-                ws = es.es_spmm_workspace(300, 700, nnz, F, ldb, 64, True, device=dev)
-                for strat in (1, 2):
-                    es.es_spmm_run_ex(rp, ci, va, B, 64, strat, 5, 1, F=F, workspace=ws)
-                es.es_spmm_run_ex(rp, ci, None, B, 64, 2, 5, 0, F=F, workspace=ws)
-                es.es_spmm_run_ex(rp, ci, va, B, 64, 2, 5, 1, F=F, workspace=ws, reuse_sampled=True)
-            torch.cuda.synchronize()
-            print("ok slab", g, F, ldb, flush=True)
+    # slab path (forced): every slab kernel, narrow tails, and a workspace sized for a quarter of
+    # the stored entries with that nnz stated (the device backstop poisons the rows that do not fit)
+    for fam, tune in (("slab_smem", (0, 8)), ("slab_smem", (0, 16)), ("slab_ldg", ()), ("slab_tma", ())):
+        with es.kernel_override(fam, *tune):
+            for F, ldb in ((602, 608), (130, 136), (200, 200), (17, 24)):
+                B = t(synth.dense(700, F, seed=F, ld=ldb))
+                for nnz in (len(colind), len(colind) // 4):
+                    ws = es.es_spmm_workspace(300, 700, nnz, F, ldb, 64, True, device=dev)
+                    for strat in (1, 2):
+                        es.es_spmm_run_ex(rp, ci, va, B, 64, strat, 5, 1, F=F, workspace=ws, nnz=nnz)
+                    es.es_spmm_run_ex(rp, ci, None, B, 64, 2, 5, 0, F=F, workspace=ws, nnz=nnz)
+                    es.es_spmm_run_ex(rp, ci, va, B, 64, 2, 5, 1, F=F, workspace=ws, reuse_sampled=True, nnz=nnz)
+                torch.cuda.synchronize()
+                print("ok slab", fam, tune, F, ldb, flush=True)
     # bf16 storage on the slab path (128-element slices + narrow tails) and the slab backward
-    os.environ["ES_SPMM_SLAB_G"] = "8"
-    for F, ldb in ((602, 608), (200, 200), (40, 40)):
-        Bh = t(synth.dense(700, F, seed=F, ld=ldb)).to(torch.bfloat16)
-        ws = es.es_spmm_workspace(300, 700, len(colind), F, ldb, 64, True, device=dev)
-        es.es_spmm_run_ex(rp, ci, va, Bh, 64, 2, 5, 1, F=F, workspace=ws)
-        dC = t(synth.dense(300, F, seed=3, ld=ldb))
-        es.es_spmm_backward_ex(rp, ci, va, dC, 700, 64, 2, 5, 1, F=F, workspace=ws, reuse_sampled=True)
-        torch.cuda.synchronize()
-        print("ok slab bf16 + backward", F, ldb, flush=True)
-    os.environ.pop("ES_SPMM_SLAB", None)
-    os.environ.pop("ES_SPMM_SLAB_G", None)
+    with es.kernel_override("slab"):
+        for F, ldb in ((602, 608), (200, 200), (40, 40)):
+            Bh = t(synth.dense(700, F, seed=F, ld=ldb)).to(torch.bfloat16)
+            ws = es.es_spmm_workspace(300, 700, len(colind), F, ldb, 64, True, device=dev)
+            es.es_spmm_run_ex(rp, ci, va, Bh, 64, 2, 5, 1, F=F, workspace=ws)
+            dC = t(synth.dense(300, F, seed=3, ld=ldb))
+            es.es_spmm_backward_ex(rp, ci, va, dC, 700, 64, 2, 5, 1, F=F, workspace=ws, reuse_sampled=True)
+            torch.cuda.synchronize()
+            print("ok slab bf16 + backward", F, ldb, flush=True)
     es.es_spmm_sample(rp, ci, va, 40, 2, 9)
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
     es.es_spmm_run_host(pin(rowptr), pin(colind), pin(val), pin(synth.dense(700, 602, 1, ld=604)), 64, 2, 0,

@@ -16,9 +16,9 @@ if not torch.cuda.is_available():  # pragma: no cover
 
 import paper_2104_10716_b200 as es  # noqa: E402
 from paper_2104_10716_b200.autograd import sampled_spmm  # noqa: E402
+from _bounds import U, bound_ok  # noqa: E402,F401
 
 DEV = "cuda:0"
-U = 2.0 ** -24
 
 
 def t(a):
@@ -28,17 +28,6 @@ def t(a):
 @pytest.fixture(scope="module")
 def graph():
     return synth.random_csr(900, 1100, seed=21, max_deg=250, special=(577, 1154, 1000))
-
-
-def bound_ok(g, rowptr, colind, val, dC, n_cols, s, strat, seed, reduce):
-    o = oracle.spmm_backward(rowptr, colind, val, dC, n_cols, s, strat, seed=seed, reduce=reduce)
-    mag = oracle.spmm_backward(rowptr, colind, None if val is None else np.abs(val), np.abs(dC), n_cols, s,
-                               strat, seed=seed, reduce=reduce).astype(np.float64)
-    _, sc, _, _ = oracle.sample(rowptr, colind, val, s, strat, seed)
-    nc = np.bincount(sc, minlength=n_cols).astype(np.float64)[:, None]
-    tol = (nc + 2) * U * mag + 1e-30
-    err = np.abs(g.astype(np.float64) - o)
-    return bool(np.all(err <= tol)), float(np.max(err / np.maximum(mag, 1e-30)))
 
 
 @pytest.mark.parametrize("F,ld", [(1, 1), (16, 16), (41, 41), (128, 128), (602, 604), (602, 602), (1100, 1100)])
@@ -91,17 +80,17 @@ def test_row_blocks_accumulate_into_one_dB(graph):
 
 
 @pytest.mark.parametrize("path", ["fused", "slab"])
-def test_autograd_gradient(graph, path, monkeypatch):
+def test_autograd_gradient(graph, path):
     rowptr, colind, val = graph
     F = 32 if path == "fused" else 136
     B = t(synth.dense(1100, F, seed=8)).requires_grad_(True)
     W = t(synth.dense(900, F, seed=9))
     ws = None
     if path == "slab":                      # forward samples into the workspace, backward reuses it
-        monkeypatch.setenv("ES_SPMM_SLAB", "1")
-        ws = es.es_spmm_workspace(900, 1100, len(colind), F, F, 24, True, device=DEV)
+        ws = es.es_spmm_workspace(900, 1100, len(colind), F, F, 24, True, device=DEV, kernel="slab")
     for seed in (1, 2):                     # a new sampled subset per "iteration"
-        C = sampled_spmm(B, t(rowptr), t(colind), t(val), 24, 2, seed, 1, workspace=ws)
+        with es.kernel_override("slab" if ws is not None else "auto"):
+            C = sampled_spmm(B, t(rowptr), t(colind), t(val), 24, 2, seed, 1, workspace=ws)
         loss = (C * W).sum()
         B.grad = None
         loss.backward()
@@ -129,10 +118,14 @@ def test_deterministic_backward_parity_and_reproducibility(graph, F, reduce):
 @pytest.mark.parametrize("F,ld", [(17, 20), (64, 64), (128, 128), (602, 604), (602, 608)])
 @pytest.mark.parametrize("strat", [1, 2])
 @pytest.mark.parametrize("reduce", [0, 1])
-def test_slab_backward_parity(graph, F, ld, strat, reduce, monkeypatch):
+def test_slab_backward_parity(graph, F, ld, strat, reduce):
     """The feature-sliced backward (a workspace passed): sampling its own slots, and reusing the
     ones a forward call left in the workspace -- same order-independent bound."""
-    monkeypatch.setenv("ES_SPMM_SLAB", "1")
+    with es.kernel_override("slab"):
+        _slab_backward_parity(graph, F, ld, strat, reduce)
+
+
+def _slab_backward_parity(graph, F, ld, strat, reduce):
     rowptr, colind, val = graph
     dC = synth.dense(900, F, seed=F + 3, ld=ld)
     B = synth.dense(1100, F, seed=F + 4, ld=ld)

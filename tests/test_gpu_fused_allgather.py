@@ -30,9 +30,13 @@ def graph():
 
 
 @pytest.mark.parametrize("path", ["fused", "slab"])
-def test_two_local_peer_buffers(path, monkeypatch):
-    if path == "slab":                  # the feature-sliced path's epilogue stores to the peers too
-        monkeypatch.setenv("ES_SPMM_SLAB", "1")
+def test_two_local_peer_buffers(path):
+    # slab: the feature-sliced path's epilogue stores to the peers too
+    with es.kernel_override(path):
+        _two_local_peer_buffers(path)
+
+
+def _two_local_peer_buffers(path):
     rowptr, colind, val, B = graph()
     dev = torch.device("cuda:0")
     bufs = [es.es_ipc_alloc(N * 132 * 4) for _ in range(2)]
@@ -50,7 +54,7 @@ def test_two_local_peer_buffers(path, monkeypatch):
                   if path == "slab" else None)
             es.es_spmm_run_ex(t(rowptr[a:b + 1]), t(colind[e0:e1]), t(val[e0:e1]), Bd, 64, 2, 3, 1, F=F,
                               C=views[0], row_begin=int(a), row_end=int(b), n_rows=N, nnz_base=int(e0),
-                              c_peers=peers, n_peers=2, workspace=ws)
+                              c_peers=peers, n_peers=2, workspace=ws, nnz=int(e1 - e0))
         torch.cuda.synchronize()
         want = oracle.spmm(rowptr, colind, val, B, 64, 2, seed=3, reduce=1, F=F)
         for v in views:

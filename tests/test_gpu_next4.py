@@ -13,6 +13,7 @@ if not torch.cuda.is_available():  # pragma: no cover
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
 import paper_2104_10716_b200 as es  # noqa: E402
+from _bounds import bound_ok  # noqa: E402
 
 DEV = "cuda:0"
 
@@ -45,8 +46,8 @@ def test_prime_override(graph, prime):
         assert rel_ok(g, o)[0], (F, prime)
     dC = synth.dense(1100, 24, seed=2)
     dB = es.es_spmm_backward_ex(t(rowptr), t(colind), t(val), t(dC), 2300, 40, 2, 5, 1, prime=prime)
-    od = oracle.spmm_backward(rowptr, colind, val, dC, 2300, 40, 2, seed=5, reduce=1, prime=prime)
-    assert np.allclose(dB.cpu().numpy(), od, rtol=1e-4, atol=1e-5)
+    ok, worst = bound_ok(dB.cpu().numpy(), rowptr, colind, val, dC, 2300, 40, 2, 5, 1, prime=prime)
+    assert ok, (prime, worst)
 
 
 def test_mean_by_degree(graph):
@@ -67,18 +68,17 @@ def test_mean_by_degree(graph):
 @pytest.mark.parametrize("F,ld", [(8, 8), (16, 16), (100, 104), (128, 128), (256, 256), (602, 608), (1100, 1104)])
 @pytest.mark.parametrize("strat", [1, 2])
 @pytest.mark.parametrize("path", ["fused", "slab"])
-def test_bf16_storage(graph, F, ld, strat, path, monkeypatch):
+def test_bf16_storage(graph, F, ld, strat, path):
     rowptr, colind, val = graph
     B32 = synth.dense(2300, F, seed=F + 7, ld=ld)
     Bh = t(B32).to(torch.bfloat16)
     Bq = Bh.float().cpu().numpy()          # the exact values the kernel reads
     ws = None
     if path == "slab":                     # 128-element bf16 slices (+ narrow tails)
-        monkeypatch.setenv("ES_SPMM_SLAB", "1")
-        ws = es.es_spmm_workspace(1100, 2300, len(colind), F, ld, 256, True, device=DEV)
+        ws = es.es_spmm_workspace(1100, 2300, len(colind), F, ld, 256, True, device=DEV, kernel="slab")
     for s, reduce in [(16, 0), (256, 1)]:
-        g = es.es_spmm_run_ex(t(rowptr), t(colind), t(val), Bh, s, strat, 3, reduce, F=F,
-                              workspace=ws).cpu().numpy()
+        g = es.es_spmm_run_ex(t(rowptr), t(colind), t(val), Bh, s, strat, 3, reduce, F=F, workspace=ws,
+                              kernel="slab" if ws is not None else None).cpu().numpy()
         o = oracle.spmm(rowptr, colind, val, Bq, s, strat, seed=3, reduce=reduce, F=F)
         ok, err = rel_ok(g, o)
         assert ok, (F, s, err)

@@ -33,12 +33,19 @@ def graph():
     return synth.random_csr(1301, 2300, seed=41, max_deg=400, special=(577, 1154, 1009, 300, 65, 33, 1))
 
 
-@pytest.fixture(params=["8", "16"])
-def lanes(request, monkeypatch):
-    monkeypatch.setenv("ES_SPMM_SLAB", "1")
-    monkeypatch.setenv("ES_SPMM_SLAB_G", request.param)
-    monkeypatch.delenv("ES_SPMM_SLAB_STAGES", raising=False)
-    return int(request.param)
+@pytest.fixture(params=["smem8", "smem16", "ldg", "tma"])
+def lanes(request):
+    """Each slab kernel, forced: the shared-memory ring with 8 / 16 lanes per slot, the
+    register-direct 256-bit kernel (32-B row pitches; else the plan's), the TMA gather4 kernel."""
+    fam, tune = {"smem8": ("slab_smem", (0, 8)), "smem16": ("slab_smem", (0, 16)), "ldg": ("slab_ldg", ()),
+                 "tma": ("slab_tma", ())}[request.param]
+    with es.kernel_override(fam, *tune):
+        yield request.param
+
+
+def _unsupported_ok(B):
+    """slab_ldg needs a 32-B row pitch: other layouts are ES_ERR_UNSUPPORTED under it."""
+    return es._OVERRIDE["kernel"] == es.ES_KERNEL_SLAB_LDG and (B.shape[1] * B.itemsize) % 32 != 0
 
 
 def slab(rowptr, colind, val, B, s, strat, seed, reduce, F, **kw):
@@ -47,8 +54,14 @@ def slab(rowptr, colind, val, B, s, strat, seed, reduce, F, **kw):
     assert ws is not None
     vd = None if val is None else t(val)
     n0 = es.es_launch_count()
+    if _unsupported_ok(B):
+        with pytest.raises(es.EsError, match="UNSUPPORTED"):
+            es.es_spmm_run_ex(t(rowptr), t(colind), vd, t(B), s, strat, seed, reduce, F=F, workspace=ws, **kw)
+        with es.kernel_override("slab_smem"):
+            return slab(rowptr, colind, val, B, s, strat, seed, reduce, F, **kw)
     out = es.es_spmm_run_ex(t(rowptr), t(colind), vd, t(B), s, strat, seed, reduce, F=F, workspace=ws,
                             **kw).cpu().numpy()
+    assert es.es_spmm_workspace_status(ws) == es.ES_WS_OK
     # the slab path really ran (it launches the sampling kernels and/or one kernel per slice;
     # a silent fallback to the fused kernel would launch exactly one)
     assert es.es_launch_count() - n0 >= (F + 63) // 64 + (0 if strat == 1 else 4) and \
@@ -95,18 +108,33 @@ def test_slab_options(graph, lanes):
     assert np.array_equal(g, np.repeat(want[:, None], 300, 1))
 
 
-def test_g16_is_bitwise_cpasync_hw(graph, monkeypatch):
+def test_g16_is_bitwise_cpasync_hw(graph):
     """The documented order: with 16 lanes per slot the slab kernel sums exactly as the fused
     two-slots-per-step ring (spmm_cpasync_hw) does, so F <= 128 results are bitwise equal."""
     rowptr, colind, val = graph
     B = synth.dense(2300, 128, seed=4)
-    monkeypatch.setenv("ES_SPMM_KERNEL", "cpasync")
-    monkeypatch.setenv("ES_SPMM_HALFWARP", "1")
-    fused = es.es_spmm_run(t(rowptr), t(colind), t(val), t(B), 256, 2, 7, 1, F=128).cpu().numpy()
-    monkeypatch.setenv("ES_SPMM_SLAB", "1")
-    monkeypatch.setenv("ES_SPMM_SLAB_G", "16")
-    g = slab(rowptr, colind, val, B, 256, 2, 7, 1, 128)
+    with es.kernel_override("halfwarp"):
+        fused = es.es_spmm_run(t(rowptr), t(colind), t(val), t(B), 256, 2, 7, 1, F=128).cpu().numpy()
+    with es.kernel_override("slab_smem", 0, 16):
+        g = slab(rowptr, colind, val, B, 256, 2, 7, 1, 128)
     assert np.array_equal(g, fused)
+
+
+@pytest.mark.parametrize("F,ld", [(128, 128), (602, 608)])
+def test_slab_kernels_same_order_bitwise(graph, F, ld):
+    """The documented per-element order: the 8-lane shared-memory ring, the register-direct
+    kernel (8 lanes x 32 B) on full slices and the TMA gather4 kernel all sum slot j into group
+    j mod 4 in slot order, so full 64-float slices agree bitwise (the narrow last slice of F=602
+    uses 4 lanes per slot in the first two, 8 in the TMA kernel)."""
+    rowptr, colind, val = graph
+    B = synth.dense(2300, F, seed=14, ld=ld)
+    outs = {}
+    for fam in ("slab_smem", "slab_ldg", "slab_tma"):
+        with es.kernel_override(fam):
+            outs[fam] = slab(rowptr, colind, val, B, 256, 2, 7, 1, F)
+    full = (F // 64) * 64
+    assert np.array_equal(outs["slab_smem"][:, :full], outs["slab_ldg"][:, :full])
+    assert np.array_equal(outs["slab_smem"][:, :full], outs["slab_tma"][:, :full])
 
 
 def test_slab_row_blocks_bitwise(graph, lanes):
@@ -120,14 +148,14 @@ def test_slab_row_blocks_bitwise(graph, lanes):
         ws = es.es_spmm_workspace(int(b - a), 2300, e1 - e0, 602, 608, 256, True, device=DEV)
         part = es.es_spmm_run_ex(t(rowptr[a:b + 1]), t(colind[e0:e1]), t(val[e0:e1]), t(B), 256, 2, 99, 1,
                                  F=602, row_begin=int(a), row_end=int(b), n_rows=len(rowptr) - 1,
-                                 nnz_base=e0, workspace=ws).cpu().numpy()
+                                 nnz_base=e0, workspace=ws, nnz=e1 - e0).cpu().numpy()
         assert np.array_equal(part, full[a:b])
 
 
 def test_slab_ldc_padding_untouched(graph, lanes):
     rowptr, colind, val = graph
-    B = synth.dense(2300, 130, seed=2, ld=132)
-    ws = es.es_spmm_workspace(1301, 2300, len(colind), 130, 132, 64, True, device=DEV)
+    B = synth.dense(2300, 130, seed=2, ld=136)
+    ws = es.es_spmm_workspace(1301, 2300, len(colind), 130, 136, 64, True, device=DEV)
     C = torch.full((1301, 140), -7.0, dtype=torch.float32, device=DEV)
     es.es_spmm_run_ex(t(rowptr), t(colind), t(val), t(B), 64, 1, 0, 0, F=130, C=C, workspace=ws)
     Ch = C.cpu().numpy()
@@ -163,11 +191,15 @@ def test_reuse_sampled_slots(graph, lanes):
     assert rel_ok(full2, o)[0]
 
 
-def test_slab_launch_count(graph, monkeypatch):
+def test_slab_launch_count(graph):
     """The launches es_launch_count reports (bench.py's gpu_launches) match the kernels the slab
     path runs: count + CUB scan (2 kernels) + materialise + one per 64-float slice; Bucket reads
     its slots in place (slices only); reuse_sampled runs the slices only."""
-    monkeypatch.setenv("ES_SPMM_SLAB", "1")
+    with es.kernel_override("slab"):
+        _slab_launch_count(graph)
+
+
+def _slab_launch_count(graph):
     rowptr, colind, val = graph
     B = synth.dense(2300, 602, seed=1, ld=608)
     ws = es.es_spmm_workspace(1301, 2300, len(colind), 602, 608, 256, True, device=DEV)
@@ -177,3 +209,75 @@ def test_slab_launch_count(graph, monkeypatch):
                           reuse_sampled=reuse)
         torch.cuda.synchronize()
         assert es.es_launch_count() - n0 == want, (strat, reuse)
+
+
+# ------------------------------------------------------------------ workspace contract
+def test_undersized_workspace_is_an_error(graph):
+    """A workspace that cannot hold the sampled slots is ES_ERR_INVALID_VALUE (never a silent
+    truncation), and so is one sized for val = NULL used with val."""
+    rowptr, colind, val = graph
+    B = synth.dense(2300, 602, seed=1, ld=608)
+    full = es.es_spmm_workspace_bytes(1301, 2300, len(colind), 602, 608, 256, True, kernel="slab")
+    small = torch.zeros(full // 2, dtype=torch.uint8, device=DEV)
+    with es.kernel_override("slab"):
+        with pytest.raises(es.EsError, match="INVALID"):
+            es.es_spmm_run_ex(t(rowptr), t(colind), t(val), t(B), 256, 2, 0, 1, F=602, workspace=small)
+        noval = es.es_spmm_workspace(1301, 2300, len(colind), 602, 608, 256, False, device=DEV)
+        with pytest.raises(es.EsError, match="INVALID"):
+            es.es_spmm_run_ex(t(rowptr), t(colind), t(val), t(B), 256, 2, 0, 1, F=602, workspace=noval)
+        # sized for val = NULL, used with val = NULL: fine
+        g = es.es_spmm_run_ex(t(rowptr), t(colind), None, t(B), 256, 2, 0, 1, F=602, workspace=noval)
+        o = oracle.spmm(rowptr, colind, None, B, 256, 2, reduce=1, F=602)
+        assert rel_ok(g.cpu().numpy(), o)[0]
+
+
+def test_understated_nnz_poisons_rows_and_flags_overflow(graph):
+    """The device backstop: a caller that understates nnz gets NaN rows for every row whose
+    slots do not fit, and ES_WS_OVERFLOW in the workspace status -- never a truncated sum."""
+    rowptr, colind, val = graph
+    B = synth.dense(2300, 128, seed=2)
+    K = int(np.minimum(np.diff(rowptr), 256).sum())
+    lie = K // 2
+    nb = es.es_spmm_workspace_bytes(1301, 2300, lie, 128, 128, 256, True, kernel="slab")
+    ws = torch.zeros(nb, dtype=torch.uint8, device=DEV)
+    with es.kernel_override("slab"):
+        C = es.es_spmm_run_ex(t(rowptr), t(colind), t(val), t(B), 256, 2, 0, 1, F=128, workspace=ws, nnz=lie)
+    st = es.es_spmm_workspace_status(ws, reset=True)
+    assert st & es.ES_WS_OVERFLOW
+    g = C.cpu().numpy()
+    bad = np.isnan(g).all(axis=1)
+    assert bad.any() and not bad.all()
+    assert not np.isnan(g[~bad]).any()
+    # rows are materialised in order: exactly the rows whose slots end past the capacity -- a
+    # suffix of the rows -- are poisoned
+    r0 = int(np.argmax(bad))
+    assert bad[r0:].all() and not bad[:r0].any()
+    fine = ~bad
+    o = oracle.spmm(rowptr, colind, val, B, 256, 2, reduce=1, F=128)
+    assert rel_ok(g[fine], o[fine])[0]
+    assert es.es_spmm_workspace_status(ws) == es.ES_WS_OK          # reset
+
+
+def test_reuse_with_other_sampling_is_detected(graph):
+    """reuse_sampled over slots of a different sampling (other seed / s / graph): NaN rows and
+    ES_WS_SIGNATURE_MISMATCH; a layout that cannot take the slab path refuses reuse."""
+    rowptr, colind, val = graph
+    B = synth.dense(2300, 300, seed=3, ld=300)
+    ws = es.es_spmm_workspace(1301, 2300, len(colind), 300, 300, 96, True, device=DEV, kernel="slab")
+    rp, ci, v = t(rowptr), t(colind), t(val)
+    with es.kernel_override("slab"):
+        es.es_spmm_run_ex(rp, ci, v, t(B), 96, 2, 13, 1, F=300, workspace=ws)
+        assert es.es_spmm_workspace_status(ws) == es.ES_WS_OK
+        for kw in (dict(seed=14), dict(s=95)):
+            args = dict(seed=13, s=96)
+            args.update(kw)
+            C = es.es_spmm_run_ex(rp, ci, v, t(B), args["s"], 2, args["seed"], 1, F=300, workspace=ws,
+                                  reuse_sampled=True)
+            assert torch.isnan(C).all()
+            assert es.es_spmm_workspace_status(ws, reset=True) & es.ES_WS_SIGNATURE_MISMATCH
+        C = es.es_spmm_run_ex(rp, ci, v, t(B), 96, 2, 13, 1, F=300, workspace=ws, reuse_sampled=True)
+        assert not torch.isnan(C).any()
+    # unaligned B rows: no slab path, so nothing to reuse -> error, not a silent fused run
+    B2 = t(synth.dense(2300, 301, seed=3, ld=301))
+    with pytest.raises(es.EsError, match="INVALID"):
+        es.es_spmm_run_ex(rp, ci, v, B2, 96, 2, 13, 1, F=301, workspace=ws, reuse_sampled=True)

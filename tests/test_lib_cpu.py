@@ -22,7 +22,7 @@ def lib():
 def test_header_declarations_are_exported(lib):
     with open(os.path.join(ROOT, "include", "es_spmm.h")) as f:
         text = f.read()
-    declared = set(re.findall(r"^\s*(?:es_status_t|int64_t|int32_t|const char\*)\s+(es_\w+)\s*\(", text, re.M))
+    declared = set(re.findall(r"^\s*(?:es_status_t|int64_t|int32_t|void|const char\*)\s+(es_\w+)\s*\(", text, re.M))
     assert declared == set(es.EXPORTS), declared ^ set(es.EXPORTS)
     for name in declared:
         assert hasattr(lib, name), name
@@ -69,30 +69,70 @@ def test_host_validation_rejects_bad_arguments(lib):
                               None) == 1
 
 
-def test_plan_selection(lib, monkeypatch):
+def test_plan_selection(lib):
     assert es.es_spmm_plan(128, 128, 128).startswith("es::spmm_cpasync_hw<stages4>")
     assert es.es_spmm_plan(200, 200, 200).startswith("es::spmm_cpasync<stages4>")
-    monkeypatch.setenv("ES_SPMM_HALFWARP", "0")
-    assert es.es_spmm_plan(128, 128, 128).startswith("es::spmm_cpasync<stages4>")
-    monkeypatch.delenv("ES_SPMM_HALFWARP")
     assert es.es_spmm_plan(256, 256, 256).startswith("es::spmm_cpasync<stages4>")
     assert es.es_spmm_plan(512, 512, 512).startswith("es::spmm_cpasync<stages4>")
     assert es.es_spmm_plan(602, 604, 604).startswith("es::spmm_tma<nch5,stages4>")
     assert es.es_spmm_plan(100, 102, 100).startswith("es::spmm_warp<vec2")      # 8-B aligned rows
-    monkeypatch.setenv("ES_SPMM_KERNEL", "warp")
-    assert es.es_spmm_plan(128, 128, 128).startswith("es::spmm_warp<vec4,nch1>")
-    assert es.es_spmm_plan(256, 256, 256).startswith("es::spmm_warp<vec4,nch2>")
-    assert "vec4,nch5" in es.es_spmm_plan(602, 604, 604)
-    monkeypatch.delenv("ES_SPMM_KERNEL")
     assert "spmm_warp<vec2" in es.es_spmm_plan(602, 602, 602)      # 8-B rows: no TMA
-    monkeypatch.setenv("ES_SPMM_KERNEL", "tma")
-    assert es.es_spmm_plan(200, 200, 200).startswith("es::spmm_tma<nch2")
-    monkeypatch.setenv("ES_SPMM_KERNEL", "cpasync")
-    assert es.es_spmm_plan(602, 604, 604).startswith("es::spmm_cpasync")
-    monkeypatch.delenv("ES_SPMM_KERNEL")
     assert "subwarp<vec4,g4>" in es.es_spmm_plan(16, 16, 16)
     assert "subwarp<vec1,g1>" in es.es_spmm_plan(1, 1, 1)
     assert "spmm_warp<vec4,nch8>" in es.es_spmm_plan(5000, 5000, 5000)   # feature-tiled
+
+
+def test_product_library_reads_no_environment():
+    """Kernel selection arrives through es_spmm_options_t only: the
+    library's sources call no getenv (the statically linked CUDA runtime reads its own
+    CUDA_* variables; that is not ours)."""
+    csrc = os.path.join(ROOT, "paper_2104_10716_b200", "csrc")
+    for f in os.listdir(csrc):
+        if f.endswith((".cu", ".cuh", ".h")):
+            assert "getenv" not in open(os.path.join(csrc, f)).read(), f
+
+
+def test_forced_kernel_option_is_validated(lib):
+    Opt = es.EsOptions
+    dummy = ctypes.c_void_p(0x1000)
+    bad = Opt.make()
+    bad.kernel = 42
+    assert lib.es_spmm_run_ex(10, 10, dummy, 0, dummy, None, dummy, 8, 8, 4, 2, 0, 0, dummy, 8, 0, 10,
+                              ctypes.byref(bad), None) == es.ES_ERR_INVALID_VALUE
+    # a slab kernel forced without a workspace: the path cannot run
+    assert lib.es_spmm_run_ex(10, 10, dummy, 0, dummy, None, dummy, 8, 8, 4, 2, 0, 0, dummy, 8, 0, 10,
+                              ctypes.byref(Opt.make(kernel="slab")), None) == es.ES_ERR_UNSUPPORTED
+
+
+def test_undersized_workspace_rejected_on_host(lib):
+    """The capacity check is host arithmetic (no device access): a workspace that cannot hold
+    min(nnz, n*s) slots -- or n*s when nnz is not stated -- is ES_ERR_INVALID_VALUE."""
+    Opt = es.EsOptions
+    dummy = ctypes.c_void_p(0x1000)
+    n, s, F, ldb = 1000, 64, 602, 608
+    need = es.es_spmm_workspace_bytes(n, n, 20000, F, ldb, s, True, kernel="slab")
+
+    class _T:                                       # a stand-in "tensor" for EsOptions.make
+        def __init__(self, nbytes):
+            self.n = nbytes
+
+        def numel(self):
+            return self.n
+
+        def element_size(self):
+            return 1
+
+        def data_ptr(self):
+            return 0x100000
+
+    def run(nbytes, nnz, val=dummy):
+        o = Opt.make(workspace=_T(nbytes), nnz=nnz, kernel="slab")
+        return lib.es_spmm_run_ex(n, n, dummy, 0, dummy, val, ctypes.c_void_p(0x2000), F, ldb, s, 2, 0, 1,
+                                  ctypes.c_void_p(0x3000), ldb, 0, n, ctypes.byref(o), None)
+    assert run(need - 4096, 20000) == es.ES_ERR_INVALID_VALUE          # too small for nnz slots
+    assert run(need, 0) == es.ES_ERR_INVALID_VALUE                     # nnz unknown: n*s = 64000 slots
+    noval = es.es_spmm_workspace_bytes(n, n, 20000, F, ldb, s, False, kernel="slab")
+    assert run(noval, 20000) == es.ES_ERR_INVALID_VALUE                # sized for val NULL, val passed
 
 
 class _B:
@@ -168,11 +208,10 @@ def test_options_validation(lib):
                                    ctypes.byref(Opt.make(bf16=True)), None) == es.ES_ERR_UNSUPPORTED
 
 
-def test_workspace_bytes_plan(lib, monkeypatch):
+def test_workspace_bytes_plan(lib):
     """es_spmm_workspace_bytes (host only): the slab path is asked for when a 64-float slab of B
-    fits L2, F >= 128 and rows sample >= 128 slots on average; the bound covers min(nnz, n*s)
-    slots (+ values)."""
-    monkeypatch.delenv("ES_SPMM_SLAB", raising=False)
+    fits L2, F >= 128, ldb % 4 == 0 and rows sample enough slots on average; the bound covers
+    min(nnz, n*s) slots (+ values)."""
     reddit = es.es_spmm_workspace_bytes(232965, 232965, 114615945, 602, 608, 256)
     assert reddit >= 8 * 232965 * 256 + 8 * 232966            # n*s < nnz here: n*s slots
     assert es.es_spmm_workspace_bytes(232965, 232965, 114615945, 602, 608, 256, has_val=False) < reddit
@@ -182,12 +221,8 @@ def test_workspace_bytes_plan(lib, monkeypatch):
     assert es.es_spmm_workspace_bytes(10_000_000, 10_000_000, 10**9, 256, 256, 128) == 0  # slab > L2
     assert es.es_spmm_workspace_bytes(232965, 232965, 114615945, 64, 64, 256) == 0      # one slice
     assert es.es_spmm_workspace_bytes(232965, 232965, 114615945, 602, 608, 64) == 0     # s < 128
-    monkeypatch.setenv("ES_SPMM_SLAB", "1")
-    small = es.es_spmm_workspace_bytes(232965, 232965, 1000, 602, 608, 256)
+    assert es.es_spmm_workspace_bytes(232965, 232965, 114615945, 602, 602, 256) == 0    # 8-B row pitch
+    small = es.es_spmm_workspace_bytes(232965, 232965, 1000, 602, 608, 256, kernel="slab")
     assert 8 * 1000 <= small - 8 * 232966 < 8 * 1000 + 4096                             # nnz < n*s
-    monkeypatch.delenv("ES_SPMM_SLAB")
     assert es.es_spmm_workspace_bytes(10, 10, 10, 602, 600, 4) == 0                     # ldb < F
-    monkeypatch.setenv("ES_SPMM_SLAB", "0")
-    assert es.es_spmm_workspace_bytes(232965, 232965, 114615945, 602, 608, 256) == 0
-    monkeypatch.setenv("ES_SPMM_SLAB", "1")
-    assert es.es_spmm_workspace_bytes(100, 100, 1000, 602, 608, 256) > 0
+    assert es.es_spmm_workspace_bytes(100, 100, 1000, 602, 608, 256, kernel="slab") > 0
