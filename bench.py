@@ -57,8 +57,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=0, help="FastRand seed (0 = paper-exact Eq. 2)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--kernel", default="auto",
-                    choices=["auto", "fused", "slab", "slab_smem", "slab_ldg", "slab_tma", "tma", "warp", "cpasync",
-                             "halfwarp"],
+                    choices=["auto", "fused", "slab", "slab_smem", "slab_ldg", "slab_tma", "slab_stream", "tma", "warp",
+                             "cpasync", "halfwarp", "rowstream"],
                     help="kernel family (A/B measurement through es_spmm_options_t.kernel; auto = the "
                          "library's plan, fused = never the feature-sliced path, slab* = that path wherever "
                          "it can run)")
@@ -271,7 +271,7 @@ def main():
         peers = PeerBuffers(n, C_d.stride(0), device=dev)
     # the library's plan: a workspace (allocated once, outside the timed region) selects the
     # feature-sliced path when B does not fit L2 but a 64-float slab of it does
-    slab_family = a.kernel in ("auto", "slab", "slab_smem", "slab_ldg", "slab_tma")
+    slab_family = a.kernel in ("auto", "slab", "slab_smem", "slab_ldg", "slab_tma", "slab_stream")
     ws = (es.es_spmm_workspace(r1 - r0, n, e1 - e0, F, ldb, a.s, True, device=dev,
                                kernel=None if a.kernel == "auto" else a.kernel) if slab_family else None)
     kern = None if a.kernel == "auto" else a.kernel

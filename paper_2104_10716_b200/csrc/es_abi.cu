@@ -73,7 +73,7 @@ es_status_t read_opts(const es_spmm_options_t* o, Opts* out) {
         out->nnz = o->nnz;
     }
     if (ES_COVERS(o, tune)) {
-        if (o->kernel < ES_KERNEL_AUTO || o->kernel > ES_KERNEL_SLAB_TMA) return ES_ERR_INVALID_VALUE;
+        if (o->kernel < ES_KERNEL_AUTO || o->kernel > ES_KERNEL_SLAB_STREAM) return ES_ERR_INVALID_VALUE;
         out->tune.kernel = o->kernel;
         out->tune.stages = o->tune[0];
         out->tune.width = o->tune[1];
@@ -198,13 +198,14 @@ es_status_t run_rows_impl(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
     if (!rowptr || !C || (n_cols > 0 && !B)) return ES_ERR_INVALID_VALUE;
     const es::Tune& tn = o.tune;
     const bool force_slab = tn.kernel == ES_KERNEL_SLAB || tn.kernel == ES_KERNEL_SLAB_SMEM ||
-                            tn.kernel == ES_KERNEL_SLAB_LDG || tn.kernel == ES_KERNEL_SLAB_TMA;
+                            tn.kernel == ES_KERNEL_SLAB_LDG || tn.kernel == ES_KERNEL_SLAB_TMA ||
+                            tn.kernel == ES_KERNEL_SLAB_STREAM;
     const uintptr_t bu = reinterpret_cast<uintptr_t>(B), cu = reinterpret_cast<uintptr_t>(C);
     const int64_t esz = o.bf16 ? 2 : 4;
     const bool slab_layout_ok = o.workspace && bu % 16 == 0 && (ldb * esz) % 16 == 0 && slab_feasible(n_cols, F) &&
                                 tn.kernel != ES_KERNEL_FUSED && tn.kernel != ES_KERNEL_WARP &&
                                 tn.kernel != ES_KERNEL_TMA && tn.kernel != ES_KERNEL_CPASYNC &&
-                                tn.kernel != ES_KERNEL_CPASYNC_HW;
+                                tn.kernel != ES_KERNEL_CPASYNC_HW && tn.kernel != ES_KERNEL_ROWSTREAM;
     if (force_slab && !slab_layout_ok) return ES_ERR_UNSUPPORTED;
     if (slab_layout_ok) {
         // any C layout: 16-B vector stores where C's rows allow them, scalar stores otherwise
@@ -292,8 +293,11 @@ es_status_t run_rows_impl(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
     p.b_bf16 = o.bf16;
     p.c_peers = o.c_peers;
     p.n_peers = o.n_peers;
-    const es::Plan plan = o.bf16 ? es::make_plan_bf16(F, ldb, ldc, B, C) : es::make_plan(F, ldb, ldc, B, C, s, tn);
+    const int64_t k_est = o.nnz > 0 ? std::min<int64_t>(s, o.nnz / n) : s;
+    const es::Plan plan = o.bf16 ? es::make_plan_bf16(F, ldb, ldc, B, C)
+                                 : es::make_plan(F, ldb, ldc, B, C, s, tn, k_est);
     if (plan.unsupported) return ES_ERR_UNSUPPORTED;
+    if (tn.kernel == ES_KERNEL_ROWSTREAM && !plan.rowstream) return ES_ERR_UNSUPPORTED;
     cudaError_t err = es::launch_spmm(p, plan, tn, st);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return err == cudaSuccess ? ES_OK : ES_ERR_CUDA;
@@ -329,7 +333,8 @@ int64_t es_spmm_workspace_bytes_ex(int64_t n_rows, int64_t n_cols, int64_t nnz, 
     Opts o;
     if (read_opts(opt, &o) != ES_OK) return 0;
     const int k = o.tune.kernel;
-    if (k != ES_KERNEL_SLAB && k != ES_KERNEL_SLAB_SMEM && k != ES_KERNEL_SLAB_LDG && k != ES_KERNEL_SLAB_TMA)
+    if (k != ES_KERNEL_SLAB && k != ES_KERNEL_SLAB_SMEM && k != ES_KERNEL_SLAB_LDG && k != ES_KERNEL_SLAB_TMA &&
+        k != ES_KERNEL_SLAB_STREAM)
         return es_spmm_workspace_bytes(n_rows, n_cols, nnz, F, ldb, s, has_val);
     // a slab kernel forced: a workspace wherever the path can run at all
     if (n_rows <= 0 || n_cols < 0 || nnz < 0 || F < 1 || ldb < F || s < 1) return 0;
@@ -355,7 +360,10 @@ es_status_t es_spmm_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, con
                          char* buf, int32_t buf_len) {
     if (F < 1 || ldb < F || ldc < F || !buf || buf_len < 1) return ES_ERR_INVALID_VALUE;
     const es::Plan pl = es::make_plan(F, ldb, ldc, B, C);
-    if (pl.tma)
+    if (pl.rowstream)
+        snprintf(buf, (size_t)buf_len, "es::spmm_rowstream<stages%d,rows%d>%s", pl.stages, pl.rows_per_warp,
+                 pl.c_vec ? "" : " (scalar C)");
+    else if (pl.tma)
         snprintf(buf, (size_t)buf_len, "es::spmm_tma<nch%d,stages%d>(rows/warp %d)%s", pl.nch, pl.stages,
                  pl.rows_per_warp, pl.c_vec ? "" : " (scalar C)");
     else if (pl.cpasync)

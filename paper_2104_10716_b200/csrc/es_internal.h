@@ -48,6 +48,7 @@ struct Plan {
     bool cpasync;      // cp.async ring kernel (spmm_cpasync)
     bool bf16;         // B stored as bf16 (cp.async ring only)
     bool halfwarp;     // cp.async ring, two slots per step (spmm_cpasync_hw)
+    bool rowstream;    // several short rows per warp as one slot stream (spmm_rowstream)
     bool unsupported;  // no kernel for this layout (bf16 with misaligned rows)
     int stages;         // ring depth (tma)
     int rows_per_warp;  // consecutive rows per warp (tma)
@@ -139,8 +140,9 @@ cudaError_t launch_backward(const BwdParams& p, cudaStream_t st);
 cudaError_t launch_backward_deterministic(const BwdParams& p, int64_t n_cols, cudaStream_t st, int* launches,
                                           bool* too_large);
 
+// k_est: expected sampled slots per row, min(s, nnz / rows) when the caller stated nnz, else s
 Plan make_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C, int32_t s = INT32_MAX,
-               const Tune& t = Tune{});
+               const Tune& t = Tune{}, int64_t k_est = -1);
 Plan make_plan_bf16(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C);
 cudaError_t launch_spmm(SpmmParams p, const Plan& plan, const Tune& t, cudaStream_t st);
 cudaError_t launch_sample_count(const int64_t* rowptr, int64_t n, int32_t s, int64_t* s_rowptr,

@@ -37,6 +37,9 @@ namespace es {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr unsigned kFull = 0xffffffffu;
+// the plan would take the row stream when rows sample at most this many slots on average; 0:
+// never -- measured slower than the two-slot ring at every Arxiv-shaped s (profiles/r02.md)
+constexpr int64_t kRowStreamMaxK = 0;
 
 template <int VEC>
 __device__ __forceinline__ void store_out(float* Crow, int64_t vidx, int64_t F, const float* r,
@@ -376,6 +379,157 @@ spmm_cpasync(const SpmmParams p) {
             }
         }
     }
+}
+
+// ------------------------------------------------------------------ row stream (short rows)
+// Degree-adaptive mapping for short rows (§4.5.1 thread management L1073-1081, §4.5.3
+// load balancing L1100-1105): one warp owns R <= 32 consecutive rows (lane i holds row i's
+// metadata) and walks their sampled slots as ONE flat stream t = 0 .. T-1 (T = sum k_i), so the
+// cp.async ring (each lane one 16-B piece of the slot's B row, 64 < F <= 128) stays D slots
+// ahead across row boundaries and the per-row costs -- the rowptr / colind latency chain, ring
+// start-up, the epilogue's reductions -- are paid once per R rows instead of once per row.
+// A row's result is stored when the stream passes its last slot (no cross-lane reduction:
+// each lane owns its columns).  Per element: the row's slots in slot order with 32-slot chunk
+// partials (chunks counted from the row's first slot) -- spmm_cpasync's order, bitwise.
+__device__ __forceinline__ int64_t sample_pos(int32_t strategy, uint64_t off, int64_t d, uint32_t prime,
+                                              bool narrow, int32_t j) {
+    if (strategy == kBucket) return j;
+    if (narrow) return (int64_t)(((uint32_t)off + (uint32_t)j * prime) % (uint32_t)d);
+    return (int64_t)((off + (uint64_t)j * prime) % (uint64_t)d);
+}
+
+template <int D, int R, int W, int MINW>
+__global__ void __launch_bounds__(32 * W, MINW / W)
+spmm_rowstream(const SpmmParams p) {
+    static_assert(D >= 2 && (D & (D - 1)) == 0 && D <= 16 && R >= 1 && R <= 32, "ring depth / rows per warp");
+    extern __shared__ __align__(16) float4 ring_smem[];          // [W][D][32]
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int64_t r0 = ((int64_t)blockIdx.x * W + warp) * R;
+    if (r0 >= p.n_rows) return;
+    const int nr = (int)min((int64_t)R, p.n_rows - r0);
+    const uint64_t pol_a = policy_evict_first();
+    const uint64_t pol_b = policy_evict_last();
+    // lane i < nr: row r0 + i (a1: k_i = min(d_i, s); a2: its FastRand rotation, R6)
+    RowSampler rs;
+    if (lane < nr)
+        rs.init(ld_stream(p.rowptr + r0 + lane, pol_a) - p.nnz_base,
+                ld_stream(p.rowptr + r0 + lane + 1, pol_a) - p.nnz_base, p.s, p.strategy, p.seed,
+                p.row_base + r0 + lane, p.prime);
+    else
+        rs.init(0, 0, p.s, p.strategy, 0, 0, p.prime);
+    const int32_t k_me = rs.k;
+    int32_t incl = k_me;                                         // inclusive prefix of k over the rows
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t v = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += v;
+    }
+    const int32_t T = __shfl_sync(kFull, incl, 31);
+    const unsigned nonempty = __ballot_sync(kFull, k_me > 0);
+    const int NV = (int)((p.F + 3) / 4);
+    const bool active = lane < NV;                               // lane owns float4 `lane` of the row
+    // rows with k_i = 0 (empty in A): a zero row (no division), stored up front
+    unsigned empty = __ballot_sync(kFull, lane < nr && k_me == 0);
+    while (empty) {
+        const int i = __ffs(empty) - 1;
+        empty &= empty - 1;
+        const float z[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        if (active) store_c<4>(p, r0 + i, lane, z, pol_a);
+    }
+    if (T == 0) return;
+
+    float4* my = ring_smem + (size_t)warp * D * 32 + lane;
+    const float* bl = p.B + lane * 4;
+    auto copy_slot = [&](int stage, int32_t c) {
+        if (active) cp_async16<false>(my + stage * 32, bl + (int64_t)c * p.ldb, pol_b);
+    };
+    // (col, val) of flat slot t (lane-parallel: each lane one slot of a 32-slot chunk): its row
+    // is the first i with incl_i > t, found by a binary search over the lanes' prefixes
+    auto load_slot = [&](int32_t t, int32_t& c, float& a) {
+        int lo = 0;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+            const int32_t v = __shfl_sync(kFull, incl, lo + step - 1);
+            if (v <= t) lo += step;
+        }
+        const int i = lo;                                        // row of slot t (lane i holds it)
+        const int64_t beg = __shfl_sync(kFull, rs.beg, i);
+        const int64_t d = __shfl_sync(kFull, rs.d, i);
+        const uint64_t off = __shfl_sync(kFull, rs.off, i);
+        const bool narrow = __shfl_sync(kFull, (int)rs.narrow, i) != 0;
+        const int32_t j = t - (__shfl_sync(kFull, incl, i) - __shfl_sync(kFull, k_me, i));
+        c = 0;
+        a = 0.0f;
+        if (t < T) {
+            const int64_t e = beg + sample_pos(p.strategy, off, d, p.prime, narrow, j);
+            c = ld_stream(p.colind + e, pol_a);
+            a = p.val ? ld_stream(p.val + e, pol_a) : 1.0f;
+        }
+    };
+    int32_t c0, c1;
+    float a0, a1;
+    load_slot(lane, c0, a0);
+    load_slot(32 + lane, c1, a1);
+#pragma unroll
+    for (int t = 0; t < D; ++t) {
+        const int32_t c = __shfl_sync(kFull, c0, t);
+        if (t < T) copy_slot(t, c);
+        cp_async_commit();
+    }
+    float part[4] = {0.0f, 0.0f, 0.0f, 0.0f}, tot[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    int cur = __ffs(nonempty) - 1;                               // row being accumulated
+    int32_t cur_end = __shfl_sync(kFull, incl, cur);
+    int32_t j = 0;                                               // slot index within the row
+    for (int32_t t0 = 0; t0 < T; t0 += 32) {
+        const int n_here = min(32, T - t0);
+#pragma unroll 4
+        for (int u = 0; u < 32; ++u) {
+            if (u >= n_here) break;
+            const int32_t t = t0 + u;
+            const int st = t & (D - 1);
+            cp_async_wait<D - 1>();                               // slot t has landed
+            const float av = __shfl_sync(kFull, a0, u);
+            if (active) {
+                const float4 x = my[st * 32];
+                part[0] = fmaf(av, x.x, part[0]);
+                part[1] = fmaf(av, x.y, part[1]);
+                part[2] = fmaf(av, x.z, part[2]);
+                part[3] = fmaf(av, x.w, part[3]);
+            }
+            const int tn = u + D;                                 // refill: slot t + D
+            const int32_t cc = __shfl_sync(kFull, c0, tn & 31);
+            const int32_t cn = __shfl_sync(kFull, c1, tn & 31);
+            if (t + D < T) copy_slot(st, tn < 32 ? cc : cn);
+            cp_async_commit();
+            if ((j & 31) == 31) {                                 // the row's 32-slot chunk partial
+#pragma unroll
+                for (int q = 0; q < 4; ++q) { tot[q] += part[q]; part[q] = 0.0f; }
+            }
+            ++j;
+            if (t + 1 == cur_end) {                               // a5: the row is complete
+                const int32_t k = j;
+                int64_t div = k;
+                if (p.reduce == kMean && p.mean_by_degree) div = __shfl_sync(kFull, rs.d, cur);
+                float res[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    res[q] = finish(tot[q] + part[q], p.reduce, div);
+                    tot[q] = 0.0f;
+                    part[q] = 0.0f;
+                }
+                if (active) store_c<4>(p, r0 + cur, lane, res, pol_a);
+                const unsigned rest = nonempty & ~((2u << cur) - 1u);
+                cur = rest ? __ffs(rest) - 1 : 31;
+                cur_end = __shfl_sync(kFull, incl, cur);
+                j = 0;
+            }
+        }
+        c0 = c1;
+        a0 = a1;
+        load_slot(t0 + 64 + lane, c1, a1);
+    }
+    cp_async_wait<0>();
 }
 
 // ------------------------------------------------------------------ cp.async ring, two slots per step
@@ -904,6 +1058,28 @@ cudaError_t launch_cpasync(const SpmmParams& p, const Plan& plan, const Tune& t,
     }
 }
 
+template <int D, int R, int W, int MINW>
+cudaError_t launch_rowstream_k(const SpmmParams& p, cudaStream_t st) {
+    const int64_t warps = (p.n_rows + R - 1) / R;
+    const int64_t blocks = (warps + W - 1) / W;
+    const size_t smem = (size_t)W * D * 32 * 16;
+    spmm_rowstream<D, R, W, MINW><<<(unsigned)blocks, 32 * W, smem, st>>>(p);
+    return cudaGetLastError();
+}
+
+// rows per warp tune.width (8, 16 or 32; default 16), ring depth tune.stages (4 default; 8)
+cudaError_t launch_rowstream(const SpmmParams& p, const Tune& t, cudaStream_t st) {
+    const int R = t.width > 0 ? t.width : 16;
+    if (t.stages == 8) {
+        if (R <= 8) return launch_rowstream_k<8, 8, 4, 40>(p, st);
+        if (R <= 16) return launch_rowstream_k<8, 16, 4, 40>(p, st);
+        return launch_rowstream_k<8, 32, 4, 40>(p, st);
+    }
+    if (R <= 8) return launch_rowstream_k<4, 8, 4, 48>(p, st);
+    if (R <= 16) return launch_rowstream_k<4, 16, 4, 48>(p, st);
+    return launch_rowstream_k<4, 32, 4, 48>(p, st);
+}
+
 template <int VEC, int NCH>
 cudaError_t launch_warp(const SpmmParams& p, const Plan& plan, cudaStream_t st) {
     constexpr int U = NCH == 1 ? 8 : (NCH == 2 ? 4 : 2);
@@ -1005,7 +1181,8 @@ Plan make_plan_bf16(int64_t F, int64_t ldb, int64_t ldc, const void* B, const vo
     return pl;
 }
 
-Plan make_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C, int32_t s, const Tune& t) {
+Plan make_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C, int32_t s, const Tune& t,
+               int64_t k_est) {
     Plan pl{};
     const uintptr_t b = reinterpret_cast<uintptr_t>(B), c = reinterpret_cast<uintptr_t>(C);
     if (b % 16 == 0 && ldb % 4 == 0) pl.vec = 4;
@@ -1048,6 +1225,19 @@ Plan make_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C
         // Proteins 1.19 vs 1.30 ms); ES_KERNEL_CPASYNC forces the one-slot ring
         pl.halfwarp = pl.nch == 1 && ov != ES_KERNEL_CPASYNC;
     }
+    // row stream for short rows (64 < F <= 128): several rows per warp as one slot stream;
+    // forced with ES_KERNEL_ROWSTREAM (A/B; the auto plan keeps the two-slot ring, faster on the
+    // Arxiv-shaped graph, mean degree 14: profiles/r02.md)
+    if (k_est < 0) k_est = s;
+    const bool rs_ok = pl.vec == 4 && nv4 > 16 && nv4 <= 32;
+    if (rs_ok && (ov == ES_KERNEL_ROWSTREAM ||
+                  ((ov == ES_KERNEL_AUTO || ov == ES_KERNEL_FUSED) && k_est <= kRowStreamMaxK))) {
+        pl.rowstream = true;
+        pl.cpasync = pl.tma = pl.halfwarp = pl.subwarp = false;
+        pl.stages = t.stages == 8 ? 8 : 4;
+        pl.rows_per_warp = t.width > 0 ? t.width : 16;
+        return pl;
+    }
     if (pl.tma) {
         pl.nch = (int)((nv4 + 31) / 32);
         pl.subwarp = false;
@@ -1064,6 +1254,7 @@ Plan make_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C
 cudaError_t launch_spmm(SpmmParams p, const Plan& plan, const Tune& t, cudaStream_t st) {
     if (p.n_rows <= 0) return cudaSuccess;
     p.c_vec = plan.c_vec ? 1 : 0;
+    if (plan.rowstream) return launch_rowstream(p, t, st);
     if (plan.tma) return dispatch_tma(p, plan, st);
     if (plan.cpasync) return launch_cpasync(p, plan, t, st);
     switch (plan.vec) {

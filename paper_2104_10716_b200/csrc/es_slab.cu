@@ -303,7 +303,10 @@ spmm_slab_ldg(const SlabParams p) {
 // 8 lanes of a quarter-warp always touch 128 contiguous bytes (conflict-free for every G).
 // Per element: group e sums slots j = e (mod S) in slot order (32-slot-chunk partials), then
 // an xor tree over the groups (G = 16: spmm_cpasync_hw's order, bitwise).
-template <int G, int P, int D, int MINB, bool FULL, int W, bool BF16 = false>
+// LA2: the (col, val) chunk window looks two 32-slot chunks ahead instead of one (the chunk
+// loads queue behind the ring's copies in the L1 miss path; one chunk of lead time was the top
+// stall of the kernel, profiles/r02.md).
+template <int G, int P, int D, int MINB, bool FULL, int W, bool BF16 = false, bool LA2 = false>
 __global__ void __launch_bounds__(32 * W, MINB * 8 / W)
 spmm_slab(const SlabParams p) {
     constexpr int E = SlabPiece<BF16>::kElems;   // B elements (-> fp32 accumulators) per piece
@@ -342,10 +345,11 @@ spmm_slab(const SlabParams p) {
 
     // (col, val) of the chunk being consumed (c0, a0) and of the next one (c1, a1); slots past
     // k carry (0, 0.0f), so their (zero-filled) pieces add exactly +0.
-    int32_t c0 = 0, c1 = 0;
-    float a0 = 0.0f, a1 = 0.0f;
+    int32_t c0 = 0, c1 = 0, c2 = 0;
+    float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f;
     if (lane < k) load_pair(lane, c0, a0);
     if (32 + lane < k) load_pair(32 + lane, c1, a1);
+    if (LA2 && 64 + lane < k) load_pair(64 + lane, c2, a2);
 #pragma unroll
     for (int t = 0; t < D; ++t) {
         copy(t, __shfl_sync(kAll, c0, S * t + e), S * t + e < k);
@@ -383,9 +387,17 @@ spmm_slab(const SlabParams p) {
             for (int c = 0; c < E; ++c) { tot[q][c] += part[q][c]; part[q][c] = 0.0f; }
         c0 = c1;
         a0 = a1;
-        c1 = 0;
-        a1 = 0.0f;
-        if (j0 + 64 + lane < k) load_pair(j0 + 64 + lane, c1, a1);
+        if (LA2) {
+            c1 = c2;
+            a1 = a2;
+            c2 = 0;
+            a2 = 0.0f;
+            if (j0 + 96 + lane < k) load_pair(j0 + 96 + lane, c2, a2);
+        } else {
+            c1 = 0;
+            a1 = 0.0f;
+            if (j0 + 64 + lane < k) load_pair(j0 + 64 + lane, c1, a1);
+        }
     }
     cp_async_wait<0>();
     const uint64_t pol_a = policy_evict_first();
@@ -553,11 +565,218 @@ cudaError_t launch_tma_slab_w(const CUtensorMap& tm, const SlabParams& p, int32_
     return cudaGetLastError();
 }
 
-template <int G, int P, int D, int MINB, int W, bool BF16 = false>
+// ---------------------------------------------------------------- row-pipelined slab kernel
+// spmm_slab's gather-FMA with the per-row start-up taken off the critical path: one warp owns
+// R <= 32 consecutive rows (lane i holds row i's slot range) and streams their slots as ONE
+// sequence, each row padded to a multiple of S = 32/G slots (padding slots are zero-filled
+// copies: no memory access, and they add exactly +0), so every step's S slots belong to one row
+// and the cp.async ring stays D steps ahead ACROSS row boundaries -- the rowptr -> slots -> B
+// latency chain and the ring's fill/drain are paid once per R rows instead of once per row
+// (at ~43 steps per Reddit-shaped row they cost about a third of the per-row time; an ideal
+// stream of the same gathers reaches the L2 streaming rate, profiles/l2_peak.json gather_smem).
+// When the stream passes a row's last step the group partials are combined by the xor tree and
+// stored, exactly as spmm_slab does: same per-element order (group e sums slots j = e mod S in
+// slot order with 32-slot chunk partials counted from the row's first slot), bitwise.
+template <int G, int P, int D, int MINW, bool FULL, int W, int R, bool BF16>
+__global__ void __launch_bounds__(32 * W, MINW / W)
+spmm_slab_stream(const SlabParams p) {
+    constexpr int E = SlabPiece<BF16>::kElems;
+    constexpr int S = 32 / G;            // slots per step
+    constexpr int U = 32 / S;            // steps per 32-slot chunk (= G)
+    static_assert((G == 2 || G == 4 || G == 8 || G == 16) && G * P <= 16, "lanes x pieces per slot");
+    static_assert(D >= 2 && U % D == 0 && R >= 1 && R <= 32, "ring depth / rows per warp");
+    constexpr int kStage = 32 * P;
+    extern __shared__ __align__(16) float4 slab_ring[];          // [warps][D][P][S][G]
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int e = lane / G, sub = lane % G;
+    const int64_t r0 = ((int64_t)blockIdx.x * W + warp) * R;
+    if (r0 >= p.n_rows) return;
+    const int nr = (int)min((int64_t)R, p.n_rows - r0);
+    // row metadata in lane i < nr: slots [beg, beg + k), padded to kp = ceil(k / S) * S stream slots
+    const uint64_t pol = policy_evict_first();
+    int64_t beg = 0;
+    int32_t k = 0;
+    bool bad = false;
+    if (lane < nr) {
+        beg = ld_stream(p.s_rowptr + r0 + lane, pol) - p.slot_base;
+        int64_t end = ld_stream(p.s_rowptr + r0 + lane + 1, pol) - p.slot_base;
+        if (p.direct_s > 0 && end - beg > p.direct_s) end = beg + p.direct_s;
+        const bool sig_bad = p.ws_sig != nullptr && *p.ws_sig != p.sig;
+        bad = end > p.cap || sig_bad;
+        if (bad && p.ws_status) atomicOr(p.ws_status, (end > p.cap ? kWsOverflow : 0) | (sig_bad ? kWsSignature : 0));
+        k = (!bad && end > beg) ? (int32_t)(end - beg) : 0;
+    }
+    // rows the guards tripped on: NaN; empty rows: zeros (no division) -- whole-warp stores
+    unsigned special = __ballot_sync(kAll, lane < nr && (bad || k == 0));
+    while (special) {
+        const int i = __ffs(special) - 1;
+        special &= special - 1;
+        if (__shfl_sync(kAll, (int)bad, i)) {
+            slab_poison_row(p, r0 + i);
+        } else {
+            for (int c = lane; c < p.w; c += 32) {
+                if (p.n_peers == 0) p.C[(r0 + i) * p.ldc + c] = 0.0f;
+                else
+                    for (int q = 0; q < p.n_peers; ++q) p.c_peers[q][(p.row_base + r0 + i) * p.ldc + p.col0 + c] = 0.0f;
+            }
+        }
+    }
+    const int32_t kp = (k + S - 1) / S * S;
+    int32_t incl = kp;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t v = __shfl_up_sync(kAll, incl, o);
+        if (lane >= o) incl += v;
+    }
+    const int32_t TP = __shfl_sync(kAll, incl, 31);              // stream length (slots)
+    if (TP == 0) return;
+    const unsigned nonempty = __ballot_sync(kAll, k > 0);
+
+    const uint32_t my_s = smem_u32(slab_ring + (size_t)warp * D * kStage + e * G + sub);
+    const char* bl = reinterpret_cast<const char*>(p.B) + sub * 16;
+    const uint32_t row_bytes = (uint32_t)(p.ldb * (BF16 ? 2 : 4));
+    // (col, val) of stream slot t, one slot per lane: col = -1 marks a padding slot
+    auto load_slot = [&](int32_t t, int32_t& c, float& a) {
+        int lo = 0;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+            const int32_t v = __shfl_sync(kAll, incl, lo + step - 1);
+            if (v <= t) lo += step;
+        }
+        const int i = lo > 31 ? 31 : lo;
+        const int64_t b = __shfl_sync(kAll, beg, i);
+        const int32_t ki = __shfl_sync(kAll, k, i);
+        const int32_t j = t - (__shfl_sync(kAll, incl, i) - __shfl_sync(kAll, kp, i));
+        c = -1;
+        a = 0.0f;
+        if (t < TP && j < ki) {
+            c = ld_stream(p.s_colind + b + j, pol);
+            a = p.s_val ? ld_stream(p.s_val + b + j, pol) : 1.0f;
+        }
+    };
+    auto copy = [&](int stage, int32_t col) {
+        const bool valid = col >= 0;
+        const char* src = bl + (uint64_t)(uint32_t)(valid ? col : 0) * row_bytes;
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            const bool on = FULL ? valid : (valid && sub + G * q < p.nv);
+            cp_async16_zfill(my_s + (stage * kStage + q * 32) * 16, src + q * G * 16, on ? 16u : 0u);
+        }
+    };
+    int32_t c0, c1;
+    float a0, a1;
+    load_slot(lane, c0, a0);
+    load_slot(32 + lane, c1, a1);
+#pragma unroll
+    for (int t = 0; t < D; ++t) {
+        copy(t, __shfl_sync(kAll, c0, S * t + e));
+        cp_async_commit();
+    }
+    float part[P][E], tot[P][E];
+#pragma unroll
+    for (int q = 0; q < P; ++q)
+#pragma unroll
+        for (int c = 0; c < E; ++c) { part[q][c] = 0.0f; tot[q][c] = 0.0f; }
+    int cur = __ffs(nonempty) - 1;                               // row being accumulated
+    int32_t cur_end = __shfl_sync(kAll, incl, cur) / S;          // its last stream step + 1
+    int32_t js = 0;                                              // step index within the row
+    const int32_t TS = TP / S;
+    // one step per iteration (not unrolled: the row epilogue below exists once in the code)
+#pragma unroll 1
+    for (int32_t ts = 0; ts < TS; ++ts) {
+        const int u = ts & (U - 1);                              // step within the stream chunk
+        const int d = ts & (D - 1);                              // ring stage
+        cp_async_wait<D - 1>();                                  // step ts has landed
+        const float av = __shfl_sync(kAll, a0, S * u + e);
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            float x[E];
+            SlabPiece<BF16>::widen(lds128(my_s + (d * kStage + q * 32) * 16), x);
+#pragma unroll
+            for (int c = 0; c < E; ++c) part[q][c] = fmaf(av, x[c], part[q][c]);
+        }
+        const int tn = u + D;                                    // refill: stream step ts + D
+        const int32_t cn = __shfl_sync(kAll, tn < U ? c0 : c1, (S * tn + e) & 31);
+        copy(d, ts + D < TS ? cn : -1);
+        cp_async_commit();
+        if (u == U - 1) {                                        // the stream chunk is consumed
+            c0 = c1;
+            a0 = a1;
+            load_slot(S * (ts + 1 + U) + lane, c1, a1);
+        }
+        ++js;
+        const bool row_done = ts + 1 == cur_end;
+        if ((js & (U - 1)) == 0 || row_done) {                   // the row's 32-slot chunk partial
+#pragma unroll
+            for (int q = 0; q < P; ++q)
+#pragma unroll
+                for (int c = 0; c < E; ++c) { tot[q][c] += part[q][c]; part[q][c] = 0.0f; }
+        }
+        if (row_done) {                                          // a5: row r0 + cur is complete
+            const int32_t kc = __shfl_sync(kAll, k, cur);
+            int64_t div = kc;
+            if (p.reduce == kMean && p.mean_by_degree)
+                div = ld_stream(p.rowptr + r0 + cur + 1, pol) - ld_stream(p.rowptr + r0 + cur, pol);
+#pragma unroll
+            for (int o = G; o < 32; o <<= 1)
+#pragma unroll
+                for (int q = 0; q < P; ++q)
+#pragma unroll
+                    for (int c = 0; c < E; ++c) {
+                        const float other = __shfl_xor_sync(kAll, tot[q][c], o);
+                        tot[q][c] = (lane & o) ? other + tot[q][c] : tot[q][c] + other;
+                    }
+            if (e == 0) {
+#pragma unroll
+                for (int q = 0; q < P; ++q) {
+                    const int piece = sub + G * q;
+                    if (FULL || piece < p.nv) slab_store_piece<E>(p, r0 + cur, piece * E, tot[q], div, pol);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < P; ++q)
+#pragma unroll
+                for (int c = 0; c < E; ++c) tot[q][c] = 0.0f;
+            const unsigned rest = nonempty & ~((2u << cur) - 1u);
+            cur = rest ? __ffs(rest) - 1 : 31;
+            cur_end = __shfl_sync(kAll, incl, cur) / S;
+            js = 0;
+        }
+    }
+    cp_async_wait<0>();
+}
+
+template <int G, int P, int D, int MINW, int W, int R>
+cudaError_t launch_slab_stream_w(const SlabParams& p, cudaStream_t st) {
+    const int64_t warps = (p.n_rows + R - 1) / R;
+    const int64_t blocks = (warps + W - 1) / W;
+    const size_t smem = (size_t)W * D * 32 * P * 16;
+    auto k = p.nv == G * P ? spmm_slab_stream<G, P, D, MINW, true, W, R, false>
+                           : spmm_slab_stream<G, P, D, MINW, false, W, R, false>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    k<<<(unsigned)blocks, 32 * W, smem, st>>>(p);
+    return cudaGetLastError();
+}
+
+// rows per warp = tune.variant >> 8 (2, 4 default, 8, 16), warps per CTA 4
+template <int G, int P, int D, int MINW>
+cudaError_t launch_slab_stream_k(const SlabParams& p, const Tune& t, cudaStream_t st) {
+    const int R = (t.variant >> 8) & 0xff;
+    if (R == 2) return launch_slab_stream_w<G, P, D, MINW, 4, 2>(p, st);
+    if (R == 8) return launch_slab_stream_w<G, P, D, MINW, 4, 8>(p, st);
+    if (R == 16) return launch_slab_stream_w<G, P, D, MINW, 4, 16>(p, st);
+    return launch_slab_stream_w<G, P, D, MINW, 4, 4>(p, st);
+}
+
+template <int G, int P, int D, int MINB, int W, bool BF16 = false, bool LA2 = false>
 cudaError_t launch_slab_w(const SlabParams& p, cudaStream_t st) {
     const int64_t blocks = (p.n_rows + W - 1) / W;
     const size_t smem = (size_t)W * D * 32 * P * 16;
-    auto k = p.nv == G * P ? spmm_slab<G, P, D, MINB, true, W, BF16> : spmm_slab<G, P, D, MINB, false, W, BF16>;
+    auto k = p.nv == G * P ? spmm_slab<G, P, D, MINB, true, W, BF16, LA2> : spmm_slab<G, P, D, MINB, false, W, BF16, LA2>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -567,7 +786,10 @@ cudaError_t launch_slab_w(const SlabParams& p, cudaStream_t st) {
 }
 
 template <int G, int D, int MINB, int P = 16 / G>
-cudaError_t launch_slab_k(const SlabParams& p, int cta_warps, cudaStream_t st) {
+cudaError_t launch_slab_k(const SlabParams& p, int cta_warps, cudaStream_t st, bool la2 = false) {
+    if constexpr (G != 16)
+        if (la2) return cta_warps == 2 ? launch_slab_w<G, P, D, MINB, 2, false, true>(p, st)
+                                       : launch_slab_w<G, P, D, MINB, 4, false, true>(p, st);
     if (cta_warps == 1) return launch_slab_w<G, P, D, MINB, 1>(p, st);
     if (cta_warps == 2) return launch_slab_w<G, P, D, MINB, 2>(p, st);
     if (cta_warps == 8) return launch_slab_w<G, P, D, MINB, 8>(p, st);
@@ -690,6 +912,11 @@ cudaError_t launch_slab_pass(const SlabParams& p, const Tune& t, cudaStream_t st
         if (t.stages == 2) return launch_ldg_k<8, 1, 2, 24, false>(p, t, st);
         return launch_ldg_k<8, 1, 4, 16, false>(p, t, st);
     }
+    if (t.kernel == ES_KERNEL_SLAB_STREAM && !p.b_bf16) {
+        if (p.nv <= 4) return launch_slab_stream_k<2, 2, 2, 32>(p, t, st);
+        if (p.nv <= 8) return launch_slab_stream_k<4, 2, 4, 32>(p, t, st);
+        return launch_slab_stream_k<8, 2, 4, 28>(p, t, st);
+    }
     const int cw = t.cta_warps;
     if (p.b_bf16) {                      // bf16 B (NEXT-4): 128-element slices, 8 elements per piece
         if (p.nv <= 4) return launch_slab_w<2, 2, 2, 3, 4, true>(p, st);
@@ -706,12 +933,15 @@ cudaError_t launch_slab_pass(const SlabParams& p, const Tune& t, cudaStream_t st
     }
     // narrow last slice: 4 lanes x 2 pieces (8 slots per step) for <= 8 pieces, 2 x 2 (16 slots
     // per step) for <= 4 -- half / a quarter of the steps of a full slice
-    if (p.nv <= 4) return launch_slab_k<2, 2, 4, 2>(p, cw, st);
-    if (p.nv <= 8) return launch_slab_k<4, 4, 4, 2>(p, cw, st);
+    const bool la2 = (t.variant & 1) != 0;  // A/B: two-chunk (col, val) lookahead
+    if (p.nv <= 4) return launch_slab_k<2, 2, 4, 2>(p, cw, st, la2);
+    if (p.nv <= 8) return launch_slab_k<4, 4, 4, 2>(p, cw, st, la2);
     switch (t.stages) {
         case 2: return launch_slab_k<8, 2, 4>(p, cw, st);
         case 8: return launch_slab_k<8, 8, 4>(p, cw, st);
-        default: return launch_slab_k<8, 4, 4>(p, cw, st);
+        default:
+            if (t.variant & 2) return launch_slab_k<8, 4, 3>(p, cw, st, la2);   // 80-register cap
+            return launch_slab_k<8, 4, 4>(p, cw, st, la2);
     }
 }
 

@@ -1,15 +1,20 @@
 #!/bin/bash
-# One GPU round: smoke, gpu tests, bench, ncu launch list + full capture of the hot kernel.
+# One GPU round: L2 peak probe, smoke, gpu tests, bench, ncu launch list + full capture of the hot kernel.
 # Usage (from this container): gpurun --timeout 2400 -- 'bash scripts/gpu_round.sh <tag> [bench args...]'
+#   SKIP_TESTS=1 / SKIP_NCU=1 / L2PEAK=1 (re-measure profiles/l2_peak.json into gpurun_out/<tag>/)
 set -u
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
-TAG=${1:-r01}; shift || true
+TAG=${1:-r02}; shift || true
 OUT=gpurun_out/$TAG
 mkdir -p "$OUT"
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > "$OUT/gpu.txt" 2>&1
+if [ "${L2PEAK:-0}" = "1" ]; then
+  timeout 300 python scripts/l2_peak.py "$OUT/l2_peak.json" > "$OUT/l2_peak.log" 2>&1
+  cp "$OUT/l2_peak.json" profiles/l2_peak.json 2>/dev/null
+fi
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > "$OUT/smoke.log" 2>&1; echo "smoke rc=$?" >> "$OUT/smoke.log"
 if [ "${SKIP_TESTS:-0}" != "1" ]; then
-  timeout 1500 python -m pytest tests -m gpu -q > "$OUT/pytest_gpu.log" 2>&1; echo "pytest rc=$?" >> "$OUT/pytest_gpu.log"
+  timeout 2400 python -m pytest tests -m gpu -q -x > "$OUT/pytest_gpu.log" 2>&1; echo "pytest rc=$?" >> "$OUT/pytest_gpu.log"
 fi
 timeout 900 python bench.py "$@" > "$OUT/bench.json" 2> "$OUT/bench.err"; echo "bench rc=$?" >> "$OUT/bench.err"
 if [ "${SKIP_NCU:-0}" != "1" ]; then

@@ -11,6 +11,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <vector>
 #include <cuda_runtime.h>
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { \
@@ -86,6 +87,79 @@ __global__ void gather_smem(const float4* __restrict__ slab, uint32_t nrows, lon
   if (acc == 1234.5f) *sink = acc;
 }
 
+// gather_smem + the slab kernel's per-step work: row indices from a coalesced index array in a
+// 32-slot chunk window (one chunk ahead), the column broadcast by shuffle, a value broadcast, 8 FMAs
+// per lane per step -- no row boundaries (an endless row).  MODE 0: all of it; 1: no FMA/value;
+// 2: hashed indices (no index loads) but with FMAs
+template <int D, int MODE>
+__global__ void gather_smem_fma(const float4* __restrict__ slab, const int* __restrict__ idx, long steps,
+                                float* sink) {
+  extern __shared__ float4 ring[];
+  const int lane = threadIdx.x & 31, e = lane >> 3, sub = lane & 7, w = threadIdx.x >> 5;
+  const long warp = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int* my_idx = idx + warp * steps * 4;
+  float4* my = ring + (size_t)w * D * 64 + e * 16 + sub;
+  auto copy = [&](int d, int row) {
+    const float4* src = slab + (size_t)row * 16 + sub;
+    const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(my + d * 64);
+    if (MODE == 3) {                                   // the zero-fill (src-size) form the kernel uses
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" :: "r"(s0), "l"(src), "r"(16) : "memory");
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" :: "r"(s0 + 128), "l"(src + 8), "r"(16) : "memory");
+    } else {
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(s0), "l"(src) : "memory");
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(s0 + 128), "l"(src + 8) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  auto row_of = [&](long slot, int c_lane) {
+    if (MODE == 2) return (int)(hash32((uint64_t)(warp * steps * 4 + slot)) % 245760u);
+    return c_lane;
+  };
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  auto ldi = [&](const int* q) {             // MODE 4: the kernel's ld_stream (L1::no_allocate + evict_first)
+    if (MODE != 4) return __ldcs(q);
+    int v;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(q), "l"(pol));
+    return v;
+  };
+  int c0 = MODE == 2 ? 0 : ldi(my_idx + lane), c1 = MODE == 2 ? 0 : ldi(my_idx + 32 + lane);
+  float a0 = 1.0f;
+  float part[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+  for (int d = 0; d < D; ++d) copy(d, row_of(4 * d + e, __shfl_sync(~0u, c0, 4 * d + e)));
+  const long nslots = steps * 4;
+  for (long j0 = 0; j0 < nslots; j0 += 32) {
+#pragma unroll 1
+    for (int u0 = 0; u0 < 8; u0 += D) {
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        const int u = u0 + d;
+        asm volatile("cp.async.wait_group %0;" :: "n"(D - 1) : "memory");
+        const float4 a = my[d * 64], b = my[d * 64 + 8];
+        if (MODE == 1) {
+          part[0] += a.x + b.w;
+        } else {
+          const float av = __shfl_sync(~0u, a0, 4 * u + e);
+          part[0] = fmaf(av, a.x, part[0]); part[1] = fmaf(av, a.y, part[1]);
+          part[2] = fmaf(av, a.z, part[2]); part[3] = fmaf(av, a.w, part[3]);
+          part[4] = fmaf(av, b.x, part[4]); part[5] = fmaf(av, b.y, part[5]);
+          part[6] = fmaf(av, b.z, part[6]); part[7] = fmaf(av, b.w, part[7]);
+        }
+        const int tn = u + D;
+        const int cn = __shfl_sync(~0u, tn < 8 ? c0 : c1, (4 * tn + e) & 31);
+        copy(d, row_of(j0 + 4 * tn + e, cn));
+      }
+    }
+    c0 = c1;
+    if (MODE != 2) c1 = (j0 + 64 + 32 <= nslots) ? ldi(my_idx + j0 + 64 + lane) : 0;
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  float acc = 0.f;
+  for (int i = 0; i < 8; ++i) acc += part[i];
+  if (acc == 1234.5f) *sink = acc;
+}
+
 int main() {
   int nsm = 148, dev = 0, sm_clk = 0;
   CK(cudaGetDevice(&dev));
@@ -138,6 +212,34 @@ int main() {
       ms = time_best([&] { gather_smem<4><<<grid, threads, smem>>>(buf, nrows, steps, sink); }, 3);
       printf("{\"probe\":\"gather_smem\",\"row_B\":256,\"footprint_MB\":%.0f,\"warps_per_sm\":%d,\"ring_depth\":4,\"GBps\":%.1f}\n",
              X / 1048576.0, wps, bytes / ms / 1e6);
+    }
+  }
+  {  // the slab kernel's inner loop as a probe: 60 MB slab, endless rows, index array in HBM
+    const uint32_t nrows = (uint32_t)((60u << 20) / 256);
+    const long steps = 4096;
+    const int threads = 128;                             // 4-warp CTAs as es::spmm_slab
+    for (int wps : {24, 32}) {
+      const int grid = nsm * wps / 4;
+      const long nidx = (long)grid * 4 * steps * 4;
+      int* idx;
+      CK(cudaMalloc(&idx, (nidx + 64) * sizeof(int)));
+      std::vector<int> h(nidx + 64);
+      uint64_t x = 0x9E3779B97F4A7C15ull;
+      for (long i = 0; i < nidx + 64; ++i) { x ^= x << 13; x ^= x >> 7; x ^= x << 17; h[i] = (int)(x % nrows); }
+      CK(cudaMemcpy(idx, h.data(), (nidx + 64) * sizeof(int), cudaMemcpyHostToDevice));
+      const double bytes = (double)grid * 4 * steps * 4 * 256;
+      const size_t smem = (size_t)4 * 4 * 64 * 16;
+      float ms = time_best([&] { gather_smem_fma<4, 0><<<grid, threads, smem>>>(buf, idx, steps, sink); }, 3);
+      printf("{\"probe\":\"slab_inner_loop\",\"mode\":\"index loads + shuffles + FMA\",\"warps_per_sm\":%d,\"GBps\":%.1f}\n", wps, bytes / ms / 1e6);
+      ms = time_best([&] { gather_smem_fma<4, 1><<<grid, threads, smem>>>(buf, idx, steps, sink); }, 3);
+      printf("{\"probe\":\"slab_inner_loop\",\"mode\":\"index loads + shuffles, no FMA\",\"warps_per_sm\":%d,\"GBps\":%.1f}\n", wps, bytes / ms / 1e6);
+      ms = time_best([&] { gather_smem_fma<4, 2><<<grid, threads, smem>>>(buf, idx, steps, sink); }, 3);
+      printf("{\"probe\":\"slab_inner_loop\",\"mode\":\"hashed rows + FMA\",\"warps_per_sm\":%d,\"GBps\":%.1f}\n", wps, bytes / ms / 1e6);
+      ms = time_best([&] { gather_smem_fma<4, 4><<<grid, threads, smem>>>(buf, idx, steps, sink); }, 3);
+      printf("{\"probe\":\"slab_inner_loop\",\"mode\":\"index loads L1::no_allocate + L2 evict_first hint + FMA\",\"warps_per_sm\":%d,\"GBps\":%.1f}\n", wps, bytes / ms / 1e6);
+      ms = time_best([&] { gather_smem_fma<4, 3><<<grid, threads, smem>>>(buf, idx, steps, sink); }, 3);
+      printf("{\"probe\":\"slab_inner_loop\",\"mode\":\"index loads + FMA, zero-fill cp.async form\",\"warps_per_sm\":%d,\"GBps\":%.1f}\n", wps, bytes / ms / 1e6);
+      cudaFree(idx);
     }
   }
   CK(cudaGetLastError());

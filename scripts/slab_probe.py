@@ -4,6 +4,10 @@ es_spmm_options_t.kernel / tune[] (paper_2104_10716_b200.kernel_override).
 
   python scripts/slab_probe.py [config] [F] [s] [strategy]      # default reddit 602 256 fastrand
   SLAB_VARIANTS="slab_ldg:4:0:4:0,slab_smem:4:8:4:0"   kernel:stages:width:cta_warps:variant
+  UNIFORM_COLS=1: the same degree sequence with uniformly random columns (no popularity skew)
+  CONST_DEG=d: nnz/d rows of degree d each, uniform columns (isolates per-row costs)
+  NOVAL=1: val = NULL (the unweighted adjacency; no slot values stored or read)
+  NOFLUSH=1: no L2 flush between reps (warm L2; F <= 64 then repeats one L2-resident slab)
 
 Each variant: the whole step (L2 flushed before every rep, like bench.py) and the slice passes
 alone (reuse_sampled, L2 flushed), median of 8, plus the max difference to the fused kernel's C
@@ -34,19 +38,29 @@ def main():
     n = len(rowptr) - 1
     K = int(np.minimum(np.diff(rowptr), s).sum())
     Bd = torch.from_numpy(synth.dense(n, F, synth.seeds(cfg)[1], ld=ldb)).to(dev)
+    if os.environ.get("UNIFORM_COLS"):        # same degree sequence, columns uniform over [0, n): no popularity skew
+        colind = np.random.default_rng(5).integers(0, n, len(colind), dtype=np.int64).astype(np.int32)
+    if os.environ.get("CONST_DEG"):           # every row the same degree (isolates per-row costs), uniform columns
+        dg = int(os.environ["CONST_DEG"])
+        m = len(colind) // dg
+        rowptr = (np.arange(m + 1, dtype=np.int64) * dg)
+        colind = np.random.default_rng(5).integers(0, n, m * dg, dtype=np.int64).astype(np.int32)
+        K = int(np.minimum(np.diff(rowptr), s).sum())
     rp = torch.from_numpy(rowptr).to(dev)
     ci = torch.from_numpy(colind).to(dev)
-    va = torch.ones(len(colind), dtype=torch.float32, device=dev)
-    C = torch.zeros((n, ldb), dtype=torch.float32, device=dev)
-    C2 = torch.zeros((n, ldb), dtype=torch.float32, device=dev)
+    va = None if os.environ.get("NOVAL") else torch.ones(len(colind), dtype=torch.float32, device=dev)
+    nr = len(rowptr) - 1
+    C = torch.zeros((nr, ldb), dtype=torch.float32, device=dev)
+    C2 = torch.zeros((nr, ldb), dtype=torch.float32, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    bm = byte_model(K, n, F)
+    bm = byte_model(K, nr, F)
     reps = int(os.environ.get("REPS", 8))
 
     def timed(fn):
         ts = []
         for i in range(3 + reps):
-            flush.zero_()
+            if not os.environ.get("NOFLUSH"):
+                flush.zero_()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
@@ -66,7 +80,7 @@ def main():
         f = v.split(":")
         kern = f[0]
         tune = [int(x) for x in f[1:]] + [0] * (5 - len(f))
-        ws = es.es_spmm_workspace(n, n, len(colind), F, ldb, s, True, device=dev, kernel=kern)
+        ws = es.es_spmm_workspace(nr, n, len(colind), F, ldb, s, va is not None, device=dev, kernel=kern)
         C2.zero_()
         kw = dict(F=F, C=C2, workspace=ws, kernel=kern, tune=tune[:4])
         try:

@@ -42,7 +42,8 @@ def to_dev(rowptr, colind, val):
             None if val is None else torch.from_numpy(np.ascontiguousarray(val)).to(DEV))
 
 
-SLAB_KERNELS = (es.ES_KERNEL_SLAB, es.ES_KERNEL_SLAB_SMEM, es.ES_KERNEL_SLAB_LDG, es.ES_KERNEL_SLAB_TMA)
+SLAB_KERNELS = (es.ES_KERNEL_SLAB, es.ES_KERNEL_SLAB_SMEM, es.ES_KERNEL_SLAB_LDG, es.ES_KERNEL_SLAB_TMA,
+                es.ES_KERNEL_SLAB_STREAM)
 FORCED_RUNS = {"forced": 0, "fallback": 0}
 
 
@@ -131,7 +132,8 @@ FS = [(1, 1), (3, 3), (3, 4), (7, 8), (16, 16), (17, 17), (32, 32), (64, 64), (1
 KERNEL_PARAMS = {                       # name -> (kernel family, tune: stages, width, cta_warps, variant)
     "auto": ("auto", ()), "warp": ("warp", ()), "tma": ("tma", ()), "cpasync": ("cpasync", ()),
     "halfwarp": ("halfwarp", ()), "slab": ("slab", ()), "slab16": ("slab_smem", (0, 16)),
-    "slab_ldg": ("slab_ldg", ()), "slab_tma": ("slab_tma", ()),
+    "slab_ldg": ("slab_ldg", ()), "slab_tma": ("slab_tma", ()), "slab_stream": ("slab_stream", (0, 0, 0, 1024)),
+    "rowstream": ("rowstream", ()),
 }
 
 
@@ -182,6 +184,21 @@ def test_ones_give_exact_counts(ragged, kernel):
                 assert np.array_equal(g, np.repeat(np.minimum(d, s)[:, None], F, 1).astype(np.float32))
                 gm = run_gpu(rowptr, colind, None, B, s, strat, seed=3, reduce=ES_REDUCE_MEAN, F=F)
                 assert np.array_equal(gm, np.repeat((d > 0)[:, None], F, 1).astype(np.float32))
+
+
+@pytest.mark.parametrize("F", [65, 100, 128])
+@pytest.mark.parametrize("rows", [8, 16, 32])
+def test_rowstream_bitwise_cpasync(ragged, F, rows):
+    """The row stream (several rows per warp as one slot stream) sums each row exactly as the
+    one-slot cp.async ring does (32-slot chunk partials from the row's first slot): bitwise."""
+    rowptr, colind, val = ragged
+    B = synth.dense(3001, F, seed=F, ld=(F + 3) // 4 * 4)
+    for s, strat in ((16, ES_FASTRAND), (64, ES_BUCKET), (700, ES_FASTRAND)):
+        with es.kernel_override("cpasync"):
+            a = run_gpu(rowptr, colind, val, B, s, strat, 5, ES_REDUCE_MEAN, F=F)
+        with es.kernel_override("rowstream", 0, rows):
+            b = run_gpu(rowptr, colind, val, B, s, strat, 5, ES_REDUCE_MEAN, F=F)
+        assert np.array_equal(a, b), (F, rows, s)
 
 
 def test_s1_bitwise_single_product(ragged):

@@ -33,12 +33,14 @@ def graph():
     return synth.random_csr(1301, 2300, seed=41, max_deg=400, special=(577, 1154, 1009, 300, 65, 33, 1))
 
 
-@pytest.fixture(params=["smem8", "smem16", "ldg", "tma"])
+@pytest.fixture(params=["smem8", "smem16", "ldg", "tma", "stream2", "stream8"])
 def lanes(request):
     """Each slab kernel, forced: the shared-memory ring with 8 / 16 lanes per slot, the
-    register-direct 256-bit kernel (32-B row pitches; else the plan's), the TMA gather4 kernel."""
+    register-direct 256-bit kernel (32-B row pitches; else the plan's), the TMA gather4 kernel,
+    the row-pipelined stream (2 / 8 rows per warp)."""
     fam, tune = {"smem8": ("slab_smem", (0, 8)), "smem16": ("slab_smem", (0, 16)), "ldg": ("slab_ldg", ()),
-                 "tma": ("slab_tma", ())}[request.param]
+                 "tma": ("slab_tma", ()), "stream2": ("slab_stream", (0, 0, 0, 512)),
+                 "stream8": ("slab_stream", (0, 0, 0, 2048))}[request.param]
     with es.kernel_override(fam, *tune):
         yield request.param
 
@@ -129,12 +131,13 @@ def test_slab_kernels_same_order_bitwise(graph, F, ld):
     rowptr, colind, val = graph
     B = synth.dense(2300, F, seed=14, ld=ld)
     outs = {}
-    for fam in ("slab_smem", "slab_ldg", "slab_tma"):
+    for fam in ("slab_smem", "slab_ldg", "slab_tma", "slab_stream"):
         with es.kernel_override(fam):
             outs[fam] = slab(rowptr, colind, val, B, 256, 2, 7, 1, F)
     full = (F // 64) * 64
     assert np.array_equal(outs["slab_smem"][:, :full], outs["slab_ldg"][:, :full])
     assert np.array_equal(outs["slab_smem"][:, :full], outs["slab_tma"][:, :full])
+    assert np.array_equal(outs["slab_smem"], outs["slab_stream"])         # same narrow-slice kernels too
 
 
 def test_slab_row_blocks_bitwise(graph, lanes):
