@@ -68,6 +68,13 @@ def parse():
     ap.add_argument("--allgather", action="store_true",
                     help="NEXT-1 variant: the C all-gather fused into the SpMM epilogue (every rank "
                          "stores its rows into all ranks' C over peer memory); N > 1")
+    ap.add_argument("--allgather-mc", action="store_true",
+                    help="the C all-gather fused into the epilogue through the NVLS multicast address of a "
+                         "torch symmetric-memory C (multimem.st: one store per row reaches every rank)")
+    ap.add_argument("--b-sharded", action="store_true",
+                    help="B sharded by equal node blocks (the output of a previous layer): each step "
+                         "all-gathers B one 256-B feature slice at a time on a side stream, overlapped with "
+                         "the previous slice's slab pass (paper_2104_10716_b200.dist.BShardedSpMM)")
     ap.add_argument("--bf16", action="store_true",
                     help="NEXT-4 sensitivity variant: B stored as bf16 (fp32 accumulation); not the headline")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
@@ -197,6 +204,9 @@ def time_oracle(rowptr, colind, val, B, a, strat, red, rows):
 
 
 def cpu_baseline(rowptr, colind, val, B, a, strat, red, steps=1):
+    """The oracle as it stands on the host cores (SURVEY 8(d) timing protocol): the fp64 parity
+    oracle on every core (the reported value), plus the same sample in the fp32-FMA timing mode
+    (a straightforward CPU port of Alg. 1) and the fp64 oracle on ONE core (a 1/cores sample)."""
     import oracle
     cores = oracle.max_threads()
     rows, m = oracle_sample_rows(rowptr, a.s, a.F, a.cpu_seconds, cores)
@@ -204,10 +214,26 @@ def cpu_baseline(rowptr, colind, val, B, a, strat, red, steps=1):
     Ks = int(np.minimum(d[rows], a.s).sum())
     ts = [time_oracle(rowptr, colind, val, B, a, strat, red, rows) for _ in range(steps)]
     t = float(np.median(ts))
-    return {"value": 2.0 * a.F * Ks / t / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
+    gf = lambda k, sec: 2.0 * a.F * k / sec / 1e9
+    t0 = time.perf_counter()
+    oracle.spmm_f32(rowptr, colind, val, B, a.s, strat, seed=a.seed, reduce=red, F=a.F, rows=rows)
+    t32 = time.perf_counter() - t0
+    rows1 = rows[::max(1, cores)]
+    K1 = int(np.minimum(d[rows1], a.s).sum())
+    oracle.set_threads(1)
+    try:
+        t1 = time_oracle(rowptr, colind, val, B, a, strat, red, rows1)
+    finally:
+        oracle.set_threads(cores)
+    return {"value": gf(Ks, t), "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
             "sample": f"every {m}-th row of the same workload ({len(rows)} rows, {Ks} sampled edges), "
                       f"fp64 C oracle (oracle/es_oracle.c, -O2, OpenMP {cores} threads), "
-                      f"median of {steps}, {t:.2f} s"}, t
+                      f"median of {steps}, {t:.2f} s",
+            "fp32_fma": {"value": round(gf(Ks, t32), 3), "cores": cores, "seconds": round(t32, 3),
+                         "what": "the same sample, fp32 FMA accumulation in slot order (oracle.spmm_f32, "
+                                 "timing mode only)"},
+            "single_thread": {"value": round(gf(K1, t1), 3), "cores": 1, "seconds": round(t1, 3),
+                              "sample": f"every {m * max(1, cores)}-th row ({len(rows1)} rows, {K1} sampled edges)"}}, t
 
 
 # ------------------------------------------------------------------ main
@@ -265,19 +291,39 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
-    peers = None
+    peers = mcast = bsh = None
     if a.allgather:
         from paper_2104_10716_b200.dist import PeerBuffers
         peers = PeerBuffers(n, C_d.stride(0), device=dev)
+    if a.allgather_mc:
+        from paper_2104_10716_b200.dist import MulticastC
+        mcast = MulticastC(n, C_d.stride(0), device=dev)
+    B_local = None
+    if a.b_sharded:
+        from paper_2104_10716_b200.dist import BShardedSpMM
+        bsh = BShardedSpMM(n, F, world, rank, dev)
+        b0, b1 = int(bsh.blocks[rank]), int(bsh.blocks[rank + 1])
+        B_local = B_d[b0:b1].contiguous()
+        del B_d                                            # this rank holds its block only
+        B_d = B_local
     # the library's plan: a workspace (allocated once, outside the timed region) selects the
     # feature-sliced path when B does not fit L2 but a 64-float slab of it does
     slab_family = a.kernel in ("auto", "slab", "slab_smem", "slab_ldg", "slab_tma", "slab_stream")
     ws = (es.es_spmm_workspace(r1 - r0, n, e1 - e0, F, ldb, a.s, True, device=dev,
                                kernel=None if a.kernel == "auto" else a.kernel) if slab_family else None)
+    if bsh is not None:                                    # one 64-float slice per call: force the slab path
+        ws = es.es_spmm_workspace(r1 - r0, n, e1 - e0, 64, 64, a.s, True, device=dev, kernel="slab")
     kern = None if a.kernel == "auto" else a.kernel
 
     def launch(st, reuse=False):
-        if peers is not None:
+        if bsh is not None:
+            bsh(rp_d, ci_d, va_d, B_local, a.s, strat_id, a.seed, red_id, C_d, n_rows=n, row_begin=r0,
+                row_end=r1, nnz_base=e0, nnz=e1 - e0, workspace=ws, stream=st)
+        elif mcast is not None:
+            es.es_spmm_run_ex(rp_d, ci_d, va_d, B_d, a.s, strat_id, a.seed, red_id, F=F, C=mcast.C,
+                              row_begin=r0, row_end=r1, n_rows=n, nnz_base=e0, c_multicast=mcast.multicast,
+                              workspace=ws, nnz=e1 - e0, kernel=kern, reuse_sampled=reuse, stream=st)
+        elif peers is not None:
             es.es_spmm_run_ex(rp_d, ci_d, va_d, B_d, a.s, strat_id, a.seed, red_id, F=F, C=peers.C,
                               row_begin=r0, row_end=r1, n_rows=n, nnz_base=e0, c_peers=peers.peers,
                               n_peers=peers.world, workspace=ws, nnz=e1 - e0, kernel=kern, reuse_sampled=reuse,
@@ -459,9 +505,13 @@ def main():
                        "sampling_rate": round(K_all / nnz, 4), "F": F, "ldb": ldb, "s": a.s,
                        "strategy": a.strategy, "reduce": a.reduce, "seed": a.seed,
                        "l2": "no flush (warm)" if a.no_flush else "flushed between timed steps (256 MiB write)",
-                       "parallelism": f"row-partitioned x{world} (sampled-byte balanced), B replicated"
+                       "parallelism": f"row-partitioned x{world} (sampled-byte balanced), "
+                                      + ("B sharded by equal node blocks, all-gathered one 256-B feature slice at a "
+                                         "time overlapped with the slab passes" if a.b_sharded else "B replicated")
                                       + ("; C all-gather fused into the SpMM epilogue (peer stores)"
                                          if a.allgather else "")
+                                      + ("; C all-gather fused into the SpMM epilogue (NVLS multicast, multimem.st)"
+                                         if a.allgather_mc else "")
                                       + ("" if backend == "nccl" else f" [{backend} validation run]"),
                        "timing": "sum of per-step CUDA-event times on the launch stream, max over ranks"
                                  + ("; each step replays a captured CUDA graph" if use_graph else "")},
@@ -487,6 +537,8 @@ def main():
         if world > 1:
             dist.barrier()                   # no rank unmaps while a peer may still write into it
         peers.close()
+    if mcast is not None:
+        mcast.barrier()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

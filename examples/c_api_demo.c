@@ -5,7 +5,7 @@
  * every output element against a direct host evaluation of Alg. 1 / Eq. 2 (PAPER.md
  * L952-976, L1064-1067) -- positions (j * 577) mod d, mean over k = min(d, s).  Then the
  * feature-sliced path (es_spmm_run_ex with a caller-owned workspace sized by
- * es_spmm_workspace_bytes; forced here with ES_SPMM_SLAB=1 since the graph is tiny) on a
+ * es_spmm_workspace_bytes_ex; forced here with opt.kernel = ES_KERNEL_SLAB since the graph is tiny) on a
  * 70-wide B (a full 64-float slice + a 6-float tail), checked the same way.
  *
  *   gcc -O2 -I include examples/c_api_demo.c -L paper_2104_10716_b200 -lesspmm \
@@ -76,15 +76,16 @@ int main(void) {
     static float B2[NC * F2], C2[N * F2], ref2[N * F2];
     for (int i = 0; i < NC * F2; ++i) B2[i] = (float)((i * 53) % 97) / 97.0f;
     host_ref(N, rowptr, colind, val, B2, F2, S, ref2);
-    setenv("ES_SPMM_SLAB", "1", 1);
-    const int64_t ws_bytes = es_spmm_workspace_bytes(N, NC, 20, F2, F2, S, 1);
+    es_spmm_options_t opt = {0};
+    opt.struct_size = (int32_t)sizeof(opt);
+    opt.kernel = ES_KERNEL_SLAB;                       /* the graph is tiny: force the slab path */
+    opt.nnz = 20;                                      /* stored entries of the rows (capacity check) */
+    const int64_t ws_bytes = es_spmm_workspace_bytes_ex(N, NC, 20, F2, F2, S, 1, &opt);
     float *d_B2, *d_C2; void* d_ws;
     CK(cudaMalloc((void**)&d_B2, sizeof(B2)));
     CK(cudaMalloc((void**)&d_C2, sizeof(C2)));
     CK(cudaMalloc(&d_ws, (size_t)ws_bytes));
     CK(cudaMemcpy(d_B2, B2, sizeof(B2), cudaMemcpyHostToDevice));
-    es_spmm_options_t opt = {0};
-    opt.struct_size = (int32_t)sizeof(opt);
     opt.workspace = d_ws;
     opt.workspace_bytes = ws_bytes;
     const int64_t l0 = es_launch_count();

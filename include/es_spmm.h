@@ -128,6 +128,13 @@ typedef struct {
      * documented summation order.  (Read only when struct_size covers them.) */
     int32_t kernel;
     int32_t tune[4];
+    /* Fused all-gather through NVLink SHARP multicast (NVLS): c_multicast [dev] is
+     * the multicast address of every rank's FULL C (n_rows x ldc, e.g. the multicast_ptr of a
+     * torch symmetric-memory buffer): the epilogue stores each output row ONCE with multimem.st
+     * and the switch delivers it to every rank (instead of n_peers unicast stores).  Takes
+     * precedence over c_peers; NULL = not used.  `C` must be this rank's own full-C base (used
+     * for alignment).  (Read only when struct_size covers it.) */
+    float* c_multicast;
 } es_spmm_options_t;
 
 enum {

@@ -67,6 +67,10 @@ def _L():
                                              i64, i32, i64, vp, i64]
         lib.oracle_max_threads.restype = ctypes.c_int
         lib.oracle_max_threads.argtypes = []
+        lib.oracle_spmm_f32.restype = ctypes.c_int
+        lib.oracle_spmm_f32.argtypes = [i64, vp, vp, vp, vp, i64, i64, i64, i32, u64, i32, vp, i64, vp, i64]
+        lib.oracle_set_threads.restype = None
+        lib.oracle_set_threads.argtypes = [ctypes.c_int]
         _lib = lib
     return _lib
 
@@ -168,6 +172,32 @@ def spmm_backward(rowptr, colind, val, dC, n_cols: int, s: int, strategy: int, s
     if rc != 0:
         raise MemoryError("oracle_spmm_backward: allocation failed")
     return dB
+
+
+def spmm_f32(rowptr, colind, val, B, s: int, strategy: int, seed: int = 0, reduce: int = SUM,
+             F: int | None = None, rows=None) -> np.ndarray:
+    """TIMING MODE ONLY (bench.py's CPU baseline): the sampled SpMM with fp32 FMA accumulation in
+    slot order (a straightforward CPU port of Alg. 1).  Parity uses spmm (fp64)."""
+    rowptr, colind, val = _csr(rowptr, colind, val)
+    B = np.ascontiguousarray(B, dtype=np.float32)
+    ldb = B.shape[1]
+    F = ldb if F is None else F
+    n = len(rowptr) - 1
+    if rows is not None:
+        rows = np.ascontiguousarray(rows, dtype=np.int64)
+    n_out = n if rows is None else len(rows)
+    C = np.empty((n_out, F), dtype=np.float32)
+    if n_out == 0 or F == 0:
+        return C
+    rc = _L().oracle_spmm_f32(n, rowptr.ctypes.data, colind.ctypes.data, _p(val), B.ctypes.data, F, ldb, s,
+                              strategy, seed & (2**64 - 1), reduce, _p(rows), n_out, C.ctypes.data, F)
+    if rc != 0:
+        raise MemoryError("oracle_spmm_f32: allocation failed")
+    return C
+
+
+def set_threads(n: int) -> None:
+    _L().oracle_set_threads(int(n))
 
 
 def max_threads() -> int:

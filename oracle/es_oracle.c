@@ -25,6 +25,7 @@
  */
 #include <stdint.h>
 #include <stddef.h>
+#include <math.h>
 #include <stdlib.h>
 #ifdef _OPENMP
 #include <omp.h>
@@ -194,6 +195,64 @@ int oracle_spmm_backward(int64_t n_rows, const int64_t* rowptr, const int32_t* c
         for (int64_t c = 0; c < F; ++c) dB[r * ldb + c] += (float)acc[r * F + c];
     free(acc);
     return 0;
+}
+
+/* fp32 TIMING MODE (SURVEY 8(d) "fp32-FMA mode for timing, like the paper's kernel"): the same
+ * rows, slots and order as oracle_row, but acc[c] = fmaf(val, B, acc[c]) in fp32 -- the
+ * arithmetic a straightforward CPU port of Alg. 1 performs.  Used only to time the CPU
+ * baseline; parity always uses the fp64 oracle_spmm.  Pinned by tests/test_oracle_pins.py
+ * (B = 1 counts exactly; within the sequential-sum bound gamma_k of oracle_spmm). */
+static void oracle_row_f32(int64_t d, const int32_t* cols, const float* vals, const float* B,
+                           int64_t F, int64_t ldb, int64_t s, int32_t strategy, int64_t off,
+                           int32_t reduce, float* acc, float* Crow) {
+    int64_t k = oracle_k(d, s);
+    for (int64_t c = 0; c < F; ++c) acc[c] = 0.0f;
+    for (int64_t j = 0; j < k; ++j) {
+        int64_t p = oracle_position_p(strategy, j, d, off, (int64_t)ORACLE_PRIME);
+        float a = vals ? vals[p] : 1.0f;
+        const float* Brow = B + (int64_t)cols[p] * ldb;
+        for (int64_t c = 0; c < F; ++c) acc[c] = fmaf(a, Brow[c], acc[c]);
+    }
+    for (int64_t c = 0; c < F; ++c) {
+        float v = acc[c];
+        if (reduce == ORACLE_MEAN) v = k > 0 ? v / (float)k : 0.0f;
+        Crow[c] = v;
+    }
+}
+
+int oracle_spmm_f32(int64_t n_rows, const int64_t* rowptr, const int32_t* colind, const float* val,
+                    const float* B, int64_t F, int64_t ldb, int64_t s, int32_t strategy, uint64_t seed,
+                    int32_t reduce, const int64_t* rows, int64_t n_sel, float* C, int64_t ldc) {
+    int64_t n_out = rows ? n_sel : n_rows;
+    int bad = 0;
+#pragma omp parallel
+    {
+        float* acc = (float*)malloc(sizeof(float) * (size_t)(F > 0 ? F : 1));
+        if (!acc) {
+#pragma omp atomic write
+            bad = 1;
+        }
+#pragma omp for schedule(dynamic, 16)
+        for (int64_t r = 0; r < n_out; ++r) {
+            if (!acc) continue;
+            int64_t i = rows ? rows[r] : r;
+            int64_t d = rowptr[i + 1] - rowptr[i];
+            int64_t off = strategy == ORACLE_FASTRAND ? oracle_offset(seed, i, d) : 0;
+            oracle_row_f32(d, colind + rowptr[i], val ? val + rowptr[i] : NULL, B, F, ldb, s, strategy, off,
+                           reduce, acc, C + r * ldc);
+        }
+        free(acc);
+    }
+    return bad ? -1 : 0;
+}
+
+/* OpenMP threads of the calls that follow (the single-thread CPU baseline time). */
+void oracle_set_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
 }
 
 int oracle_max_threads(void) {

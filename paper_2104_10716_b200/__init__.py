@@ -50,18 +50,19 @@ class EsOptions(ctypes.Structure):
                 ("c_peers", ctypes.c_void_p), ("n_peers", ctypes.c_int32),
                 ("deterministic", ctypes.c_int32), ("workspace", ctypes.c_void_p),
                 ("workspace_bytes", ctypes.c_int64), ("reuse_sampled", ctypes.c_int32),
-                ("nnz", ctypes.c_int64), ("kernel", ctypes.c_int32), ("tune", ctypes.c_int32 * 4)]
+                ("nnz", ctypes.c_int64), ("kernel", ctypes.c_int32), ("tune", ctypes.c_int32 * 4),
+                ("c_multicast", ctypes.c_void_p)]
 
     @classmethod
     def make(cls, prime: int = 0, mean_by_degree: bool = False, bf16: bool = False, c_peers=None,
              n_peers: int = 0, deterministic: bool = False, workspace=None, reuse_sampled: bool = False,
-             nnz: int = 0, kernel=None, tune=None):
+             nnz: int = 0, kernel=None, tune=None, c_multicast: int = 0):
         ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
         kern, tun = _forced(kernel, tune)
         return cls(ctypes.sizeof(cls), prime, ES_MEAN_BY_DEGREE if mean_by_degree else ES_MEAN_BY_SAMPLED,
                    ES_DTYPE_BF16 if bf16 else ES_DTYPE_F32, _ptr(c_peers), n_peers, int(deterministic),
                    _ptr(workspace), ws_bytes, int(reuse_sampled), int(nnz), kern,
-                   (ctypes.c_int32 * 4)(*[int(x) for x in tun]))
+                   (ctypes.c_int32 * 4)(*[int(x) for x in tun]), c_multicast or None)
 
 
 # Kernel selection for A/B measurement and the tests' per-family coverage (es_spmm_options_t.kernel
@@ -304,7 +305,7 @@ def es_spmm_run_ex(rowptr, colind, val, B, s: int, strategy: int, seed: int = 0,
                    mean_by_degree: bool = False, row_begin: int = 0, row_end: int | None = None,
                    n_rows: int | None = None, nnz_base: int = 0, c_peers=None, n_peers: int = 0,
                    workspace=None, reuse_sampled: bool = False, nnz: int | None = None, kernel=None, tune=None,
-                   stream=None):
+                   c_multicast: int = 0, stream=None):
     """es_spmm_run_rows with the options: P' override, MEAN by original degree, bf16 storage of
     B (pass a torch.bfloat16 B; accumulation stays fp32) -- NEXT-4 -- the fused all-gather
     (c_peers: int64 CUDA tensor of n_peers full-C base pointers; C = this rank's full C) --
@@ -330,12 +331,13 @@ def es_spmm_run_ex(rowptr, colind, val, B, s: int, strategy: int, seed: int = 0,
         n_rows = row_end
     if C is None:
         C = torch.empty((row_end - row_begin, F), dtype=torch.float32, device=B.device)
-    rows_out = row_end - row_begin if n_peers == 0 else n_rows
+    rows_out = row_end - row_begin if (n_peers == 0 and not c_multicast) else n_rows
     _check_out(C, rows_out, F, "C")
     if nnz is None:
         nnz = colind.numel() if (nnz_base == 0 and row_end - row_begin == rowptr.numel() - 1) else 0
     opt = EsOptions.make(prime, mean_by_degree, B.dtype == torch.bfloat16, c_peers, n_peers,
-                         workspace=workspace, reuse_sampled=reuse_sampled, nnz=nnz, kernel=kernel, tune=tune)
+                         workspace=workspace, reuse_sampled=reuse_sampled, nnz=nnz, kernel=kernel, tune=tune,
+                         c_multicast=c_multicast)
     _check(load_library().es_spmm_run_ex(n_rows, B.shape[0], _ptr(rowptr), nnz_base, _ptr(colind), _ptr(val),
                                          _ptr(B), F, ldb, s, strategy, seed & (2**64 - 1), reduce, _ptr(C),
                                          C.stride(0), row_begin, row_end, ctypes.byref(opt), _stream(stream)),
@@ -411,8 +413,8 @@ def es_spmm_backward_ex(rowptr, colind, val, dC, n_cols: int, s: int, strategy: 
     n = rowptr.numel() - 1
     F = dC.shape[1] if F is None else F
     _check_out(dC, n, F, "dC")
-    if dB is None:
-        dB = torch.zeros((n_cols, F), dtype=torch.float32, device=dC.device)
+    if dB is None:                                   # rows at a 16-B pitch: the slab backward can run
+        dB = torch.zeros((n_cols, (F + 3) // 4 * 4), dtype=torch.float32, device=dC.device)[:, :F]
     _check_out(dB, n_cols, F, "dB")
     opt = EsOptions.make(prime, mean_by_degree, deterministic=deterministic, workspace=workspace,
                          reuse_sampled=reuse_sampled, nnz=colind.numel())

@@ -42,6 +42,7 @@ struct Opts {
     int32_t reuse_sampled = 0;
     int64_t nnz = 0;             // stored entries of the call's rows (0 = unknown)
     es::Tune tune;
+    float* c_mc = nullptr;       // NVLS multicast base of the full C (fused all-gather)
 };
 
 #define ES_COVERS(o, field) ((o)->struct_size >= (int32_t)(offsetof(es_spmm_options_t, field) + sizeof((o)->field)))
@@ -80,6 +81,7 @@ es_status_t read_opts(const es_spmm_options_t* o, Opts* out) {
         out->tune.cta_warps = o->tune[2];
         out->tune.variant = o->tune[3];
     }
+    if (ES_COVERS(o, c_multicast)) out->c_mc = o->c_multicast;
     return ES_OK;
 }
 
@@ -155,10 +157,12 @@ bool slab_slots(const Opts& o, int64_t n, int32_t s, bool has_val, SlabSlots* ou
     return true;
 }
 
-// Signature of a sampling: everything the sampled slots depend on (never 0).
+// Signature of a sampling: the call parameters the sampled slots depend on (never 0).  The graph
+// itself is checked per row on reuse (SlabParams.reuse_s: the slab passes compare each row's slot
+// count with min(d_i, s) from the caller's rowptr), so a re-uploaded copy of the same CSR may be
+// reused, a different one is caught.
 uint64_t sampling_signature(int64_t n, int64_t row_begin, int32_t s, int32_t strategy, uint64_t seed,
-                            uint32_t prime, const int64_t* rowptr, int64_t nnz_base, const int32_t* colind,
-                            const float* val) {
+                            uint32_t prime, int64_t nnz_base, bool has_val) {
     uint64_t h = 0x6a09e667f3bcc908ull;
     auto mix = [&](uint64_t x) {
         h ^= x + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2);
@@ -166,8 +170,7 @@ uint64_t sampling_signature(int64_t n, int64_t row_begin, int32_t s, int32_t str
         h ^= h >> 31;
     };
     mix((uint64_t)n); mix((uint64_t)row_begin); mix((uint64_t)s); mix((uint64_t)strategy); mix(seed);
-    mix(prime); mix(reinterpret_cast<uintptr_t>(rowptr)); mix((uint64_t)nnz_base);
-    mix(reinterpret_cast<uintptr_t>(colind)); mix(reinterpret_cast<uintptr_t>(val));
+    mix(prime); mix((uint64_t)nnz_base); mix(has_val ? 1u : 0u);
     return h ? h : 1;
 }
 
@@ -217,8 +220,7 @@ es_status_t run_rows_impl(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
         if (!direct && !slab_slots(o, n, s, val != nullptr, &sl)) return ES_ERR_INVALID_VALUE;
         int launches = 0;
         cudaError_t err = cudaSuccess;
-        const uint64_t sig = sampling_signature(n, row_begin, s, strategy, seed, o.prime, rowptr, nnz_base,
-                                                colind, val);
+        const uint64_t sig = sampling_signature(n, row_begin, s, strategy, seed, o.prime, nnz_base, val != nullptr);
         if (!o.reuse_sampled && !direct)
             err = slab_sample(sl, rowptr, nnz_base, colind, val, n, s, strategy, seed, row_begin, o.prime, sig, st,
                               &launches);
@@ -239,6 +241,7 @@ es_status_t run_rows_impl(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
             sp.ws_status = direct ? nullptr : &sl.hdr->status;
             sp.ws_sig = direct ? nullptr : &sl.hdr->sig;
             sp.sig = sig;
+            sp.reuse_s = (o.reuse_sampled && !direct) ? s : 0;
             sp.rowptr = rowptr;
             sp.b_bf16 = o.bf16;
             sp.B = o.bf16 ? reinterpret_cast<const float*>(static_cast<const uint16_t*>(B) + c0)
@@ -253,6 +256,7 @@ es_status_t run_rows_impl(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
             sp.C = C + c0;
             sp.c_peers = o.c_peers;
             sp.n_peers = o.n_peers;
+            sp.c_mc = o.c_mc;
             sp.row_base = row_begin;
             sp.col0 = c0;
             sp.ldc = ldc;
@@ -293,6 +297,7 @@ es_status_t run_rows_impl(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
     p.b_bf16 = o.bf16;
     p.c_peers = o.c_peers;
     p.n_peers = o.n_peers;
+    p.c_mc = o.c_mc;
     const int64_t k_est = o.nnz > 0 ? std::min<int64_t>(s, o.nnz / n) : s;
     const es::Plan plan = o.bf16 ? es::make_plan_bf16(F, ldb, ldc, B, C)
                                  : es::make_plan(F, ldb, ldc, B, C, s, tn, k_est);
@@ -495,8 +500,7 @@ es_status_t es_spmm_backward_ex(int64_t n_rows, int64_t n_cols, const int64_t* r
         cudaStream_t st = as_stream(stream);
         int launches = 0;
         cudaError_t err = cudaSuccess;
-        const uint64_t sig = sampling_signature(n, row_begin, s, strategy, seed, o.prime, rowptr, nnz_base,
-                                                colind, val);
+        const uint64_t sig = sampling_signature(n, row_begin, s, strategy, seed, o.prime, nnz_base, val != nullptr);
         if (!o.reuse_sampled && !direct)
             err = slab_sample(sl, rowptr, nnz_base, colind, val, n, s, strategy, seed, row_begin, o.prime, sig, st,
                               &launches);
@@ -511,6 +515,7 @@ es_status_t es_spmm_backward_ex(int64_t n_rows, int64_t n_cols, const int64_t* r
             sp.ws_status = direct ? nullptr : &sl.hdr->status;
             sp.ws_sig = direct ? nullptr : &sl.hdr->sig;
             sp.sig = sig;
+            sp.reuse_s = (o.reuse_sampled && !direct) ? s : 0;
             sp.rowptr = rowptr;
             sp.ldb = ldb;
             sp.w = (int32_t)(F - c0 < kSlabF ? F - c0 : kSlabF);
@@ -686,7 +691,7 @@ es_status_t es_spmm_run_host_ex(int64_t n_rows, int64_t n_cols, const int64_t* r
     es_status_t rc = check_common(n_rows, n_cols, F, ldb, ldc, s, strategy, reduce);
     if (rc != ES_OK) return rc;
     Opts o;
-    if (read_opts(opt, &o) != ES_OK || o.bf16 || o.n_peers || o.workspace || o.reuse_sampled)
+    if (read_opts(opt, &o) != ES_OK || o.bf16 || o.n_peers || o.c_mc || o.workspace || o.reuse_sampled)
         return ES_ERR_INVALID_VALUE;                 // host buffers: fp32 B, no peers, own workspace
     if (n_rows == 0) return ES_OK;
     if (!rowptr || !C || !workspace || (n_cols > 0 && !B) || row_base < 0) return ES_ERR_INVALID_VALUE;

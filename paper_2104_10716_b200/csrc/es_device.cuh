@@ -119,6 +119,16 @@ __device__ __forceinline__ void st_stream2(float* p, const float* a, uint64_t po
                  :: "l"(p), "f"(a[0]), "f"(a[1]), "l"(pol) : "memory");
 }
 
+// Stores to an NVLS multicast address (multimem.st): one store, delivered by the NVSwitch to
+// the bound buffer of every rank (the fused C all-gather, NEXT-1).
+__device__ __forceinline__ void st_multicast4(float* p, const float* a) {
+    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};"
+                 :: "l"(p), "f"(a[0]), "f"(a[1]), "f"(a[2]), "f"(a[3]) : "memory");
+}
+__device__ __forceinline__ void st_multicast(float* p, float a) {
+    asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" :: "l"(p), "f"(a) : "memory");
+}
+
 // Vector reductions into global memory (SASS REDG.E.ADD.F32x4): relaxed, gpu scope.  Note the
 // hardware add flushes fp32 denormals to zero (FTZ), unlike the FMA path.
 __device__ __forceinline__ void red_add4(float* p, float a, float b, float c, float d) {

@@ -36,6 +36,7 @@ struct SpmmParams {
     int32_t b_bf16;          // B stored as bf16 (fp32 accumulation, NEXT-4)
     float* const* c_peers;   // fused all-gather: full-C bases of every rank (NEXT-1)
     int32_t n_peers;         // 0: plain store to C
+    float* c_mc;             // fused all-gather through NVLS multicast (multimem.st), or NULL
 };
 
 struct Plan {
@@ -96,6 +97,7 @@ struct SlabParams {
     int32_t mean_by_degree;
     float* const* c_peers;    // fused all-gather (NEXT-1): full-C bases of every rank, or NULL
     int32_t n_peers;
+    float* c_mc;              // fused all-gather through NVLS multicast (multimem.st), or NULL
     int64_t row_base;         // global id of local row 0 (peer stores)
     int64_t col0;             // the slice's first column (peer stores)
     int32_t b_bf16;           // B holds bf16 (NEXT-4 storage variant): B points at uint16_t elements
@@ -108,6 +110,7 @@ struct SlabParams {
     int32_t* ws_status;       // NULL: no workspace (direct Bucket slots)
     const uint64_t* ws_sig;   // signature written by the sampling call (NULL: not checked)
     uint64_t sig;             // the signature this call expects
+    int32_t reuse_s;          // > 0 (reuse_sampled): also check each row's slot count == min(d_i, reuse_s)
 };
 
 // workspace header (first 256 B of a slab workspace)

@@ -61,6 +61,17 @@ __device__ __forceinline__ void store_out(float* Crow, int64_t vidx, int64_t F, 
 template <int VEC>
 __device__ __forceinline__ void store_c(const SpmmParams& p, int64_t r, int64_t vidx, const float* res,
                                         uint64_t pol) {
+    if (p.c_mc) {                                   // NVLS multicast: one store reaches every rank
+        float* row = p.c_mc + (p.row_base + r) * p.ldc;
+        const int64_t c0 = vidx * VEC;
+        if constexpr (VEC == 4) {
+            if (p.c_vec && c0 + 4 <= p.F) { st_multicast4(row + c0, res); return; }
+        }
+#pragma unroll
+        for (int q = 0; q < VEC; ++q)
+            if (c0 + q < p.F) st_multicast(row + c0 + q, res[q]);
+        return;
+    }
     if (p.n_peers == 0) {
         store_out<VEC>(p.C + r * p.ldc, vidx, p.F, res, p.c_vec, pol);
         return;

@@ -78,7 +78,8 @@ __device__ __forceinline__ bool slab_row_guard(const SlabParams& p, int64_t raw_
 __device__ __forceinline__ void slab_poison_row(const SlabParams& p, int64_t r) {
     const float nan = __int_as_float(0x7fc00000);
     for (int c = threadIdx.x & 31; c < p.w; c += 32) {
-        if (p.n_peers == 0) p.C[r * p.ldc + c] = nan;
+        if (p.c_mc) st_multicast(p.c_mc + (p.row_base + r) * p.ldc + p.col0 + c, nan);
+        else if (p.n_peers == 0) p.C[r * p.ldc + c] = nan;
         else
             for (int q = 0; q < p.n_peers; ++q) p.c_peers[q][(p.row_base + r) * p.ldc + p.col0 + c] = nan;
     }
@@ -107,7 +108,14 @@ __device__ __forceinline__ void slab_store_piece(const SlabParams& p, int64_t r,
                 for (int c = 0; c < 4; ++c)
                     if (c < rem) st_stream(dst + c, res[c], pol);
         };
-        if (p.n_peers == 0) {
+        if (p.c_mc) {                                // fused all-gather through NVLS multicast
+            float* dst = p.c_mc + (p.row_base + r) * p.ldc + p.col0 + c0;
+            if (p.c_vec && rem >= 4) st_multicast4(dst, res);
+            else
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    if (c < rem) st_multicast(dst + c, res[c]);
+        } else if (p.n_peers == 0) {
             put(p.C + r * p.ldc + c0);
         } else {                                     // fused all-gather: every rank's C (NEXT-1)
             const int64_t off = (p.row_base + r) * p.ldc + p.col0 + c0;
@@ -123,7 +131,11 @@ __device__ __forceinline__ bool slab_row_slots(const SlabParams& p, int64_t r, i
     beg = ld_stream(p.s_rowptr + r, pol) - p.slot_base;
     int64_t end = ld_stream(p.s_rowptr + r + 1, pol) - p.slot_base;
     if (p.direct_s > 0 && end - beg > p.direct_s) end = beg + p.direct_s;   // Bucket: first s of the row
-    const bool sig_bad = p.ws_sig != nullptr && *p.ws_sig != p.sig;
+    bool sig_bad = p.ws_sig != nullptr && *p.ws_sig != p.sig;
+    if (p.reuse_s > 0 && !sig_bad && end <= p.cap) {              // reused slots: the caller's graph?
+        const int64_t d = ld_stream(p.rowptr + r + 1, pol) - ld_stream(p.rowptr + r, pol);
+        sig_bad = end - beg != (d < p.reuse_s ? d : (int64_t)p.reuse_s);
+    }
     if (slab_row_guard(p, end, sig_bad)) {
         slab_poison_row(p, r);
         return false;
@@ -602,7 +614,11 @@ spmm_slab_stream(const SlabParams p) {
         beg = ld_stream(p.s_rowptr + r0 + lane, pol) - p.slot_base;
         int64_t end = ld_stream(p.s_rowptr + r0 + lane + 1, pol) - p.slot_base;
         if (p.direct_s > 0 && end - beg > p.direct_s) end = beg + p.direct_s;
-        const bool sig_bad = p.ws_sig != nullptr && *p.ws_sig != p.sig;
+        bool sig_bad = p.ws_sig != nullptr && *p.ws_sig != p.sig;
+        if (p.reuse_s > 0 && !sig_bad && end <= p.cap) {
+            const int64_t d = ld_stream(p.rowptr + r0 + lane + 1, pol) - ld_stream(p.rowptr + r0 + lane, pol);
+            sig_bad = end - beg != (d < p.reuse_s ? d : (int64_t)p.reuse_s);
+        }
         bad = end > p.cap || sig_bad;
         if (bad && p.ws_status) atomicOr(p.ws_status, (end > p.cap ? kWsOverflow : 0) | (sig_bad ? kWsSignature : 0));
         k = (!bad && end > beg) ? (int32_t)(end - beg) : 0;
@@ -616,7 +632,8 @@ spmm_slab_stream(const SlabParams p) {
             slab_poison_row(p, r0 + i);
         } else {
             for (int c = lane; c < p.w; c += 32) {
-                if (p.n_peers == 0) p.C[(r0 + i) * p.ldc + c] = 0.0f;
+                if (p.c_mc) st_multicast(p.c_mc + (p.row_base + r0 + i) * p.ldc + p.col0 + c, 0.0f);
+                else if (p.n_peers == 0) p.C[(r0 + i) * p.ldc + c] = 0.0f;
                 else
                     for (int q = 0; q < p.n_peers; ++q) p.c_peers[q][(p.row_base + r0 + i) * p.ldc + p.col0 + c] = 0.0f;
             }
@@ -834,7 +851,11 @@ spmm_slab_bwd(const SlabParams p, const float* __restrict__ dC, float* __restric
     const int64_t beg = ld_stream(p.s_rowptr + r, pol_a) - p.slot_base;
     int64_t end = ld_stream(p.s_rowptr + r + 1, pol_a) - p.slot_base;
     if (p.direct_s > 0 && end - beg > p.direct_s) end = beg + p.direct_s;
-    const bool sig_bad = p.ws_sig != nullptr && *p.ws_sig != p.sig;
+    bool sig_bad = p.ws_sig != nullptr && *p.ws_sig != p.sig;
+    if (p.reuse_s > 0 && !sig_bad && end <= p.cap) {
+        const int64_t d = ld_stream(p.rowptr + r + 1, pol_a) - ld_stream(p.rowptr + r, pol_a);
+        sig_bad = end - beg != (d < p.reuse_s ? d : (int64_t)p.reuse_s);
+    }
     if (slab_row_guard(p, end, sig_bad)) return;      // dB is accumulated into: flagged, not poisoned
     const int32_t k = end > beg ? (int32_t)(end - beg) : 0;
     if (k == 0) return;

@@ -101,6 +101,88 @@ def sampled_spmm_distributed(rowptr_host, colind_host, val_host, B_local, F: int
     return C
 
 
+# --------------------------------------------------------------------------- B sharded, pipelined
+def equal_blocks(n: int, world: int) -> np.ndarray:
+    """Node blocks of B in the B-sharded mode: m = ceil(n / world) rows per rank (the last block
+    shorter), so the all-gathered blocks ARE B's rows in order -- no compaction copy."""
+    m = (n + world - 1) // world if world else n
+    return np.minimum(np.arange(world + 1, dtype=np.int64) * m, n)
+
+
+def _allgather_slab(out, send, group=None):
+    """out (world*m x w) <- every rank's send (m x w), rank order.  NCCL on CUDA tensors; other
+    backends (gloo: the multi-process validation on one GPU) stage through host memory."""
+    import torch
+    import torch.distributed as dist
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        out[: send.shape[0]].copy_(send, non_blocking=True)
+        return
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out, send, group=group)
+        return
+    h_send = send.cpu()
+    h_out = torch.empty(out.shape, dtype=out.dtype)
+    dist.all_gather_into_tensor(h_out, h_send, group=group)
+    out.copy_(h_out)
+
+
+class BShardedSpMM:
+    """One sampled SpMM with B SHARDED by node blocks (the output of a previous layer, SURVEY
+    8(e)): C[:, c] needs only B[:, c] (Alg. 1 l.13-15), so the all-gather runs one 256-B feature
+    slice at a time on a side stream and slice j+1's gather overlaps slice j's slab pass (the
+    library's feature-sliced path over the gathered slab, double-buffered).  Exact: the same
+    per-element order as the replicated-B slab path (bitwise).
+
+    B_local: this rank's rows [blocks[r], blocks[r+1]) of B (equal_blocks), fp32, ldb columns.
+    The call samples once (first slice) into the workspace and every other slice reuses it."""
+
+    def __init__(self, n_cols: int, F: int, world: int, rank: int, device, group=None, width: int = 64):
+        import torch
+        self.n_cols, self.F, self.world, self.rank, self.group, self.w = n_cols, F, world, rank, group, width
+        self.blocks = equal_blocks(n_cols, world)
+        self.m = int(self.blocks[1] - self.blocks[0]) if world else n_cols
+        self.slabs = [torch.empty((world * self.m, width), dtype=torch.float32, device=device) for _ in range(2)]
+        self.send = [torch.empty((self.m, width), dtype=torch.float32, device=device) for _ in range(2)]
+        self.comm = torch.cuda.Stream(device)
+        self.ready = [torch.cuda.Event() for _ in range(2)]
+        self.free = [torch.cuda.Event() for _ in range(2)]
+
+    def __call__(self, rp, ci, va, B_local, s: int, strategy: int, seed: int, reduce: int, C, *, n_rows: int,
+                 row_begin: int, row_end: int, nnz_base: int, nnz: int, workspace, stream=None):
+        import torch
+        from . import es_spmm_run_ex
+        main = stream if stream is not None else torch.cuda.current_stream()
+        n_sl = (self.F + self.w - 1) // self.w
+        rows_here = B_local.shape[0]
+
+        def gather(j):
+            b = j % 2
+            c0 = j * self.w
+            w = min(self.w, self.F - c0)
+            with torch.cuda.stream(self.comm):
+                if j >= 2:
+                    self.comm.wait_event(self.free[b])          # slab b consumed by slice j-2
+                else:
+                    self.comm.wait_stream(main)                 # B_local written before this call
+                self.send[b][:rows_here, :w].copy_(B_local[:, c0:c0 + w])
+                _allgather_slab(self.slabs[b], self.send[b], self.group)
+                self.ready[b].record(self.comm)
+
+        gather(0)
+        for j in range(n_sl):
+            if j + 1 < n_sl:
+                gather(j + 1)                                   # overlaps slice j below
+            b = j % 2
+            c0 = j * self.w
+            w = min(self.w, self.F - c0)
+            main.wait_event(self.ready[b])
+            es_spmm_run_ex(rp, ci, va, self.slabs[b], s, strategy, seed, reduce, F=w, C=C[:, c0:c0 + w],
+                           row_begin=row_begin, row_end=row_end, n_rows=n_rows, nnz_base=nnz_base,
+                           workspace=workspace, nnz=nnz, reuse_sampled=j > 0, stream=main)
+            self.free[b].record(main)
+        return C
+
+
 # --------------------------------------------------------------------------- fused all-gather
 class _CudaArray:
     """Minimal __cuda_array_interface__ holder to view a raw allocation as a torch tensor."""
@@ -148,6 +230,32 @@ class PeerBuffers:
         if self.local_ptr:
             es_ipc_free(self.local_ptr)
             self.local_ptr = 0
+
+
+class MulticastC:
+    """A full-size C (n_rows x ldc fp32) in torch symmetric memory on every rank of `group`, with
+    the NVLS multicast address of the set: the SpMM epilogue stores each output
+    row ONCE through it (es_spmm_options_t.c_multicast, multimem.st) and the NVSwitch delivers it
+    to every rank -- 1x NVLink egress per row instead of (P-1)x unicast peer stores.  PyTorch does
+    the plumbing (allocation, handle exchange, multicast binding); raises if the node has no
+    multicast support (use PeerBuffers then)."""
+
+    def __init__(self, n_rows: int, ldc: int, group=None, device=None):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        grp = group if group is not None else dist.group.WORLD
+        self.C = symm.empty((n_rows, ldc), dtype=torch.float32, device=dev)
+        self.handle = symm.rendezvous(self.C, grp.group_name if hasattr(grp, "group_name") else grp)
+        if not self.handle.has_multicast_support() or not self.handle.multicast_ptr:
+            raise RuntimeError("no NVLS multicast support for this group (use PeerBuffers)")
+        self.multicast = int(self.handle.multicast_ptr)
+        self.world = self.handle.world_size
+        self.rank = self.handle.rank
+
+    def barrier(self):
+        self.handle.barrier()
 
 
 def sampled_spmm_fused_allgather(rowptr_host, colind_host, val_host, B, F: int, s: int, strategy: int,

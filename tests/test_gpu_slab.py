@@ -182,9 +182,9 @@ def test_reuse_sampled_slots(graph, lanes):
     """reuse_sampled: the gather passes alone over the slots an earlier call sampled into the
     workspace (a second feature matrix over the same sampled graph) == a full call, bitwise."""
     rowptr, colind, val = graph
-    B1 = synth.dense(2300, 300, seed=21, ld=300)
-    B2 = synth.dense(2300, 300, seed=22, ld=300)
-    ws = es.es_spmm_workspace(1301, 2300, len(colind), 300, 300, 96, True, device=DEV)
+    B1 = synth.dense(2300, 300, seed=21, ld=304)
+    B2 = synth.dense(2300, 300, seed=22, ld=304)
+    ws = es.es_spmm_workspace(1301, 2300, len(colind), 300, 304, 96, True, device=DEV)
     rp, ci, v = t(rowptr), t(colind), t(val)
     es.es_spmm_run_ex(rp, ci, v, t(B1), 96, 2, 13, 1, F=300, workspace=ws)
     g2 = es.es_spmm_run_ex(rp, ci, v, t(B2), 96, 2, 13, 1, F=300, workspace=ws, reuse_sampled=True)
@@ -271,6 +271,16 @@ def test_reuse_with_other_sampling_is_detected(graph):
     with es.kernel_override("slab"):
         es.es_spmm_run_ex(rp, ci, v, t(B), 96, 2, 13, 1, F=300, workspace=ws)
         assert es.es_spmm_workspace_status(ws) == es.ES_WS_OK
+        # a re-uploaded copy of the same graph may reuse the slots; a different graph (same row
+        # count, other degrees) is caught row by row
+        C = es.es_spmm_run_ex(t(rowptr), t(colind), t(val), t(B), 96, 2, 13, 1, F=300, workspace=ws,
+                              reuse_sampled=True)
+        assert not torch.isnan(C).any() and es.es_spmm_workspace_status(ws) == es.ES_WS_OK
+        rp2 = rowptr.copy()
+        rp2[1:-1] = np.minimum(rp2[1:-1] + 1, rp2[-1])     # shifted row boundaries
+        C = es.es_spmm_run_ex(t(rp2), ci, v, t(B), 96, 2, 13, 1, F=300, workspace=ws, reuse_sampled=True)
+        assert torch.isnan(C).any()
+        assert es.es_spmm_workspace_status(ws, reset=True) & es.ES_WS_SIGNATURE_MISMATCH
         for kw in (dict(seed=14), dict(s=95)):
             args = dict(seed=13, s=96)
             args.update(kw)

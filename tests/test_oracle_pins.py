@@ -392,3 +392,25 @@ def test_mean_by_degree_variant():
                               mean_by_degree=True)
     assert abs(float(np.sum(C.astype(np.float64) * dC)) - float(np.sum(B.astype(np.float64) * dB))) \
         <= 1e-6 * abs(float(np.sum(C.astype(np.float64) * dC)))
+
+
+# ---- the fp32 timing mode (bench.py's CPU baseline only; parity uses the fp64 oracle)
+def test_f32_timing_mode_counts_and_bound():
+    """oracle.spmm_f32: B = 1 and val = 1 give the sampled counts exactly (integers < 2^24), and
+    with non-negative inputs it stays within the sequential fp32 sum bound gamma_k = k u / (1 - k u)
+    of the fp64 oracle (+ one rounding for MEAN) -- a dropped slot, a wrong position or a
+    mis-indexed B row fails one of them."""
+    rowptr, colind, val = synth.random_csr(400, 900, seed=3, max_deg=300, special=(577, 1154))
+    d = np.diff(rowptr)
+    ones = np.ones((900, 24), np.float32)
+    for strat in (BUCKET, FASTRAND):
+        c = oracle.spmm_f32(rowptr, colind, None, ones, 64, strat, seed=0)
+        assert np.array_equal(c, np.repeat(np.minimum(d, 64)[:, None], 24, 1).astype(np.float32))
+        B = synth.dense(900, 40, seed=8)
+        for s, red in ((16, SUM), (256, MEAN), (1000, SUM)):
+            g = oracle.spmm_f32(rowptr, colind, val, B, s, strat, seed=0, reduce=red).astype(np.float64)
+            o = oracle.spmm(rowptr, colind, val, B, s, strat, seed=0, reduce=red).astype(np.float64)
+            mag = oracle.spmm(rowptr, colind, np.abs(val), np.abs(B), s, strat, seed=0, reduce=red).astype(np.float64)
+            k = np.minimum(d, s).astype(np.float64)[:, None]
+            u = 2.0 ** -24
+            assert np.all(np.abs(g - o) <= (k * u / (1 - k * u) + 2 * u) * mag + 1e-30)
