@@ -6,7 +6,7 @@
  * L952-976, L1064-1067) -- positions (j * 577) mod d, mean over k = min(d, s).  Then the
  * feature-sliced path (es_spmm_run_ex with a caller-owned workspace sized by
  * es_spmm_workspace_bytes_ex; forced here with opt.kernel = ES_KERNEL_SLAB since the graph is tiny) on a
- * 70-wide B (a full 64-float slice + a 6-float tail), checked the same way.
+ * 72-wide B (a full 64-float slice + an 8-float tail), checked the same way.
  *
  *   gcc -O2 -I include examples/c_api_demo.c -L paper_2104_10716_b200 -lesspmm \
  *       -I /usr/local/cuda/include -L /usr/local/cuda/lib64 -lcudart -o /tmp/c_api_demo
@@ -40,7 +40,7 @@ static void host_ref(int n, const int64_t* rowptr, const int32_t* colind, const 
 }
 
 int main(void) {
-    enum { N = 6, NC = 9, F = 5, S = 3, F2 = 70 };
+    enum { N = 6, NC = 9, F = 5, S = 3, F2 = 72 };   /* F2: 16-B row pitch for the slab path */
     const int64_t rowptr[N + 1] = {0, 4, 4, 5, 12, 13, 20};       /* row 1 empty */
     int32_t colind[20];
     float val[20], B[NC * F], C[N * F], ref[N * F];
