@@ -258,7 +258,7 @@ def main():
     backend = os.environ.get("ES_BENCH_BACKEND", "nccl")
     dev = torch.device("cuda", local % torch.cuda.device_count())
     torch.cuda.set_device(dev)
-    if world > 1:
+    if world > 1 or a.allgather_mc:               # symmetric memory needs a group, even of one rank
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
         else:
@@ -541,6 +541,7 @@ def main():
         mcast.barrier()
     if world > 1:
         dist.barrier()
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 

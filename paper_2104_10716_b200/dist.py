@@ -245,11 +245,15 @@ class MulticastC:
         import torch.distributed as dist
         import torch.distributed._symmetric_memory as symm
         dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        if not dist.is_initialized():
+            raise RuntimeError("MulticastC needs an initialised process group (world size 1 included)")
         grp = group if group is not None else dist.group.WORLD
+        if not symm._SymmetricMemory.has_multicast_support(torch._C._autograd.DeviceType.CUDA, dev.index or 0):
+            raise RuntimeError("no NVLS multicast support on this device (use PeerBuffers)")
         self.C = symm.empty((n_rows, ldc), dtype=torch.float32, device=dev)
-        self.handle = symm.rendezvous(self.C, grp.group_name if hasattr(grp, "group_name") else grp)
-        if not self.handle.has_multicast_support() or not self.handle.multicast_ptr:
-            raise RuntimeError("no NVLS multicast support for this group (use PeerBuffers)")
+        self.handle = symm.rendezvous(self.C, grp.group_name)
+        if not self.handle.multicast_ptr:
+            raise RuntimeError("no multicast address for this group (use PeerBuffers)")
         self.multicast = int(self.handle.multicast_ptr)
         self.world = self.handle.world_size
         self.rank = self.handle.rank

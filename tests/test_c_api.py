@@ -40,4 +40,4 @@ def test_c_demo_runs(tmp_path):
     res = subprocess.run([str(exe)], capture_output=True, text=True, env=env, timeout=120)
     assert res.returncode == 0, res.stdout + res.stderr
     assert "0/30 elements off" in res.stdout
-    assert "0/420 off" in res.stdout                  # the slab path from C (workspace via options)
+    assert "0/432 off" in res.stdout                  # the slab path from C (workspace via options)
