@@ -15,16 +15,21 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import synth  # noqa: E402
 import paper_2104_10716_b200 as es  # noqa: E402
-from bench import byte_model, ldb_for, measured_peaks  # noqa: E402
+from bench import L2_RESIDENT_BYTES, byte_model, l2_peak, ldb_for, measured_peaks  # noqa: E402
 
 CASES = [("pubmed", 16, 0), ("arxiv", 128, 0), ("proteins", 128, 0), ("reddit", 128, 1), ("reddit", 602, 1)]
 
 
 def main():
     dev = torch.device("cuda:0")
-    peak, _ = measured_peaks()
+    hbm, _ = measured_peaks()
+    l2, _ = l2_peak()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    only = sys.argv[1:] or None
+    args = sys.argv[1:]
+    kernel = None
+    if args[:1] == ["--kernel"]:
+        kernel, args = args[1], args[2:]
+    only = args or None
     for name, F, red in CASES:
         if only and name not in only:
             continue
@@ -38,7 +43,7 @@ def main():
         C = torch.empty((n, ldb), device=dev)
         for s in (16, 32, 64, 128, 256, 512):
             K = int(np.minimum(d, s).sum())
-            ws = es.es_spmm_workspace(n, n, len(colind), F, ldb, s, True, device=dev)
+            ws = (None if kernel == "fused" else es.es_spmm_workspace(n, n, len(colind), F, ldb, s, True, device=dev))
             for strat in (1, 2):
                 ts = []
                 for i in range(7):
@@ -55,10 +60,14 @@ def main():
                         ts.append(e0.elapsed_time(e1))
                 ms = float(np.median(ts))
                 gbs = byte_model(K, n, F) / (ms / 1e3) / 1e9
+                # the ceiling that binds (as bench.py): L2 when the gathered operand is L2-resident
+                resident = (n * 256 if ws is not None else n * ldb * 4) <= L2_RESIDENT_BYTES
+                bound, peak = ("l2", l2) if (resident and l2) else ("hbm", hbm)
                 print(json.dumps({"graph": name, "F": F, "s": s, "strategy": "bucket" if strat == 1 else "fastrand",
                                   "reduce": "mean" if red else "sum", "K": K, "rate": round(K / d.sum(), 4),
                                   "ms": round(ms, 4), "GFLOPs": round(2 * F * K / (ms / 1e3) / 1e9, 1),
-                                  "model_GBs": round(gbs, 1), "frac": round(gbs / peak, 3),
+                                  "model_GBs": round(gbs, 1), "bound": bound, "frac": round(gbs / peak, 3),
+                                  "step_incl_sampling": True,
                                   "sampled_edges_per_s": round(K / (ms / 1e3)),
                                   "plan": "slab path (spmm_slab x %d + sampling)" % ((F + 63) // 64)
                                   if ws is not None else es.es_spmm_plan(F, ldb, ldb, B, C)}), flush=True)
