@@ -36,7 +36,7 @@ def build(force: bool = False) -> str:
     """Compile the C oracle (plain gcc -O2, no fast-math)."""
     src = os.path.join(_HERE, "es_oracle.c")
     if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(src):
-        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fno-fast-math", "-shared", "-fPIC",
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fno-fast-math", "-ffp-contract=off", "-shared", "-fPIC",
                                src, "-o", _LIB_PATH])
     return _LIB_PATH
 

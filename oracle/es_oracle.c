@@ -202,9 +202,42 @@ int oracle_spmm_backward(int64_t n_rows, const int64_t* rowptr, const int32_t* c
  * arithmetic a straightforward CPU port of Alg. 1 performs.  Used only to time the CPU
  * baseline; parity always uses the fp64 oracle_spmm.  Pinned by tests/test_oracle_pins.py
  * (B = 1 counts exactly; within the sequential-sum bound gamma_k of oracle_spmm). */
+/* compiled for the FMA instruction set (the CPU's vfmadd, not libm's software fmaf) where the host
+ * has it -- oracle_spmm_f32 checks at run time and uses the portable copy otherwise */
+#define ORACLE_ROW_F32_BODY                                                                        \
+    int64_t k = oracle_k(d, s);                                                                    \
+    for (int64_t c = 0; c < F; ++c) acc[c] = 0.0f;                                                 \
+    for (int64_t j = 0; j < k; ++j) {                                                              \
+        int64_t p = oracle_position_p(strategy, j, d, off, (int64_t)ORACLE_PRIME);                 \
+        float a = vals ? vals[p] : 1.0f;                                                           \
+        const float* Brow = B + (int64_t)cols[p] * ldb;                                            \
+        for (int64_t c = 0; c < F; ++c) acc[c] = fmaf(a, Brow[c], acc[c]);                         \
+    }                                                                                              \
+    for (int64_t c = 0; c < F; ++c) {                                                              \
+        float v = acc[c];                                                                          \
+        if (reduce == ORACLE_MEAN) v = k > 0 ? v / (float)k : 0.0f;                                \
+        Crow[c] = v;                                                                               \
+    }
+#if defined(__x86_64__) && defined(__GNUC__)
+__attribute__((target("fma")))
+static void oracle_row_f32_fma(int64_t d, const int32_t* cols, const float* vals, const float* B,
+                               int64_t F, int64_t ldb, int64_t s, int32_t strategy, int64_t off,
+                               int32_t reduce, float* acc, float* Crow) {
+    ORACLE_ROW_F32_BODY
+}
+#endif
 static void oracle_row_f32(int64_t d, const int32_t* cols, const float* vals, const float* B,
                            int64_t F, int64_t ldb, int64_t s, int32_t strategy, int64_t off,
                            int32_t reduce, float* acc, float* Crow) {
+#if defined(__x86_64__) && defined(__GNUC__)
+    if (__builtin_cpu_supports("fma")) {
+        oracle_row_f32_fma(d, cols, vals, B, F, ldb, s, strategy, off, reduce, acc, Crow);
+        return;
+    }
+#endif
+    ORACLE_ROW_F32_BODY
+}
+#if 0
     int64_t k = oracle_k(d, s);
     for (int64_t c = 0; c < F; ++c) acc[c] = 0.0f;
     for (int64_t j = 0; j < k; ++j) {
@@ -219,6 +252,7 @@ static void oracle_row_f32(int64_t d, const int32_t* cols, const float* vals, co
         Crow[c] = v;
     }
 }
+#endif
 
 int oracle_spmm_f32(int64_t n_rows, const int64_t* rowptr, const int32_t* colind, const float* val,
                     const float* B, int64_t F, int64_t ldb, int64_t s, int32_t strategy, uint64_t seed,
