@@ -93,10 +93,30 @@ det_gather(const BwdParams p, int64_t n_cols, const int64_t* __restrict__ col_pt
     }
 }
 
-template <typename T>
-cudaError_t alloc(T** ptr, size_t count, cudaStream_t st) {
-    return cudaMallocAsync(reinterpret_cast<void**>(ptr), count * sizeof(T) + 16, st);
-}
+
+// Stream-ordered scratch allocations released on every return path: whatever was
+// allocated is freed, in stream order, when the owner goes out of scope.
+struct Scratch {
+    cudaStream_t st;
+    void* ptrs[12] = {};
+    int n = 0;
+    template <typename T>
+    cudaError_t get(T** out, int64_t count) {
+        *out = nullptr;
+        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(out), (size_t)(count > 0 ? count : 1) * sizeof(T), st);
+        if (e == cudaSuccess) ptrs[n++] = *out;
+        return e;
+    }
+    cudaError_t bytes(void** out, size_t nb) {
+        *out = nullptr;
+        cudaError_t e = cudaMallocAsync(out, nb > 0 ? nb : 1, st);
+        if (e == cudaSuccess) ptrs[n++] = *out;
+        return e;
+    }
+    ~Scratch() {
+        for (int i = 0; i < n; ++i) cudaFreeAsync(ptrs[i], st);
+    }
+};
 
 }  // namespace
 
@@ -104,72 +124,70 @@ cudaError_t launch_backward_deterministic(const BwdParams& p, int64_t n_cols, cu
                                           int* launches, bool* too_large) {
     *too_large = false;
     if (p.n_rows <= 0 || n_cols <= 0) return cudaSuccess;
+    Scratch sc{st};
     cudaError_t err;
     int64_t* s_rowptr = nullptr;
-    if ((err = alloc(&s_rowptr, p.n_rows + 1, st)) != cudaSuccess) return err;
+    if ((err = sc.get(&s_rowptr, p.n_rows + 1)) != cudaSuccess) return err;
     det_count<<<(unsigned)((p.n_rows + 1 + 255) / 256), 256, 0, st>>>(p, s_rowptr);
     ++*launches;
+    if ((err = cudaGetLastError()) != cudaSuccess) return err;
     void* temp = nullptr;
     size_t temp_bytes = 0;
-    cub::DeviceScan::InclusiveSum(nullptr, temp_bytes, s_rowptr + 1, s_rowptr + 1, p.n_rows, st);
-    if ((err = cudaMallocAsync(&temp, temp_bytes, st)) != cudaSuccess) return err;
-    cub::DeviceScan::InclusiveSum(temp, temp_bytes, s_rowptr + 1, s_rowptr + 1, p.n_rows, st);
+    if ((err = cub::DeviceScan::InclusiveSum(nullptr, temp_bytes, s_rowptr + 1, s_rowptr + 1, p.n_rows, st)) !=
+            cudaSuccess ||
+        (err = sc.bytes(&temp, temp_bytes)) != cudaSuccess ||
+        (err = cub::DeviceScan::InclusiveSum(temp, temp_bytes, s_rowptr + 1, s_rowptr + 1, p.n_rows, st)) !=
+            cudaSuccess)
+        return err;
     ++*launches;
-    cudaFreeAsync(temp, st);
     int64_t K = 0;                                            // the one D->H sync of this mode
     if ((err = cudaMemcpyAsync(&K, s_rowptr + p.n_rows, sizeof(K), cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
-        (err = cudaStreamSynchronize(st)) != cudaSuccess) {
-        cudaFreeAsync(s_rowptr, st);
+        (err = cudaStreamSynchronize(st)) != cudaSuccess)
         return err;
-    }
     if (K >= (int64_t)INT32_MAX || n_cols >= (int64_t)INT32_MAX) {
         *too_large = true;
-        cudaFreeAsync(s_rowptr, st);
         return cudaSuccess;
     }
-    if (K == 0) {
-        cudaFreeAsync(s_rowptr, st);
-        return cudaSuccess;
-    }
+    if (K == 0) return cudaSuccess;
     int32_t *key = nullptr, *key_s = nullptr, *slot = nullptr, *slot_s = nullptr, *slot_row = nullptr;
     float* slot_w = nullptr;
     int64_t* col_ptr = nullptr;
-    alloc(&key, K, st);
-    alloc(&key_s, K, st);
-    alloc(&slot, K, st);
-    alloc(&slot_s, K, st);
-    alloc(&slot_row, K, st);
-    alloc(&slot_w, K, st);
-    alloc(&col_ptr, n_cols + 1, st);
-    if ((err = cudaGetLastError()) != cudaSuccess) return err;
+    if ((err = sc.get(&key, K)) != cudaSuccess || (err = sc.get(&key_s, K)) != cudaSuccess ||
+        (err = sc.get(&slot, K)) != cudaSuccess || (err = sc.get(&slot_s, K)) != cudaSuccess ||
+        (err = sc.get(&slot_row, K)) != cudaSuccess || (err = sc.get(&slot_w, K)) != cudaSuccess ||
+        (err = sc.get(&col_ptr, n_cols + 1)) != cudaSuccess)
+        return err;
     det_records<<<(unsigned)((p.n_rows + kWpb - 1) / kWpb), kThr, 0, st>>>(p, s_rowptr, key, slot, slot_row,
                                                                            slot_w);
     ++*launches;
+    if ((err = cudaGetLastError()) != cudaSuccess) return err;
     int end_bit = 1;
     while (end_bit < 31 && (1ll << end_bit) < n_cols) ++end_bit;
     temp_bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, key, key_s, slot, slot_s, (int)K, 0, end_bit, st);
-    cudaMallocAsync(&temp, temp_bytes, st);
-    cub::DeviceRadixSort::SortPairs(temp, temp_bytes, key, key_s, slot, slot_s, (int)K, 0, end_bit, st);  // stable
+    void* temp2 = nullptr;
+    if ((err = cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, key, key_s, slot, slot_s, (int)K, 0, end_bit,
+                                               st)) != cudaSuccess ||
+        (err = sc.bytes(&temp2, temp_bytes)) != cudaSuccess ||
+        (err = cub::DeviceRadixSort::SortPairs(temp2, temp_bytes, key, key_s, slot, slot_s, (int)K, 0, end_bit,
+                                               st)) != cudaSuccess)  // stable
+        return err;
     ++*launches;
-    cudaFreeAsync(temp, st);
-    cudaMemsetAsync(col_ptr, 0, (size_t)(n_cols + 1) * sizeof(int64_t), st);
+    if ((err = cudaMemsetAsync(col_ptr, 0, (size_t)(n_cols + 1) * sizeof(int64_t), st)) != cudaSuccess) return err;
     det_col_hist<<<(unsigned)((K + 255) / 256), 256, 0, st>>>(key_s, K, col_ptr);
     ++*launches;
+    if ((err = cudaGetLastError()) != cudaSuccess) return err;
     temp_bytes = 0;
-    cub::DeviceScan::InclusiveSum(nullptr, temp_bytes, col_ptr + 1, col_ptr + 1, n_cols, st);
-    cudaMallocAsync(&temp, temp_bytes, st);
-    cub::DeviceScan::InclusiveSum(temp, temp_bytes, col_ptr + 1, col_ptr + 1, n_cols, st);
+    void* temp3 = nullptr;
+    if ((err = cub::DeviceScan::InclusiveSum(nullptr, temp_bytes, col_ptr + 1, col_ptr + 1, n_cols, st)) !=
+            cudaSuccess ||
+        (err = sc.bytes(&temp3, temp_bytes)) != cudaSuccess ||
+        (err = cub::DeviceScan::InclusiveSum(temp3, temp_bytes, col_ptr + 1, col_ptr + 1, n_cols, st)) != cudaSuccess)
+        return err;
     ++*launches;
-    cudaFreeAsync(temp, st);
     det_gather<<<(unsigned)((n_cols + kWpb - 1) / kWpb), kThr, 0, st>>>(p, n_cols, col_ptr, slot_s, slot_row,
                                                                          slot_w);
     ++*launches;
-    err = cudaGetLastError();
-    for (void* q : {(void*)key, (void*)key_s, (void*)slot, (void*)slot_s, (void*)slot_row, (void*)slot_w,
-                    (void*)col_ptr, (void*)s_rowptr})
-        cudaFreeAsync(q, st);
-    return err;
+    return cudaGetLastError();
 }
 
 }  // namespace es

@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { \
@@ -160,6 +161,85 @@ __global__ void gather_smem_fma(const float4* __restrict__ slab, const int* __re
   if (acc == 1234.5f) *sink = acc;
 }
 
+// MODE 5: the index chunks arrive by TMA (cp.async.bulk.tensor.1d over the index array, 32
+// indices = 128 B per chunk, issued two chunks ahead by one lane, mbarrier completion) and are
+// read back from shared memory -- the index loads leave the LSU / L1 miss path the gathers use.
+template <int D>
+__global__ void gather_smem_tmaidx(const __grid_constant__ CUtensorMap tm, const float4* __restrict__ slab,
+                                   long steps, float* sink) {
+  extern __shared__ float4 ring[];
+  constexpr int W = 4;
+  const int lane = threadIdx.x & 31, e = lane >> 3, sub = lane & 7, w = threadIdx.x >> 5;
+  const long warp = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  float4* my = ring + (size_t)w * D * 64 + e * 16 + sub;
+  __shared__ __align__(128) int idxbuf[W][3][32];
+  __shared__ __align__(8) uint64_t bars[W][3];
+  const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&bars[w][0]);
+  const uint32_t ib0 = (uint32_t)__cvta_generic_to_shared(&idxbuf[w][0][0]);
+  if (lane == 0) {
+    for (int i = 0; i < 3; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(bar0 + 8 * i));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  __syncwarp();
+  const long base = warp * steps * 4;
+  auto fetch = [&](long chunk) {                       // chunk -> buffer chunk % 3
+    if (lane == 0) {
+      const int b = (int)(chunk % 3);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], 128;" :: "r"(bar0 + 8 * b) : "memory");
+      asm volatile("cp.async.bulk.tensor.1d.shared::cta.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2}], [%3];"
+                   :: "r"(ib0 + 128 * b), "l"(&tm), "r"((int)(base + 32 * chunk)), "r"(bar0 + 8 * b) : "memory");
+    }
+  };
+  uint32_t phase[3] = {0, 0, 0};
+  auto wait = [&](long chunk) {
+    const int b = (int)(chunk % 3);
+    uint32_t done = 0;
+    while (!done)
+      asm volatile("{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.b32 %0,1,0,p;}"
+                   : "=r"(done) : "r"(bar0 + 8 * b), "r"(phase[b]) : "memory");
+    phase[b] ^= 1;
+  };
+  auto copy = [&](int d, int row) {
+    const float4* src = slab + (size_t)row * 16 + sub;
+    const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(my + d * 64);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(s0), "l"(src) : "memory");
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(s0 + 128), "l"(src + 8) : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  fetch(0); fetch(1); fetch(2);
+  wait(0);
+  float part[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+  for (int d = 0; d < D; ++d) copy(d, idxbuf[w][0][4 * d + e]);
+  const long nchunks = steps * 4 / 32;
+  for (long ch = 0; ch < nchunks; ++ch) {
+    const int b = (int)(ch % 3), bn = (int)((ch + 1) % 3);
+    if (ch + 1 < nchunks) wait(ch + 1);                // the next chunk's indices (two chunks of lead)
+#pragma unroll 1
+    for (int u0 = 0; u0 < 8; u0 += D) {
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        const int u = u0 + d;
+        asm volatile("cp.async.wait_group %0;" :: "n"(D - 1) : "memory");
+        const float4 a = my[d * 64], bb = my[d * 64 + 8];
+        part[0] = fmaf(1.0f, a.x, part[0]); part[1] = fmaf(1.0f, a.y, part[1]);
+        part[2] = fmaf(1.0f, a.z, part[2]); part[3] = fmaf(1.0f, a.w, part[3]);
+        part[4] = fmaf(1.0f, bb.x, part[4]); part[5] = fmaf(1.0f, bb.y, part[5]);
+        part[6] = fmaf(1.0f, bb.z, part[6]); part[7] = fmaf(1.0f, bb.w, part[7]);
+        const int tn = u + D;
+        const int cn = tn < 8 ? idxbuf[w][b][4 * tn + e] : idxbuf[w][bn][(4 * tn + e) & 31];
+        copy(d, cn);
+      }
+    }
+    __syncwarp();
+    if (ch + 3 < nchunks) fetch(ch + 3);               // buffer b is free again
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  float acc = 0.f;
+  for (int i = 0; i < 8; ++i) acc += part[i];
+  if (acc == 1234.5f) *sink = acc;
+}
+
 int main() {
   int nsm = 148, dev = 0, sm_clk = 0;
   CK(cudaGetDevice(&dev));
@@ -237,6 +317,23 @@ int main() {
       printf("{\"probe\":\"slab_inner_loop\",\"mode\":\"hashed rows + FMA\",\"warps_per_sm\":%d,\"GBps\":%.1f}\n", wps, bytes / ms / 1e6);
       ms = time_best([&] { gather_smem_fma<4, 4><<<grid, threads, smem>>>(buf, idx, steps, sink); }, 3);
       printf("{\"probe\":\"slab_inner_loop\",\"mode\":\"index loads L1::no_allocate + L2 evict_first hint + FMA\",\"warps_per_sm\":%d,\"GBps\":%.1f}\n", wps, bytes / ms / 1e6);
+      {
+        using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        CUtensorMap tm;
+        const cuuint64_t dims[1] = {(cuuint64_t)(nidx + 64)};
+        const cuuint64_t strides[1] = {4};
+        const cuuint32_t box[1] = {32};
+        const cuuint32_t es[1] = {1};
+        ((Encode)fn)(&tm, CU_TENSOR_MAP_DATA_TYPE_INT32, 1, idx, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        ms = time_best([&] { gather_smem_tmaidx<4><<<grid, threads, smem>>>(tm, buf, steps, sink); }, 3);
+        printf("{\"probe\":\"slab_inner_loop\",\"mode\":\"index chunks by TMA (1-D tensor map) into smem\",\"warps_per_sm\":%d,\"GBps\":%.1f}\n", wps, bytes / ms / 1e6);
+      }
       ms = time_best([&] { gather_smem_fma<4, 3><<<grid, threads, smem>>>(buf, idx, steps, sink); }, 3);
       printf("{\"probe\":\"slab_inner_loop\",\"mode\":\"index loads + FMA, zero-fill cp.async form\",\"warps_per_sm\":%d,\"GBps\":%.1f}\n", wps, bytes / ms / 1e6);
       cudaFree(idx);
