@@ -434,8 +434,10 @@ def main():
         # ncu: ~97 % of the step).  Its launches are timed alone here, live, on the launch
         # stream with the same L2 flush: the same call with reuse_sampled=1 runs exactly the
         # slice passes over the slots the timed steps sampled into the workspace.
-        wsl = 128 if a.bf16 else 64                        # elements per 256-B slab row
-        n_launch = (F + wsl - 1) // wsl
+        lc = es.es_launch_count()
+        launch(stream, reuse=True)                         # the slice passes alone: count them
+        torch.cuda.synchronize(dev)
+        n_launch = es.es_launch_count() - lc
         pe0 = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
         pe1 = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
         for i in range(a.steps):
@@ -446,9 +448,11 @@ def main():
             pe1[i].record(stream)
         torch.cuda.synchronize(dev)
         t_launch = float(np.sum([x.elapsed_time(y) for x, y in zip(pe0, pe1)])) / 1e3 / a.steps   # s per step
-        resident = n * 256 <= L2_RESIDENT_BYTES            # one slab of B
-        kname = (f"slab pass ({a.kernel if a.kernel != 'auto' else 'es::spmm_slab, shared-memory cp.async ring'}), "
-                 f"one launch per {wsl}-element feature slice ({n_launch}/step)")
+        slab_row = -(-(F * b_elem) // (16 * n_launch)) * 16   # bytes of B per row and slice (widest)
+        resident = n * slab_row <= L2_RESIDENT_BYTES       # one slab of B
+        fam = a.kernel if a.kernel not in ("auto", "slab", "slab_flow") else \
+            "es::spmm_slab_flow: persistent warps streaming slot-balanced row ranges"
+        kname = f"slab pass ({fam}), one launch per feature slice ({n_launch}/step, <= {slab_row} B of each B row)"
         what = ("the slab passes alone (reuse_sampled), timed live; the step adds count + scan + sample "
                 "materialisation")
     achieved = bytes_rank / t_launch / 1e9

@@ -149,7 +149,9 @@ enum {
     ES_KERNEL_SLAB_LDG = 8,     /* feature-sliced path, register-direct 256-bit gathers           */
     ES_KERNEL_SLAB_TMA = 9,     /* feature-sliced path, TMA tile::gather4 into a shared-memory ring */
     ES_KERNEL_ROWSTREAM = 10,   /* short rows: R rows per warp as one flat slot stream (F <= 128)   */
-    ES_KERNEL_SLAB_STREAM = 11  /* feature-sliced path, R rows per warp as one padded slot stream   */
+    ES_KERNEL_SLAB_STREAM = 11, /* feature-sliced path, R rows per warp as one padded slot stream   */
+    ES_KERNEL_SLAB_FLOW = 12    /* feature-sliced path, persistent warps streaming slot-balanced
+                                   row ranges across row boundaries (the plan's slab kernel)      */
 };
 
 /* Status word of a slab workspace (written by the device; reading it synchronises `stream`).

@@ -74,7 +74,7 @@ es_status_t read_opts(const es_spmm_options_t* o, Opts* out) {
         out->nnz = o->nnz;
     }
     if (ES_COVERS(o, tune)) {
-        if (o->kernel < ES_KERNEL_AUTO || o->kernel > ES_KERNEL_SLAB_STREAM) return ES_ERR_INVALID_VALUE;
+        if (o->kernel < ES_KERNEL_AUTO || o->kernel > ES_KERNEL_SLAB_FLOW) return ES_ERR_INVALID_VALUE;
         out->tune.kernel = o->kernel;
         out->tune.stages = o->tune[0];
         out->tune.width = o->tune[1];
@@ -88,6 +88,7 @@ es_status_t read_opts(const es_spmm_options_t* o, Opts* out) {
 // ---- slab path (es_slab.cu): when, and the workspace layout
 constexpr int64_t kSlabF = 64;                       // floats per feature slice (256-B slab rows)
 constexpr int64_t kSlabMaxBytes = (int64_t)80 << 20; // largest slab kept L2-resident (126 MB L2)
+constexpr int64_t kSlabMaxBytes24 = (int64_t)96 << 20;  // ... for 24-piece flow slices (Reddit: 89 MB)
 
 // A workspace was passed: the slab path runs whenever the layout allows -- F > 16, B rows 16-B
 // aligned, and a 64-float slab of B (n_cols x 256 B) fits L2.
@@ -109,22 +110,37 @@ bool slab_wanted(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t F, int64_t
 
 int64_t slab_align(int64_t x) { return (x + 255) & ~(int64_t)255; }
 
-// [header 256 B][s_rowptr (n+1) x 8][scan temp][s_colind cap x 4][s_val cap x 4]
+// [header 256 B][s_rowptr (n+1) x 8][scan temp][s_k n x 4][s_colind cap x 4][s_val cap x 4]
 struct SlabLayout {
-    int64_t off_rowptr, off_temp, temp_bytes, off_col, bytes_fixed;
+    int64_t off_rowptr, off_temp, temp_bytes, off_k, off_col, bytes_fixed;
 };
 SlabLayout slab_layout(int64_t n) {
     SlabLayout L{};
     L.off_rowptr = 256;
     L.off_temp = slab_align(L.off_rowptr + 8 * (n + 1));
     L.temp_bytes = (int64_t)es::slab_scan_temp_bytes(n);
-    L.off_col = slab_align(L.off_temp + L.temp_bytes);
+    L.off_k = slab_align(L.off_temp + L.temp_bytes);
+    L.off_col = slab_align(L.off_k + 4 * n);
     L.bytes_fixed = L.off_col;
     return L;
 }
 int64_t slab_bytes(int64_t n, int64_t cap, bool has_val) {
     const int64_t c = cap > 0 ? cap : 1;
     return slab_layout(n).bytes_fixed + slab_align(4 * c) + (has_val ? slab_align(4 * c) : 0);
+}
+// slots a workspace must hold: min(nnz, n*s) sampled slots plus up to 15 padding slots per row
+// (the flow layout pads every row to a multiple of 16 slots)
+int64_t slab_cap_needed(int64_t n, int64_t nnz, int32_t s) {
+    const int64_t ns = n * (int64_t)s;
+    return (nnz > 0 && nnz < ns ? nnz : ns) + 15 * n;
+}
+
+// Which slab kernel a call's options select: the flow kernel (default; padded slot layout, row
+// partition) unless a per-row slab kernel is forced (A/B) -- the layout follows the kernel, and
+// the sampling signature records it, so slots are never reused across layouts.
+bool slab_flow(const es::Tune& t) {
+    return t.kernel != ES_KERNEL_SLAB_SMEM && t.kernel != ES_KERNEL_SLAB_LDG && t.kernel != ES_KERNEL_SLAB_TMA &&
+           t.kernel != ES_KERNEL_SLAB_STREAM;
 }
 
 // The workspace's sampled-slot arrays (es_spmm_sample layout).
@@ -136,6 +152,7 @@ struct SlabSlots {
     int64_t cap;
     void* temp;
     size_t temp_bytes;
+    int32_t* s_k;        // flow layout: unpadded k_i
 };
 // false: the workspace cannot hold the slots the call may sample -- min(nnz, n*s) when the
 // caller stated nnz, else n*s (an undersized workspace is an error, never a truncation)
@@ -143,8 +160,7 @@ bool slab_slots(const Opts& o, int64_t n, int32_t s, bool has_val, SlabSlots* ou
     const SlabLayout L = slab_layout(n);
     const int64_t per_slot = has_val ? 8 : 4;
     int64_t cap = (o.workspace_bytes - L.bytes_fixed - (has_val ? 256 : 0)) / per_slot;
-    const int64_t need_max = n * (int64_t)s;
-    const int64_t need = o.nnz > 0 && o.nnz < need_max ? o.nnz : need_max;
+    const int64_t need = slab_cap_needed(n, o.nnz, s);
     if (cap < need || cap < 1) return false;
     char* ws = static_cast<char*>(o.workspace);
     out->hdr = reinterpret_cast<es::WsHeader*>(ws);
@@ -154,6 +170,7 @@ bool slab_slots(const Opts& o, int64_t n, int32_t s, bool has_val, SlabSlots* ou
     out->cap = cap;
     out->temp = ws + L.off_temp;
     out->temp_bytes = (size_t)L.temp_bytes;
+    out->s_k = reinterpret_cast<int32_t*>(ws + L.off_k);
     return true;
 }
 
@@ -162,7 +179,7 @@ bool slab_slots(const Opts& o, int64_t n, int32_t s, bool has_val, SlabSlots* ou
 // count with min(d_i, s) from the caller's rowptr), so a re-uploaded copy of the same CSR may be
 // reused, a different one is caught.
 uint64_t sampling_signature(int64_t n, int64_t row_begin, int32_t s, int32_t strategy, uint64_t seed,
-                            uint32_t prime, int64_t nnz_base, bool has_val) {
+                            uint32_t prime, int64_t nnz_base, bool has_val, int32_t pad) {
     uint64_t h = 0x6a09e667f3bcc908ull;
     auto mix = [&](uint64_t x) {
         h ^= x + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2);
@@ -170,20 +187,23 @@ uint64_t sampling_signature(int64_t n, int64_t row_begin, int32_t s, int32_t str
         h ^= h >> 31;
     };
     mix((uint64_t)n); mix((uint64_t)row_begin); mix((uint64_t)s); mix((uint64_t)strategy); mix(seed);
-    mix(prime); mix((uint64_t)nnz_base); mix(has_val ? 1u : 0u);
+    mix(prime); mix((uint64_t)nnz_base); mix(has_val ? 1u : 0u); mix((uint64_t)pad);
     return h ? h : 1;
 }
 
-// a1-a3 once into the workspace: count, scan, materialise, sign
+// a1-a3 once into the workspace: count, scan, materialise, sign; for the flow layout rows padded
+// to 4 slots and each row's unpadded k_i
 cudaError_t slab_sample(const SlabSlots& sl, const int64_t* rowptr, int64_t nnz_base, const int32_t* colind,
                         const float* val, int64_t n, int32_t s, int32_t strategy, uint64_t seed, int64_t row_begin,
-                        uint32_t prime, uint64_t sig, cudaStream_t st, int* launches) {
+                        uint32_t prime, uint64_t sig, cudaStream_t st, int* launches, bool flow = false) {
+    const int32_t pad = flow ? 16 : 1;
     // the count kernel clears the header (status 0, signature invalid) and the materialisation
     // signs it: no extra launches
-    cudaError_t err = es::launch_slab_count(rowptr, n, s, sl.s_rowptr, sl.temp, sl.temp_bytes, st, launches, sl.hdr);
+    cudaError_t err = es::launch_slab_count(rowptr, n, s, sl.s_rowptr, sl.temp, sl.temp_bytes, st, launches, sl.hdr,
+                                            pad, flow ? sl.s_k : nullptr);
     if (err != cudaSuccess) return err;
     err = es::launch_sample_materialize(rowptr, nnz_base, colind, val, n, s, strategy, seed, row_begin, prime,
-                                        sl.s_rowptr, sl.s_col, sl.s_val, nullptr, st, sl.cap, sl.hdr, sig);
+                                        sl.s_rowptr, sl.s_col, sl.s_val, nullptr, st, sl.cap, sl.hdr, sig, pad);
     ++*launches;
     return err;
 }
@@ -202,7 +222,7 @@ es_status_t run_rows_impl(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
     const es::Tune& tn = o.tune;
     const bool force_slab = tn.kernel == ES_KERNEL_SLAB || tn.kernel == ES_KERNEL_SLAB_SMEM ||
                             tn.kernel == ES_KERNEL_SLAB_LDG || tn.kernel == ES_KERNEL_SLAB_TMA ||
-                            tn.kernel == ES_KERNEL_SLAB_STREAM;
+                            tn.kernel == ES_KERNEL_SLAB_STREAM || tn.kernel == ES_KERNEL_SLAB_FLOW;
     const uintptr_t bu = reinterpret_cast<uintptr_t>(B), cu = reinterpret_cast<uintptr_t>(C);
     const int64_t esz = o.bf16 ? 2 : 4;
     const bool slab_layout_ok = o.workspace && bu % 16 == 0 && (ldb * esz) % 16 == 0 && slab_feasible(n_cols, F) &&
@@ -213,24 +233,23 @@ es_status_t run_rows_impl(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
     if (slab_layout_ok) {
         // any C layout: 16-B vector stores where C's rows allow them, scalar stores otherwise
         const bool c_vec16 = cu % 16 == 0 && ldc % 4 == 0;
-        // Bucket takes the first k_i entries of each row: they already lie contiguous in the
-        // CSR (Alg. 1 with p_j = j), so the passes read them in place -- no sampling pass
-        const bool direct = strategy == ES_BUCKET;
+        // the flow kernel (default) streams a padded, partitioned slot layout; a forced per-row
+        // kernel reads the compact one -- and for Bucket, whose sampled slots are the first k_i
+        // entries of each row (Alg. 1 with p_j = j), the CSR itself (no sampling pass)
+        const bool flow = slab_flow(tn);
+        const bool direct = strategy == ES_BUCKET && !flow;
         SlabSlots sl{};
         if (!direct && !slab_slots(o, n, s, val != nullptr, &sl)) return ES_ERR_INVALID_VALUE;
         int launches = 0;
         cudaError_t err = cudaSuccess;
-        const uint64_t sig = sampling_signature(n, row_begin, s, strategy, seed, o.prime, nnz_base, val != nullptr);
+        const uint64_t sig = sampling_signature(n, row_begin, s, strategy, seed, o.prime, nnz_base, val != nullptr,
+                                                flow ? 16 : 1);
         if (!o.reuse_sampled && !direct)
             err = slab_sample(sl, rowptr, nnz_base, colind, val, n, s, strategy, seed, row_begin, o.prime, sig, st,
-                              &launches);
-        // slices of 256-B slab rows: 64 fp32 or 128 bf16 elements
-        const int64_t wsl = o.bf16 ? 2 * kSlabF : kSlabF;
+                              &launches, flow);
         const bool b32 = bu % 32 == 0 && (ldb * esz) % 32 == 0;
-        CUtensorMap tmap;
-        const bool use_tma = tn.kernel == ES_KERNEL_SLAB_TMA;
-        if (use_tma && !es::encode_b_tensor_map(&tmap, B, F, ldb, n_cols, o.bf16)) return ES_ERR_UNSUPPORTED;
-        for (int64_t c0 = 0; err == cudaSuccess && c0 < F; c0 += wsl) {
+        // one slice: columns [c0, c0 + w) of B and C
+        auto slice = [&](int64_t c0, int64_t w) {
             es::SlabParams sp{};
             sp.s_rowptr = direct ? rowptr : sl.s_rowptr;
             sp.slot_base = direct ? nnz_base : 0;
@@ -240,19 +259,18 @@ es_status_t run_rows_impl(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
             sp.direct_s = direct ? s : 0;
             sp.ws_status = direct ? nullptr : &sl.hdr->status;
             sp.ws_sig = direct ? nullptr : &sl.hdr->sig;
+            sp.s_k = flow ? sl.s_k : nullptr;
             sp.sig = sig;
+            sp.s = s;
             sp.reuse_s = (o.reuse_sampled && !direct) ? s : 0;
             sp.rowptr = rowptr;
             sp.b_bf16 = o.bf16;
             sp.B = o.bf16 ? reinterpret_cast<const float*>(static_cast<const uint16_t*>(B) + c0)
                           : static_cast<const float*>(B) + c0;
             sp.ldb = ldb;
-            sp.w = (int32_t)(F - c0 < wsl ? F - c0 : wsl);
+            sp.w = (int32_t)w;
             sp.b32 = b32 ? 1 : 0;
-            const bool ldg = b32 && tn.kernel == ES_KERNEL_SLAB_LDG;
-            if (tn.kernel == ES_KERNEL_SLAB_LDG && !b32) return ES_ERR_UNSUPPORTED;
-            // 16-B pieces (shared-memory ring) or 32-B pieces (register-direct)
-            sp.nv = ldg ? (int32_t)((sp.w * esz + 31) / 32) : (int32_t)((sp.w * esz + 15) / 16);
+            sp.nv = (int32_t)((w * esz + 15) / 16);     // 16-B pieces
             sp.C = C + c0;
             sp.c_peers = o.c_peers;
             sp.n_peers = o.n_peers;
@@ -264,12 +282,48 @@ es_status_t run_rows_impl(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
             sp.n_rows = n;
             sp.reduce = reduce;
             sp.mean_by_degree = o.mean_by_degree;
-            if (use_tma) {
-                sp.nv = (int32_t)((sp.w * esz + 15) / 16);
-                err = es::launch_slab_pass_tma(tmap, sp, (int32_t)c0, (int32_t)n_cols, tn, st);
-            } else {
-                err = es::launch_slab_pass(sp, tn, st);
+            return sp;
+        };
+        if (flow) {
+            // slices of MP 16-B pieces (tune.width 8, 16 or 24; default 16 = 256-B slab rows), so
+            // every slice starts on a 128-B line (a slice start inside a line makes each 8-lane
+            // copy touch two lines: 15- and 19-piece slices ran 35 % slower per byte); a remainder
+            // of <= 24 - MP pieces joins the last slice (3 pieces per lane) instead of running as
+            // a narrow pass of its own -- F = 602: 8 x 16 + 23 pieces
+            const int64_t epp = 16 / esz;                     // elements per piece
+            const int64_t NP = (F + epp - 1) / epp;
+            auto passes = [&](int64_t mp) {
+                const int64_t q = NP / mp, r = NP % mp;
+                return q + ((r > 0 && !(q > 0 && mp + r <= 24)) ? 1 : 0);
+            };
+            // default: the width with fewer passes (a pass costs about the same from 16 to 24
+            // pieces on a 2.4-KB-pitch B: Reddit F=602 7 passes of 24 (+7) 7.17 ms vs 9 of 16 (+7
+            // merged) 9.15 ms; F=128: 2 x 16), 24 only while its slab (n_cols x 384 B) fits L2
+            int64_t MP = (tn.width == 8 || tn.width == 16 || tn.width == 24) ? tn.width : 16;
+            if (tn.width == 0 && passes(24) < passes(16) && n_cols * 384 <= kSlabMaxBytes24) MP = 24;
+            const int64_t m = passes(MP);
+            for (int64_t i = 0; err == cudaSuccess && i < m; ++i) {
+                const int64_t c0 = i * MP * epp;
+                const int64_t np_i = (i + 1 == m) ? NP - i * MP : MP;
+                const int64_t w = F - c0 < np_i * epp ? F - c0 : np_i * epp;
+                err = es::launch_slab_flow(slice(c0, w), tn, st);
+                ++launches;
             }
+            g_launches.fetch_add(launches, std::memory_order_relaxed);
+            return err == cudaSuccess ? ES_OK : ES_ERR_CUDA;
+        }
+        // per-row slab kernels (A/B): slices of 256-B slab rows, 64 fp32 or 128 bf16 elements
+        const int64_t wsl = o.bf16 ? 2 * kSlabF : kSlabF;
+        CUtensorMap tmap;
+        const bool use_tma = tn.kernel == ES_KERNEL_SLAB_TMA;
+        if (use_tma && !es::encode_b_tensor_map(&tmap, B, F, ldb, n_cols, o.bf16)) return ES_ERR_UNSUPPORTED;
+        if (tn.kernel == ES_KERNEL_SLAB_LDG && !b32) return ES_ERR_UNSUPPORTED;
+        for (int64_t c0 = 0; err == cudaSuccess && c0 < F; c0 += wsl) {
+            es::SlabParams sp = slice(c0, F - c0 < wsl ? F - c0 : wsl);
+            // 16-B pieces (shared-memory ring) or 32-B pieces (register-direct)
+            if (b32 && tn.kernel == ES_KERNEL_SLAB_LDG) sp.nv = (int32_t)((sp.w * esz + 31) / 32);
+            if (use_tma) err = es::launch_slab_pass_tma(tmap, sp, (int32_t)c0, (int32_t)n_cols, tn, st);
+            else err = es::launch_slab_pass(sp, tn, st);
             ++launches;
         }
         g_launches.fetch_add(launches, std::memory_order_relaxed);
@@ -329,8 +383,7 @@ int64_t es_spmm_workspace_bytes(int64_t n_rows, int64_t n_cols, int64_t nnz, int
                                 int32_t s, int32_t has_val) {
     if (n_rows <= 0 || n_cols < 0 || nnz < 0 || F < 1 || ldb < F || s < 1) return 0;
     if (!slab_wanted(n_rows, n_cols, nnz, F, ldb, s)) return 0;
-    const int64_t cap = nnz < n_rows * (int64_t)s ? nnz : n_rows * (int64_t)s;
-    return slab_bytes(n_rows, cap, has_val != 0) + 256;
+    return slab_bytes(n_rows, slab_cap_needed(n_rows, nnz, s), has_val != 0) + 256;
 }
 
 int64_t es_spmm_workspace_bytes_ex(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t F, int64_t ldb,
@@ -339,13 +392,12 @@ int64_t es_spmm_workspace_bytes_ex(int64_t n_rows, int64_t n_cols, int64_t nnz, 
     if (read_opts(opt, &o) != ES_OK) return 0;
     const int k = o.tune.kernel;
     if (k != ES_KERNEL_SLAB && k != ES_KERNEL_SLAB_SMEM && k != ES_KERNEL_SLAB_LDG && k != ES_KERNEL_SLAB_TMA &&
-        k != ES_KERNEL_SLAB_STREAM)
+        k != ES_KERNEL_SLAB_STREAM && k != ES_KERNEL_SLAB_FLOW)
         return es_spmm_workspace_bytes(n_rows, n_cols, nnz, F, ldb, s, has_val);
     // a slab kernel forced: a workspace wherever the path can run at all
     if (n_rows <= 0 || n_cols < 0 || nnz < 0 || F < 1 || ldb < F || s < 1) return 0;
     if (!slab_feasible(n_cols, F) || ldb % 4 != 0) return 0;
-    const int64_t cap = nnz < n_rows * (int64_t)s ? nnz : n_rows * (int64_t)s;
-    return slab_bytes(n_rows, cap, has_val != 0) + 256;
+    return slab_bytes(n_rows, slab_cap_needed(n_rows, nnz, s), has_val != 0) + 256;
 }
 
 es_status_t es_spmm_workspace_status(void* workspace, int64_t workspace_bytes, int32_t reset, int32_t* status_out,
@@ -500,10 +552,15 @@ es_status_t es_spmm_backward_ex(int64_t n_rows, int64_t n_cols, const int64_t* r
         cudaStream_t st = as_stream(stream);
         int launches = 0;
         cudaError_t err = cudaSuccess;
-        const uint64_t sig = sampling_signature(n, row_begin, s, strategy, seed, o.prime, nnz_base, val != nullptr);
+        // the layout the forward call's plan samples (padded + partitioned unless a per-row slab
+        // kernel is forced), so reuse_sampled finds the forward's slots
+        const bool flow = slab_flow(o.tune);
+        const int32_t pad = flow ? 16 : 1;
+        const uint64_t sig = sampling_signature(n, row_begin, s, strategy, seed, o.prime, nnz_base, val != nullptr,
+                                                pad);
         if (!o.reuse_sampled && !direct)
             err = slab_sample(sl, rowptr, nnz_base, colind, val, n, s, strategy, seed, row_begin, o.prime, sig, st,
-                              &launches);
+                              &launches, flow);
         for (int64_t c0 = 0; err == cudaSuccess && c0 < F; c0 += kSlabF) {
             es::SlabParams sp{};
             sp.s_rowptr = direct ? rowptr : sl.s_rowptr;
@@ -516,6 +573,8 @@ es_status_t es_spmm_backward_ex(int64_t n_rows, int64_t n_cols, const int64_t* r
             sp.ws_sig = direct ? nullptr : &sl.hdr->sig;
             sp.sig = sig;
             sp.reuse_s = (o.reuse_sampled && !direct) ? s : 0;
+            sp.s = s;
+            sp.pad = direct ? 1 : pad;
             sp.rowptr = rowptr;
             sp.ldb = ldb;
             sp.w = (int32_t)(F - c0 < kSlabF ? F - c0 : kSlabF);
@@ -651,7 +710,8 @@ HostLayout host_layout(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t F, i
     L.off_C = L.off_B + align256(n_cols * ldb * 4);
     L.off_slab = L.off_C + align256(n_rows * ldb * 4);
     // room for the slab path (sampled slots of any s: at most nnz) where the layout can take it
-    L.slab_bytes = (slab_feasible(n_cols, F) && F >= 128 && ldb % 4 == 0) ? slab_bytes(n_rows, nnz, has_val) + 256 : 0;
+    L.slab_bytes = (slab_feasible(n_cols, F) && F >= 128 && ldb % 4 == 0)
+                       ? slab_bytes(n_rows, nnz + 15 * n_rows, has_val) + 256 : 0;
     L.total = L.off_slab + L.slab_bytes;
     return L;
 }

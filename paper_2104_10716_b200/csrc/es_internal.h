@@ -111,6 +111,10 @@ struct SlabParams {
     const uint64_t* ws_sig;   // signature written by the sampling call (NULL: not checked)
     uint64_t sig;             // the signature this call expects
     int32_t reuse_s;          // > 0 (reuse_sampled): also check each row's slot count == min(d_i, reuse_s)
+    // flow layout (spmm_slab_flow): rows padded to 4-slot multiples, k_i = min(d_i, s) from rowptr
+    int32_t s;                // the sampling cap s
+    const int32_t* s_k;       // flow layout: k_i = min(d_i, s) of every row (the count kernel's)
+    int32_t pad;              // backward: slot padding of the layout (1 compact, 4 flow; col -1 = padding)
 };
 
 // workspace header (first 256 B of a slab workspace)
@@ -122,6 +126,9 @@ struct WsHeader {
 constexpr int kWsOverflow = 1, kWsSignature = 2;
 
 cudaError_t launch_slab_pass(const SlabParams& p, const Tune& t, cudaStream_t st);
+// Flow slab path (the default, es_slab.cu spmm_slab_flow): one slice pass over the padded slot
+// layout.  Slices of up to 16 pieces run the 2-piece-per-lane kernel, up to 24 the 3-piece one.
+cudaError_t launch_slab_flow(const SlabParams& p, const Tune& t, cudaStream_t st);
 // TMA gather4 slab pass: tm = a 2-D tensor map over B (inner dim F elements, rows n_cols, box
 // {256 B of elements, 1}), c0 = the slice's first column
 cudaError_t launch_slab_pass_tma(const CUtensorMap& tm, const SlabParams& p, int32_t c0, int32_t n_cols,
@@ -135,9 +142,12 @@ cudaError_t launch_slab_backward(const SlabParams& p, const float* dC, float* dB
 size_t slab_scan_temp_bytes(int64_t n);
 // hdr (may be NULL): the workspace header, cleared by the count kernel (status 0, signature 0)
 cudaError_t launch_slab_count(const int64_t* rowptr, int64_t n, int32_t s, int64_t* s_rowptr, void* temp,
-                              size_t temp_bytes, cudaStream_t st, int* launches, WsHeader* hdr = nullptr);
+                              size_t temp_bytes, cudaStream_t st, int* launches, WsHeader* hdr = nullptr,
+                              int32_t pad = 1, int32_t* s_k = nullptr);
+// s_k (may be NULL): k_i of every row, unpadded
 cudaError_t launch_sample_count_only(const int64_t* rowptr, int64_t n, int32_t s, int64_t* s_rowptr,
-                                     cudaStream_t st, WsHeader* hdr = nullptr);
+                                     cudaStream_t st, WsHeader* hdr = nullptr, int32_t pad = 1,
+                                     int32_t* s_k = nullptr);
 
 cudaError_t launch_backward(const BwdParams& p, cudaStream_t st);
 cudaError_t launch_backward_deterministic(const BwdParams& p, int64_t n_cols, cudaStream_t st, int* launches,
@@ -155,6 +165,6 @@ cudaError_t launch_sample_materialize(const int64_t* rowptr, int64_t nnz_base, c
                                       uint64_t seed, int64_t row_base, uint32_t prime,
                                       const int64_t* s_rowptr, int32_t* s_colind, float* s_val,
                                       int64_t* s_pos, cudaStream_t st, int64_t cap = INT64_MAX,
-                                      WsHeader* hdr = nullptr, uint64_t sig = 0);
+                                      WsHeader* hdr = nullptr, uint64_t sig = 0, int32_t pad = 1);
 
 }  // namespace es

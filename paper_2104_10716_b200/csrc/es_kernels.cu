@@ -941,8 +941,11 @@ cudaError_t launch_backward(const BwdParams& p, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------ sampler (es_spmm_sample)
+// k_i = min(d_i, s), rounded up to a multiple of `pad` slots (pad 4: the flow slab layout, whose
+// rows start on a 4-slot step; 1 elsewhere)
 __global__ void sample_count(const int64_t* __restrict__ rowptr, int64_t n, int32_t s,
-                             int64_t* __restrict__ s_rowptr, WsHeader* hdr) {
+                             int64_t* __restrict__ s_rowptr, WsHeader* hdr, int32_t pad,
+                             int32_t* __restrict__ s_k) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i == 0) {
         s_rowptr[0] = 0;
@@ -950,7 +953,9 @@ __global__ void sample_count(const int64_t* __restrict__ rowptr, int64_t n, int3
     }
     if (i < n) {
         const int64_t d = rowptr[i + 1] - rowptr[i];
-        s_rowptr[i + 1] = d < (int64_t)s ? d : (int64_t)s;
+        const int64_t k = d < (int64_t)s ? d : (int64_t)s;
+        s_rowptr[i + 1] = (k + pad - 1) / pad * pad;
+        if (s_k) s_k[i] = (int32_t)k;
     }
 }
 
@@ -960,7 +965,7 @@ sample_materialize(const int64_t* __restrict__ rowptr, int64_t nnz_base,
                    int32_t s, int32_t strategy, uint64_t seed, int64_t row_base, uint32_t prime,
                    const int64_t* __restrict__ s_rowptr, int32_t* __restrict__ s_colind,
                    float* __restrict__ s_val, int64_t* __restrict__ s_pos, int64_t cap, WsHeader* hdr,
-                   uint64_t sig) {
+                   uint64_t sig, int32_t pad) {
     const int lane = threadIdx.x & 31;
     const int64_t r = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
     if (hdr && blockIdx.x == 0 && threadIdx.x == 0) hdr->sig = sig;    // the slots' signature
@@ -970,13 +975,20 @@ sample_materialize(const int64_t* __restrict__ rowptr, int64_t nnz_base,
     const int64_t o0 = s_rowptr[r];
     // overflow backstop: the row's slots do not fit (the caller understated nnz); the slab
     // passes poison the row (es_slab.cu slab_row_guard) -- flagged here too
-    if (hdr && lane == 0 && o0 + rs.k > cap) atomicOr(&hdr->status, kWsOverflow);
+    if (hdr && lane == 0 && o0 + (rs.k + pad - 1) / pad * pad > cap) atomicOr(&hdr->status, kWsOverflow);
     for (int32_t j = lane; j < rs.k && o0 + j < cap; j += 32) {
         const int64_t pj = rs.pos(j);
         const int64_t e = rs.beg + pj;
         s_colind[o0 + j] = colind[e];
         if (s_val) s_val[o0 + j] = val ? val[e] : 1.0f;
         if (s_pos) s_pos[o0 + j] = pj;
+    }
+    // padding slots of the flow layout (k_i .. next multiple of pad): column -1, value 0 -- the
+    // flow kernel zero-fills their pieces, so they add exactly +0
+    const int32_t kp = (rs.k + pad - 1) / pad * pad;
+    if (lane < kp - rs.k && o0 + rs.k + lane < cap) {
+        s_colind[o0 + rs.k + lane] = -1;
+        if (s_val) s_val[o0 + rs.k + lane] = 0.0f;
     }
 }
 
@@ -1276,9 +1288,9 @@ cudaError_t launch_spmm(SpmmParams p, const Plan& plan, const Tune& t, cudaStrea
 }
 
 cudaError_t launch_sample_count_only(const int64_t* rowptr, int64_t n, int32_t s, int64_t* s_rowptr,
-                                     cudaStream_t st, WsHeader* hdr) {
+                                     cudaStream_t st, WsHeader* hdr, int32_t pad, int32_t* s_k) {
     const int64_t blocks = (n + 1 + 255) / 256;
-    sample_count<<<(unsigned)(blocks > 0 ? blocks : 1), 256, 0, st>>>(rowptr, n, s, s_rowptr, hdr);
+    sample_count<<<(unsigned)(blocks > 0 ? blocks : 1), 256, 0, st>>>(rowptr, n, s, s_rowptr, hdr, pad, s_k);
     return cudaGetLastError();
 }
 
@@ -1304,12 +1316,13 @@ cudaError_t launch_sample_materialize(const int64_t* rowptr, int64_t nnz_base, c
                                       uint64_t seed, int64_t row_base, uint32_t prime,
                                       const int64_t* s_rowptr, int32_t* s_colind, float* s_val,
                                       int64_t* s_pos, cudaStream_t st, int64_t cap, WsHeader* hdr,
-                                      uint64_t sig) {
+                                      uint64_t sig, int32_t pad) {
     if (n <= 0) return cudaSuccess;
     const int64_t blocks = (n + kWarps - 1) / kWarps;
     sample_materialize<<<(unsigned)blocks, kThreads, 0, st>>>(rowptr, nnz_base, colind, val, n, s,
                                                                strategy, seed, row_base, prime,
-                                                               s_rowptr, s_colind, s_val, s_pos, cap, hdr, sig);
+                                                               s_rowptr, s_colind, s_val, s_pos, cap, hdr, sig,
+                                                               pad);
     return cudaGetLastError();
 }
 

@@ -13,6 +13,7 @@
 // group adds its partial to its total every 32 slots; the group totals are added by an xor tree
 // (with S = 2 groups the order of spmm_cpasync_hw, bitwise; DESIGN.md §6 error bound).
 // Also here: the feature-sliced backward (spmm_slab_bwd, NEXT-2).
+#include <atomic>
 #include <cstdint>
 #include <type_traits>
 #include <cuda.h>
@@ -120,6 +121,55 @@ __device__ __forceinline__ void slab_store_piece(const SlabParams& p, int64_t r,
         } else {                                     // fused all-gather: every rank's C (NEXT-1)
             const int64_t off = (p.row_base + r) * p.ldc + p.col0 + c0;
             for (int q = 0; q < p.n_peers; ++q) put(p.c_peers[q] + off);
+        }
+    }
+}
+
+// Stores of 4 results to peer ranks' C or through NVLS multicast (the fused all-gather): out of
+// line, so the flow kernel's row epilogue stays small in the instruction stream.
+__device__ __noinline__ void slab_store_remote(const SlabParams& p, int64_t r, int c0, int rem, float r0, float r1,
+                                               float r2, float r3) {
+    const float res[4] = {r0, r1, r2, r3};
+    const int64_t off = (p.row_base + r) * p.ldc + p.col0 + c0;
+    const uint64_t pol = policy_evict_first();
+    if (p.c_mc) {
+        if (p.c_vec && rem >= 4) st_multicast4(p.c_mc + off, res);
+        else
+            for (int c = 0; c < 4 && c < rem; ++c) st_multicast(p.c_mc + off + c, res[c]);
+        return;
+    }
+    for (int q = 0; q < p.n_peers; ++q) {
+        if (p.c_vec && rem >= 4) st_stream4(p.c_peers[q] + off, res, pol);
+        else
+            for (int c = 0; c < 4 && c < rem; ++c) st_stream(p.c_peers[q] + off + c, res[c], pol);
+    }
+}
+
+// slab_store_piece with the MEAN divisor already converted to float (flow kernel; (float)k_i or
+// (float)d_i -- the same value the int64 form converts)
+template <int E>
+__device__ __forceinline__ void slab_store_piece_f(const SlabParams& p, int64_t r, int col, const float* tot,
+                                                   float div, uint64_t pol) {
+#pragma unroll
+    for (int h4 = 0; h4 < E / 4; ++h4) {
+        const int c0 = col + 4 * h4;
+        const int rem = p.w - c0;
+        if (rem <= 0) break;
+        float res[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const float t = tot[4 * h4 + c];
+            res[c] = p.reduce == kMean ? (div > 0.0f ? __fdiv_rn(t, div) : 0.0f) : t;
+        }
+        if (p.c_mc || p.n_peers > 0) {
+            slab_store_remote(p, r, c0, rem, res[0], res[1], res[2], res[3]);
+        } else {
+            float* dst = p.C + r * p.ldc + c0;
+            if (p.c_vec && rem >= 4) st_stream4(dst, res, pol);
+            else
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    if (c < rem) st_stream(dst + c, res[c], pol);
         }
     }
 }
@@ -434,6 +484,330 @@ spmm_slab(const SlabParams p) {
             if (FULL || piece < p.nv) slab_store_piece<E>(p, r, piece * E, tot[q], div, pol_a);
         }
     }
+}
+
+// ---------------------------------------------------------------- flow slab kernel (the default)
+// The per-row ring kernel above pays, for every (row, slice): the rowptr -> (col, val) -> first
+// copies latency chain before its ring is full, the ring's drain at the row's end (refills of
+// steps past k_i are zero-fills that still write shared memory), and a 4-row CTA that waits for
+// its longest row.  Here a PERSISTENT warp owns a contiguous range of rows balanced by slots
+// (flow_search below), and the rows' sampled slots -- padded in the
+// workspace to multiples of 4 (column -1, value 0; es_kernels.cu sample_materialize) -- are ONE
+// contiguous stream of 4-slot steps.  The cp.async ring therefore runs D steps ahead across row
+// boundaries, the (col, val) chunks are 32 consecutive stream slots loaded one chunk ahead, and
+// the row metadata (slot ends, divisors) is loaded 32 rows at a time, one batch ahead: a warp
+// pays the latency chain once per pass instead of once per row.  Each step belongs to exactly
+// one row (the padding), so a row's end is an event of the step stream: after the step that
+// completes it, the group partials are combined and stored.
+// Per element (bitwise the order of spmm_slab<8, 2, ...>): group e = lane / 8 sums slots
+// j = e (mod 4) of the row in slot order, with partials over the row's 32-slot chunks (flushed
+// when the stream passes row-local step 8m), then the xor tree over the 4 groups.  Padding
+// slots add exactly +0 (zero-filled pieces).
+// P = 16-B pieces per lane: a slice of up to 8P pieces (P = 3: 96 fp32 / 192 bf16 elements),
+// so F = 602 runs as 7 balanced passes of 21-22 pieces instead of 9 x 16 plus a 7-piece tail.
+__device__ __noinline__ void slab_fill_row(const SlabParams& p, int64_t r, float v) {
+    for (int c = threadIdx.x & 31; c < p.w; c += 32) {
+        if (p.c_mc) st_multicast(p.c_mc + (p.row_base + r) * p.ldc + p.col0 + c, v);
+        else if (p.n_peers == 0) p.C[r * p.ldc + c] = v;
+        else
+            for (int q = 0; q < p.n_peers; ++q) p.c_peers[q][(p.row_base + r) * p.ldc + p.col0 + c] = v;
+    }
+}
+
+// The row partition of the flow grid: warp w of nw owns rows [i(w), i(w+1)) where i(w) is the
+// smallest row index with s_rowptr[i] + kFlowRowCost * i >= total * w / nw (the rows' padded
+// slots plus a per-row cost for the epilogue and store, in slot units).  Found by the warp
+// itself with a 32-ary search (each round probes 32 rows, one per lane, and keeps the interval
+// between the last probe below the target and the first at or above it): ~log32(n) dependent
+// loads instead of a partition array in the workspace, so every pass kernel can size its own
+// persistent grid.
+constexpr int64_t kFlowRowCost = 8;
+constexpr int kFlowPad = 16;         // slots: every row of the flow layout is a whole number of 4-step blocks
+
+// Per-warp rare-path state of the flow kernel (shared memory, after the ring).
+struct FlowMeta {
+    int64_t rb, P0;                 // the warp's first row and first slot
+    int32_t nrows, bo, bstart;      // rows; first row of the current batch (from rb); its first step
+    int32_t caprel, fetch_t;        // capacity bound (relative to P0); step of the last batch fetch
+    uint32_t live, pmask;           // rows of the batch still to stream / to poison at their end
+    int32_t endstep[32];            // lane i: row bo + i ends before this stream step
+    float divf[32];                 // lane i: its MEAN divisor
+    int32_t nse[2][32], nk[2][32];  // raw batches (double-buffered): s_rowptr[r+1] low word, k_i
+};
+__device__ __forceinline__ int64_t flow_search(const int64_t* __restrict__ s_rowptr, int64_t n, int64_t target,
+                                               int lane) {
+    int64_t lo = 0, hi = n;          // answer in [lo, hi]; s_rowptr[hi] + c*hi >= target
+    while (lo < hi) {
+        const int64_t q = lo + (hi - lo) * (lane + 1) / 32;      // lane 31 probes hi
+        const bool ge = ld_stream(s_rowptr + q, policy_evict_first()) + kFlowRowCost * q >= target;
+        const int f = __ffs(__ballot_sync(kAll, ge)) - 1;       // lane 31 always votes
+        const int64_t qf = __shfl_sync(kAll, q, f);
+        const int64_t qb = __shfl_sync(kAll, q, f > 0 ? f - 1 : 0);
+        lo = f > 0 ? qb + 1 : lo;
+        hi = qf;
+    }
+    return lo;
+}
+
+template <int G, int P, int D, int W, int MINB, bool FULL, bool BF16>
+__global__ void __launch_bounds__(32 * W, MINB)
+spmm_slab_flow(const __grid_constant__ SlabParams p) {
+    constexpr int E = SlabPiece<BF16>::kElems;
+    constexpr int S = 32 / G;            // slots per step
+    constexpr int U = G;                 // steps per 32-slot chunk
+    static_assert(G == 8 && (P == 2 || P == 3), "4 slots per step, 2 or 3 pieces per lane");
+    constexpr int kBlk = 4;                                      // steps per block = one padded row unit
+    static_assert(S * kBlk == kFlowPad && (D == 4 || D == 8), "ring of one or two blocks");
+    constexpr int kStage = 32 * P;                               // float4 per warp stage
+    constexpr int32_t kNone = 0x7fffffff;
+    extern __shared__ __align__(16) float4 slab_ring[];          // [warps][D][P][S][G]
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int e = lane / G, sub = lane % G;
+    const int64_t gw = (int64_t)blockIdx.x * W + warp;
+    const int64_t nw = (int64_t)gridDim.x * W;
+    const uint64_t pol = policy_evict_first();
+    // the slots' sampling signature (a whole-call guard)
+    if (p.ws_sig && *p.ws_sig != p.sig) {
+        if (lane == 0 && p.ws_status) atomicOr(p.ws_status, kWsSignature);
+        for (int64_t r = p.n_rows * gw / nw; r < p.n_rows * (gw + 1) / nw; ++r) slab_fill_row(p, r, __int_as_float(0x7fc00000));
+        return;
+    }
+    // this warp's rows: an equal share of the rows' padded slots + kFlowRowCost per row
+    const int64_t total = ld_stream(p.s_rowptr + p.n_rows, pol) + kFlowRowCost * p.n_rows;
+    const int64_t rb = flow_search(p.s_rowptr, p.n_rows, total / nw * gw + total % nw * gw / nw, lane);
+    const int64_t re = gw + 1 == nw ? p.n_rows
+                                    : flow_search(p.s_rowptr, p.n_rows, total / nw * (gw + 1) + total % nw * (gw + 1) / nw, lane);
+    if (rb >= re) return;
+
+    // the warp's stream: slots [P0, P0 + nsl) of the workspace; overflowing rows (slot end past
+    // cap, a suffix of the rows) are poisoned and not streamed
+    const int64_t P0 = ld_stream(p.s_rowptr + rb, pol);
+    int64_t P1 = ld_stream(p.s_rowptr + re, pol);
+    const bool huge = P1 - P0 >= (int64_t)0x7fffffff;                 // > 2^31 slots: not streamed
+    if (P1 > p.cap) P1 = p.cap & ~(int64_t)(kFlowPad - 1);
+    if (huge) P1 = P0;
+    const int32_t nsl = P1 > P0 ? (int32_t)(P1 - P0) : 0;          // a multiple of kFlowPad
+
+    // ---- row metadata (rare-path state, kept in shared memory so the step loop's registers are
+    // the per-row kernel's): 32 rows per batch, lane i <-> row rb + bo + i; the next batch's raw
+    // slot ends (low 32 bits of s_rowptr[r+1]: the stream spans < 2^31 slots, so differences to
+    // P0 are exact in 32-bit arithmetic) and k_i (s_k) arrive by cp.async one batch ahead.
+    FlowMeta* fm = reinterpret_cast<FlowMeta*>(slab_ring + (size_t)W * D * kStage) + warp;
+    if (lane == 0) {
+        fm->rb = rb;
+        fm->P0 = P0;
+        fm->nrows = (int32_t)(re - rb);
+        fm->bo = 0;
+        fm->bstart = 0;
+        // a row ending past the workspace capacity overflowed (relative to P0; -1: every row)
+        fm->caprel = (int32_t)max(min(p.cap - P0, (int64_t)0x7fffffff), (int64_t)-1);
+        fm->fetch_t = 0;
+    }
+    __syncwarp();
+    auto fetch = [&](int32_t o, int buf) {           // raw metadata of rows rb + o .. + 31
+        const int64_t r = fm->rb + o + lane;
+        if (o + lane < fm->nrows) {
+            cp_async4(&fm->nse[buf][lane], reinterpret_cast<const int32_t*>(p.s_rowptr + r + 1));
+            cp_async4(&fm->nk[buf][lane], p.s_k + r);
+        }
+    };
+    int cur = 0;                                      // lane of the current row in its batch
+    int32_t cur_end = kNone, next_flush = kNone;
+    auto setup = [&](int buf) {                       // the batch at fm->bo from raw buffer buf
+        const int32_t bo = fm->bo, nrows = fm->nrows;
+        const bool in = bo + lane < nrows;
+        const int32_t nse = in ? fm->nse[buf][lane] : 0, nk = in ? fm->nk[buf][lane] : 0;
+        const int32_t rel = (int32_t)((uint32_t)nse - (uint32_t)(uint64_t)fm->P0);
+        const bool over = in && rel > fm->caprel;
+        const int32_t endstep = in && !over ? (int32_t)(rel / S) : 0x3fffffff;
+        int32_t st = __shfl_up_sync(kAll, endstep, 1);
+        if (lane == 0) st = fm->bstart;
+        bool mism = false;
+        float dv = (float)nk;
+        if (in && (p.reuse_s > 0 || p.mean_by_degree)) {       // the caller's rowptr (not prefetched)
+            const int64_t r = fm->rb + bo + lane;
+            const int64_t d = ld_stream(p.rowptr + r + 1, policy_evict_first()) - ld_stream(p.rowptr + r, policy_evict_first());
+            if (p.mean_by_degree) dv = (float)d;
+            if (p.reuse_s > 0 && !over) {
+                const int64_t kr = d < (int64_t)p.reuse_s ? d : (int64_t)p.reuse_s;
+                mism = nk != kr || (int64_t)(endstep - st) * S != ((kr + kFlowPad - 1) & ~(int64_t)(kFlowPad - 1));
+            }
+        }
+        if ((over || mism) && p.ws_status) atomicOr(p.ws_status, (over ? kWsOverflow : 0) | (mism ? kWsSignature : 0));
+        fm->endstep[lane] = endstep;
+        fm->divf[lane] = dv;
+        const unsigned live = __ballot_sync(kAll, in && !over && endstep > st);
+        const unsigned pmask = __ballot_sync(kAll, mism);
+        // rows no step belongs to: empty (0, or NaN if the reuse check failed) and overflowing (NaN)
+        unsigned special = __ballot_sync(kAll, in && (over || endstep == st));
+        const unsigned bad = __ballot_sync(kAll, over || mism);
+        if (lane == 0) {
+            fm->live = live;
+            fm->pmask = pmask;
+        }
+        while (special) {
+            const int i = __ffs(special) - 1;
+            special &= special - 1;
+            slab_fill_row(p, fm->rb + bo + i, ((bad >> i) & 1u) ? __int_as_float(0x7fc00000) : 0.0f);
+        }
+        __syncwarp();
+    };
+    // the next live row (after step t: the batch switch waits for its cp.async metadata)
+    auto next_row = [&](int32_t t) {
+        unsigned live = fm->live;
+        while (live == 0) {
+            const int32_t bo = fm->bo + 32;
+            if (bo >= fm->nrows) { cur_end = next_flush = kNone; return; }
+            // the raw batch was committed with the refill group after step fetch_t; the step
+            // loop's wait_group<D-1> has completed it once D + 1 steps have passed since
+            if (t < fm->fetch_t + D + 1) cp_async_wait<0>();
+            __syncwarp();
+            const int32_t bstart = fm->endstep[31];
+            __syncwarp();
+            if (lane == 0) {
+                fm->bstart = bstart;
+                fm->bo = bo;
+                fm->fetch_t = t;
+            }
+            __syncwarp();
+            setup((bo >> 5) & 1);
+            fetch(bo + 32, ((bo >> 5) + 1) & 1);
+            live = fm->live;
+        }
+        cur = __ffs(live) - 1;
+        if (lane == 0) fm->live = live & (live - 1);
+        cur_end = fm->endstep[cur];
+        next_flush = (cur == 0 ? fm->bstart : fm->endstep[cur - 1]) + U;
+        __syncwarp();
+    };
+    fetch(0, 0);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncwarp();
+    setup(0);
+    fetch(32, 1);                                     // lands with the prologue's copies
+    next_row(kNone - D - 1);
+
+    const uint32_t my_s = smem_u32(slab_ring + (size_t)warp * D * kStage + e * G + sub);
+    const char* bl = reinterpret_cast<const char*>(p.B) + sub * 16;
+    const uint32_t row_bytes = (uint32_t)(p.ldb * (BF16 ? 2 : 4));
+    // padding slots and slots past the stream's end (col -1): zero-filled pieces, no memory read
+    auto copy = [&](uint32_t stage, int32_t col) {
+        const bool ok = col >= 0;
+        const char* src = bl + (uint64_t)(uint32_t)(ok ? col : 0) * row_bytes;
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            const bool on = FULL ? ok : (ok && sub + G * q < p.nv);
+            cp_async16_zfill(stage + q * 32 * 16, src + q * G * 16, on ? 16u : 0u);
+        }
+    };
+    auto load_pair = [&](int32_t j, int32_t& c, float& a) {       // stream slot j (coalesced)
+        c = -1;
+        a = 0.0f;
+        if (j < nsl) {
+            c = ld_stream(p.s_colind + P0 + j, pol);
+            a = p.s_val ? ld_stream(p.s_val + P0 + j, pol) : 1.0f;
+        }
+    };
+    // (col, val) chunks: c0 = the chunk being consumed, c1 = the next; with an 8-step ring the
+    // refills read the next chunk from the first step on, so a third (c2) is in flight
+    int32_t c0, c1, c2 = -1;
+    float a0, a1, a2 = 0.0f;
+    load_pair(lane, c0, a0);
+    load_pair(32 + lane, c1, a1);
+    if (D == 8) load_pair(64 + lane, c2, a2);
+#pragma unroll
+    for (int t = 0; t < D; ++t) {
+        copy(my_s + (uint32_t)t * (kStage * 16), __shfl_sync(kAll, c0, S * t + e));
+        cp_async_commit();
+    }
+    float part[P][E], tot[P][E];
+#pragma unroll
+    for (int q = 0; q < P; ++q)
+#pragma unroll
+        for (int c = 0; c < E; ++c) { part[q][c] = 0.0f; tot[q][c] = 0.0f; }
+    // a stream event after step t: the row's 32-slot chunk partial, and at the row's end a5
+    auto event = [&](int32_t t) {
+#pragma unroll
+        for (int q = 0; q < P; ++q)
+#pragma unroll
+            for (int c = 0; c < E; ++c) { tot[q][c] += part[q][c]; part[q][c] = 0.0f; }
+        if (t + 1 == cur_end) {
+            const int64_t r = fm->rb + fm->bo + cur;
+#pragma unroll
+            for (int o = G; o < 32; o <<= 1)
+#pragma unroll
+                for (int q = 0; q < P; ++q)
+#pragma unroll
+                    for (int c = 0; c < E; ++c) {
+                        const float other = __shfl_xor_sync(kAll, tot[q][c], o);
+                        tot[q][c] = (lane & o) ? other + tot[q][c] : tot[q][c] + other;
+                    }
+            const float dv = fm->divf[cur];
+            if ((fm->pmask >> cur) & 1u) {
+                slab_fill_row(p, r, __int_as_float(0x7fc00000));
+            } else if (e == 0) {
+#pragma unroll
+                for (int q = 0; q < P; ++q) {
+                    const int piece = sub + G * q;
+                    if (FULL || piece < p.nv) slab_store_piece_f<E>(p, r, piece * E, tot[q], dv, pol);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < P; ++q)
+#pragma unroll
+                for (int c = 0; c < E; ++c) tot[q][c] = 0.0f;
+            next_row(t);
+        } else {
+            next_flush += U;
+        }
+    };
+    // The step loop runs BLOCKS of D = 4 steps with static ring stages -- the per-row kernel's
+    // inner loop, which the compiler interleaves across the block.  Rows are padded to multiples
+    // of 16 slots (4 steps), so every row starts and ends, and every 32-slot partial flushes, on
+    // a block boundary: the block body has no event branch (one inside cost 8 accumulator moves
+    // and a reconvergence per step), and the row epilogue exists once in the code (inlined per
+    // step it overflowed the instruction cache: D = 2 / 4 / 8 ran 9.5 / 10.9 / 21.5 ms on Reddit
+    // F=602, profiles/r02_flow_probe.jsonl).
+    const int32_t TS = nsl / S;                                  // a multiple of kBlk
+#pragma unroll 1
+    for (int32_t t = 0; t < TS; t += kBlk) {
+        const int u0 = t & (U - 1);
+        const uint32_t base = my_s + (uint32_t)(t & (D - 1)) * (kStage * 16);
+#pragma unroll
+        for (int d = 0; d < kBlk; ++d) {
+            const int u = u0 + d;
+            const uint32_t stage = base + (uint32_t)d * (kStage * 16);
+            cp_async_wait<D - 1>();                              // step t + d has landed
+            const float av = __shfl_sync(kAll, a0, S * u + e);
+#pragma unroll
+            for (int q = 0; q < P; ++q) {
+                float x[E];
+                SlabPiece<BF16>::widen(lds128(stage + q * 32 * 16), x);
+#pragma unroll
+                for (int c = 0; c < E; ++c) part[q][c] = fmaf(av, x[c], part[q][c]);
+            }
+            const int tn = u + D;                                // the stage takes step t + d + D
+            const int32_t cn = D == 8 ? __shfl_sync(kAll, c1, (S * u + e) & (32 - 1))
+                                      : __shfl_sync(kAll, tn < U ? c0 : c1, (S * tn + e) & (32 - 1));
+            copy(stage, cn);
+            cp_async_commit();
+        }
+        if (u0 + kBlk == U) {                                    // the (col, val) chunk is consumed
+            c0 = c1;
+            a0 = a1;
+            if (D == 8) {
+                c1 = c2;
+                a1 = a2;
+                load_pair(S * (t + kBlk + 2 * U) + lane, c2, a2);
+            } else {
+                load_pair(S * (t + kBlk + U) + lane, c1, a1);
+            }
+        }
+        if (t + kBlk == min(cur_end, next_flush)) event(t + kBlk - 1); // one call site: one epilogue
+    }
+    cp_async_wait<0>();
 }
 
 // ---------------------------------------------------------------- TMA gather4 slab kernel
@@ -852,16 +1226,19 @@ spmm_slab_bwd(const SlabParams p, const float* __restrict__ dC, float* __restric
     int64_t end = ld_stream(p.s_rowptr + r + 1, pol_a) - p.slot_base;
     if (p.direct_s > 0 && end - beg > p.direct_s) end = beg + p.direct_s;
     bool sig_bad = p.ws_sig != nullptr && *p.ws_sig != p.sig;
+    const int64_t deg = ld_stream(p.rowptr + r + 1, pol_a) - ld_stream(p.rowptr + r, pol_a);
+    const int32_t pad = p.pad > 1 ? p.pad : 1;
     if (p.reuse_s > 0 && !sig_bad && end <= p.cap) {
-        const int64_t d = ld_stream(p.rowptr + r + 1, pol_a) - ld_stream(p.rowptr + r, pol_a);
-        sig_bad = end - beg != (d < p.reuse_s ? d : (int64_t)p.reuse_s);
+        const int64_t kr = deg < p.reuse_s ? deg : (int64_t)p.reuse_s;
+        sig_bad = end - beg != (kr + pad - 1) / pad * pad;
     }
     if (slab_row_guard(p, end, sig_bad)) return;      // dB is accumulated into: flagged, not poisoned
+    // slots [beg, end): k_i sampled ones, then (flow layout) padding slots with column -1
     const int32_t k = end > beg ? (int32_t)(end - beg) : 0;
     if (k == 0) return;
-    float div = (float)k;
-    if (p.reduce == kMean && p.mean_by_degree)
-        div = (float)(ld_stream(p.rowptr + r + 1, pol_a) - ld_stream(p.rowptr + r, pol_a));
+    const int64_t ks = deg < (int64_t)p.s ? deg : (int64_t)p.s;
+    float div = (float)ks;
+    if (p.reduce == kMean && p.mean_by_degree) div = (float)deg;
     float x[P][4];
 #pragma unroll
     for (int q = 0; q < P; ++q) {
@@ -886,7 +1263,7 @@ spmm_slab_bwd(const SlabParams p, const float* __restrict__ dC, float* __restric
             const int slot = S * u + e;
             const int32_t cn = __shfl_sync(kAll, cj, slot);
             const float av = __shfl_sync(kAll, aj, slot);
-            if (slot < n_here) {
+            if (slot < n_here && cn >= 0) {
                 float* brow = dB + (int64_t)(uint32_t)cn * ldb;
 #pragma unroll
                 for (int q = 0; q < P; ++q) {
@@ -905,7 +1282,67 @@ spmm_slab_bwd(const SlabParams p, const float* __restrict__ dC, float* __restric
     }
 }
 
+// ---- flow launchers.  Register caps (blocks of 4 warps per SM): 8 (64 registers) for 2 fp32
+// pieces per lane, 6 (80) for 3; bf16 (8 accumulators per piece) 6 and 5.  Each pass runs a
+// persistent grid of SMs x (that kernel's occupancy) CTAs: every warp is resident at once.
+template <int P, bool BF16> struct FlowCap;
+template <> struct FlowCap<2, false> { static constexpr int kMinB = 8; };
+template <> struct FlowCap<3, false> { static constexpr int kMinB = 6; };
+template <> struct FlowCap<2, true> { static constexpr int kMinB = 6; };
+template <> struct FlowCap<3, true> { static constexpr int kMinB = 5; };
+
+template <int P, int D, int W, bool BF16, bool FULL>
+cudaError_t launch_flow_k(const SlabParams& p, cudaStream_t st) {
+    // one block less for the variants whose extra predicates / accumulators would otherwise spill
+    // (an 8-step ring is shared-memory bound at 6 / 4 blocks: its register cap follows)
+    constexpr int kMinB = D == 8 ? (P == 2 ? 6 : 4)
+                                 : FlowCap<P, BF16>::kMinB - ((BF16 || (P == 2 && !FULL)) ? 1 : 0);
+    auto k = spmm_slab_flow<8, P, D, W, kMinB * 4 / W, FULL, BF16>;
+    constexpr size_t smem = (size_t)W * D * 32 * P * 16 + (size_t)W * sizeof(FlowMeta);
+    // grid = SMs x resident CTAs, computed once per device (occupancy queries are not free)
+    static std::atomic<int> grid_cache[8];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return cudaErrorInvalidDevice;
+    int grid = dev < 8 ? grid_cache[dev].load(std::memory_order_relaxed) : 0;
+    if (grid <= 0) {
+        if (smem > 48 * 1024) {
+            cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+        }
+        int sms = 0, nb = 0;
+        cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, 32 * W, smem);
+        if (e != cudaSuccess) return e;
+        grid = sms * (nb > 0 ? nb : 1);
+        if (dev < 8) grid_cache[dev].store(grid, std::memory_order_relaxed);
+    }
+    k<<<(unsigned)grid, 32 * W, smem, st>>>(p);
+    return cudaGetLastError();
+}
+
+template <int P, int D, int W, bool BF16>
+cudaError_t launch_flow_w(const SlabParams& p, cudaStream_t st) {
+    return p.nv == 8 * P ? launch_flow_k<P, D, W, BF16, true>(p, st) : launch_flow_k<P, D, W, BF16, false>(p, st);
+}
+
 }  // namespace
+
+// ring depth tune.stages (4 default = one 4-step block; 8), warps per CTA W = tune.cta_warps (8
+// default; 4); bf16 B: 4-step ring, 4-warp CTAs
+cudaError_t launch_slab_flow(const SlabParams& p, const Tune& t, cudaStream_t st) {
+    if (p.n_rows <= 0) return cudaSuccess;
+    if (p.nv > 24 || p.nv < 1) return cudaErrorInvalidValue;
+    const bool p3 = p.nv > 16;
+    if (p.b_bf16) {
+        if (t.stages == 8) return cudaErrorInvalidValue;
+        return p3 ? launch_flow_w<3, 4, 4, true>(p, st) : launch_flow_w<2, 4, 4, true>(p, st);
+    }
+    if (t.stages == 8) return p3 ? launch_flow_w<3, 8, 4, false>(p, st) : launch_flow_w<2, 8, 4, false>(p, st);
+    // 8-warp CTAs by default (Reddit F=602 6.97 vs 7.16 ms, F=128 1.61 vs 1.65, Proteins 1.093 vs
+    // 1.121 with 4; profiles/r02_flow_probe.jsonl)
+    if (t.cta_warps == 4) return p3 ? launch_flow_w<3, 4, 4, false>(p, st) : launch_flow_w<2, 4, 4, false>(p, st);
+    return p3 ? launch_flow_w<3, 4, 8, false>(p, st) : launch_flow_w<2, 4, 8, false>(p, st);
+}
 
 // Slab kernel selection.  Default: the shared-memory ring, G = tune.width (8 default, or 16)
 // lanes x 16-B pieces per slot (profiles/r02.md: it beats the register-direct and the TMA
@@ -1023,8 +1460,9 @@ size_t slab_scan_temp_bytes(int64_t n) {
 }
 
 cudaError_t launch_slab_count(const int64_t* rowptr, int64_t n, int32_t s, int64_t* s_rowptr, void* temp,
-                              size_t temp_bytes, cudaStream_t st, int* launches, WsHeader* hdr) {
-    cudaError_t err = launch_sample_count_only(rowptr, n, s, s_rowptr, st, hdr);
+                              size_t temp_bytes, cudaStream_t st, int* launches, WsHeader* hdr, int32_t pad,
+                              int32_t* s_k) {
+    cudaError_t err = launch_sample_count_only(rowptr, n, s, s_rowptr, st, hdr, pad, s_k);
     ++*launches;
     if (err != cudaSuccess || n == 0) return err;
     err = cub::DeviceScan::InclusiveSum(temp, temp_bytes, s_rowptr + 1, s_rowptr + 1, n, st);

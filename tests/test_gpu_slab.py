@@ -33,12 +33,16 @@ def graph():
     return synth.random_csr(1301, 2300, seed=41, max_deg=400, special=(577, 1154, 1009, 300, 65, 33, 1))
 
 
-@pytest.fixture(params=["smem8", "smem16", "ldg", "tma", "stream2", "stream8"])
+@pytest.fixture(params=["flow", "flow_mp16", "flow_mp8", "flow_w4", "flow_d8", "smem8", "smem16", "ldg", "tma",
+                        "stream2", "stream8"])
 def lanes(request):
-    """Each slab kernel, forced: the shared-memory ring with 8 / 16 lanes per slot, the
+    """Each slab kernel, forced: the flow kernel (the plan's slicing; slices of 16 pieces, of 8;
+    4-warp CTAs; an 8-step ring), the per-row shared-memory ring with 8 / 16 lanes per slot, the
     register-direct 256-bit kernel (32-B row pitches; else the plan's), the TMA gather4 kernel,
     the row-pipelined stream (2 / 8 rows per warp)."""
-    fam, tune = {"smem8": ("slab_smem", (0, 8)), "smem16": ("slab_smem", (0, 16)), "ldg": ("slab_ldg", ()),
+    fam, tune = {"flow": ("slab_flow", ()), "flow_mp16": ("slab_flow", (0, 16)), "flow_mp8": ("slab_flow", (0, 8)),
+                 "flow_w4": ("slab_flow", (0, 0, 4)), "flow_d8": ("slab_flow", (8,)),
+                 "smem8": ("slab_smem", (0, 8)), "smem16": ("slab_smem", (0, 16)), "ldg": ("slab_ldg", ()),
                  "tma": ("slab_tma", ()), "stream2": ("slab_stream", (0, 0, 0, 512)),
                  "stream8": ("slab_stream", (0, 0, 0, 2048))}[request.param]
     with es.kernel_override(fam, *tune):
@@ -48,6 +52,32 @@ def lanes(request):
 def _unsupported_ok(B):
     """slab_ldg needs a 32-B row pitch: other layouts are ES_ERR_UNSUPPORTED under it."""
     return es._OVERRIDE["kernel"] == es.ES_KERNEL_SLAB_LDG and (B.shape[1] * B.itemsize) % 32 != 0
+
+
+def flow_launches(F, reuse=False, bf16=False, n_cols=2300):
+    """Launches of one flow-path call: count + CUB scan (2) + materialise, then one pass per
+    slice of MP 16-B pieces, a remainder of <= 24 - MP pieces merged into the last slice; MP =
+    tune width 8 / 16 / 24, else whichever of 16 and 24 needs fewer passes (24 while n_cols x
+    384 B <= 96 MB)."""
+    npieces = -(-F * (2 if bf16 else 4) // 16)
+
+    def passes(mp):
+        q, r = divmod(npieces, mp)
+        return q + (1 if r and not (q > 0 and mp + r <= 24) else 0)
+
+    mp = _OVERRIDE_WIDTH()
+    if not mp:
+        mp = 24 if passes(24) < passes(16) and n_cols * 384 <= 96 << 20 else 16
+    return (0 if reuse else 4) + passes(mp)
+
+
+def _OVERRIDE_WIDTH():
+    w = es._OVERRIDE["tune"][1]
+    return w if w in (8, 16, 24) else 0
+
+
+def _is_flow():
+    return es._OVERRIDE["kernel"] in (es.ES_KERNEL_AUTO, es.ES_KERNEL_SLAB, es.ES_KERNEL_SLAB_FLOW)
 
 
 def slab(rowptr, colind, val, B, s, strat, seed, reduce, F, **kw):
@@ -66,8 +96,11 @@ def slab(rowptr, colind, val, B, s, strat, seed, reduce, F, **kw):
     assert es.es_spmm_workspace_status(ws) == es.ES_WS_OK
     # the slab path really ran (it launches the sampling kernels and/or one kernel per slice;
     # a silent fallback to the fused kernel would launch exactly one)
-    assert es.es_launch_count() - n0 >= (F + 63) // 64 + (0 if strat == 1 else 4) and \
-        es.es_launch_count() - n0 > 1 or F <= 64, "slab path not taken"
+    if _is_flow():
+        assert es.es_launch_count() - n0 == flow_launches(F), "flow path not taken"
+    else:
+        assert es.es_launch_count() - n0 >= (F + 63) // 64 + (0 if strat == 1 else 4) and \
+            es.es_launch_count() - n0 > 1 or F <= 64, "slab path not taken"
     return out
 
 
@@ -131,13 +164,19 @@ def test_slab_kernels_same_order_bitwise(graph, F, ld):
     rowptr, colind, val = graph
     B = synth.dense(2300, F, seed=14, ld=ld)
     outs = {}
-    for fam in ("slab_smem", "slab_ldg", "slab_tma", "slab_stream"):
-        with es.kernel_override(fam):
-            outs[fam] = slab(rowptr, colind, val, B, 256, 2, 7, 1, F)
+    for fam, tune in (("slab_smem", ()), ("slab_ldg", ()), ("slab_tma", ()), ("slab_stream", ()),
+                      ("slab_flow", ()), ("slab_flow", (0, 16)), ("slab_flow", (8,))):
+        with es.kernel_override(fam, *tune):
+            outs[(fam,) + tune] = slab(rowptr, colind, val, B, 256, 2, 7, 1, F)
     full = (F // 64) * 64
-    assert np.array_equal(outs["slab_smem"][:, :full], outs["slab_ldg"][:, :full])
-    assert np.array_equal(outs["slab_smem"][:, :full], outs["slab_tma"][:, :full])
-    assert np.array_equal(outs["slab_smem"], outs["slab_stream"])         # same narrow-slice kernels too
+    ref = outs[("slab_smem",)]
+    assert np.array_equal(ref[:, :full], outs[("slab_ldg",)][:, :full])
+    assert np.array_equal(ref[:, :full], outs[("slab_tma",)][:, :full])
+    assert np.array_equal(ref, outs[("slab_stream",)])                    # same narrow-slice kernels too
+    # the flow kernel: 8 lanes per slot for every slice width (no narrow-slice kernel), so it is
+    # the TMA kernel's order on every column, whatever the slicing or CTA size
+    for key in (("slab_flow",), ("slab_flow", 0, 16), ("slab_flow", 8)):
+        assert np.array_equal(outs[key], outs[("slab_tma",)]), key
 
 
 def test_slab_row_blocks_bitwise(graph, lanes):
@@ -198,15 +237,21 @@ def test_slab_launch_count(graph):
     """The launches es_launch_count reports (bench.py's gpu_launches) match the kernels the slab
     path runs: count + CUB scan (2 kernels) + materialise + one per 64-float slice; Bucket reads
     its slots in place (slices only); reuse_sampled runs the slices only."""
+    with es.kernel_override("slab_smem"):
+        _slab_launch_count(graph, ((2, False, 4 + 10), (1, False, 10), (2, True, 10)))
+    # the flow kernel (the plan's): F = 602 is 151 16-B pieces -> 6 passes of 24 + one of 7;
+    # Bucket is materialised too (the padded layout)
     with es.kernel_override("slab"):
-        _slab_launch_count(graph)
+        _slab_launch_count(graph, ((2, False, 4 + 7), (1, False, 4 + 7), (2, True, 7)))
+    with es.kernel_override("slab_flow", 0, 16):                # 8 x 16 + 23 merged
+        _slab_launch_count(graph, ((2, False, 4 + 9), (2, True, 9)))
 
 
-def _slab_launch_count(graph):
+def _slab_launch_count(graph, cases):
     rowptr, colind, val = graph
     B = synth.dense(2300, 602, seed=1, ld=608)
     ws = es.es_spmm_workspace(1301, 2300, len(colind), 602, 608, 256, True, device=DEV)
-    for strat, reuse, want in ((2, False, 4 + 10), (1, False, 10), (2, True, 10)):
+    for strat, reuse, want in cases:
         n0 = es.es_launch_count()
         es.es_spmm_run_ex(t(rowptr), t(colind), t(val), t(B), 256, strat, 0, 1, F=602, workspace=ws,
                           reuse_sampled=reuse)
@@ -239,8 +284,11 @@ def test_understated_nnz_poisons_rows_and_flags_overflow(graph):
     slots do not fit, and ES_WS_OVERFLOW in the workspace status -- never a truncated sum."""
     rowptr, colind, val = graph
     B = synth.dense(2300, 128, seed=2)
-    K = int(np.minimum(np.diff(rowptr), 256).sum())
-    lie = K // 2
+    k = np.minimum(np.diff(rowptr), 256)
+    # the workspace bound includes the flow layout's padding slack (15 slots per row): state an
+    # nnz that leaves the padded slots ~2,000 short
+    kpad = int(((k + 15) // 16 * 16).sum())
+    lie = max(1, kpad - 15 * 1301 - 2000)
     nb = es.es_spmm_workspace_bytes(1301, 2300, lie, 128, 128, 256, True, kernel="slab")
     ws = torch.zeros(nb, dtype=torch.uint8, device=DEV)
     with es.kernel_override("slab"):
@@ -294,3 +342,58 @@ def test_reuse_with_other_sampling_is_detected(graph):
     B2 = t(synth.dense(2300, 301, seed=3, ld=301))
     with pytest.raises(es.EsError, match="INVALID"):
         es.es_spmm_run_ex(rp, ci, v, B2, 96, 2, 13, 1, F=301, workspace=ws, reuse_sampled=True)
+
+
+# ------------------------------------------------------------------ flow kernel specifics
+@pytest.mark.parametrize("case", ["short", "empty_batches", "one_long_row", "all_empty", "few_rows"])
+def test_flow_row_structure(case):
+    """The flow kernel's stream bookkeeping: rows of every length mod 4 (padding), runs of more
+    than 32 empty rows (whole metadata batches with nothing to stream), one row holding most of
+    the slots (the slot-balanced partition puts it alone), a graph with no edges, and fewer rows
+    than warps -- every row against the oracle, bitwise equal to the per-row TMA gather4 kernel
+    (the same per-element order)."""
+    rng = np.random.default_rng(7)
+    n_cols = 3000
+    if case == "short":
+        d = rng.integers(0, 23, 5000)
+    elif case == "empty_batches":
+        d = rng.integers(1, 40, 4000)
+        d[100:190] = 0
+        d[1000:1033] = 0
+        d[3900:] = 0
+    elif case == "one_long_row":
+        d = rng.integers(0, 5, 3000)
+        d[1500] = 2999
+    elif case == "all_empty":
+        d = np.zeros(777, np.int64)
+    else:
+        d = rng.integers(0, 300, 37)
+    rowptr = np.zeros(len(d) + 1, np.int64)
+    np.cumsum(d, out=rowptr[1:])
+    colind = synth.columns(rowptr, n_cols, np.ones(n_cols, np.int64), 11) if rowptr[-1] else np.zeros(0, np.int32)
+    val = (rng.random(len(colind), dtype=np.float32) + 0.5).astype(np.float32)
+    B = synth.dense(n_cols, 602, seed=3, ld=608)
+    for s, strat, reduce in ((256, 2, 1), (7, 1, 0), (3000, 2, 0)):
+        with es.kernel_override("slab_flow"):
+            g = slab(rowptr, colind, val, B, s, strat, 5, reduce, 602)
+        o = oracle.spmm(rowptr, colind, val, B, s, strat, seed=5, reduce=reduce, F=602)
+        ok, err = rel_ok(g, o)
+        assert ok, (case, s, err)
+        with es.kernel_override("slab_tma"):
+            ref = slab(rowptr, colind, val, B, s, strat, 5, reduce, 602)
+        assert np.array_equal(g, ref), case
+
+
+def test_flow_bf16_parity(graph):
+    """bf16 storage of B (NEXT-4) on the flow kernel: slices of <= 16 pieces (128 elements)."""
+    rowptr, colind, val = graph
+    Bf = synth.dense(2300, 602, seed=5, ld=608)
+    Bb = torch.from_numpy(Bf).to(DEV).to(torch.bfloat16)
+    Bw = Bb.float().cpu().numpy()                       # the exactly widened values
+    ws = es.es_spmm_workspace(1301, 2300, len(colind), 602, 608, 256, True, device=DEV, kernel="slab")
+    n0 = es.es_launch_count()
+    g = es.es_spmm_run_ex(t(rowptr), t(colind), t(val), Bb, 256, 2, 3, 1, F=602, workspace=ws, kernel="slab")
+    torch.cuda.synchronize()
+    assert es.es_launch_count() - n0 == flow_launches(602, bf16=True)
+    o = oracle.spmm(rowptr, colind, val, Bw, 256, 2, seed=3, reduce=1, F=602)
+    assert rel_ok(g.cpu().numpy(), o)[0]

@@ -211,7 +211,8 @@ def test_options_validation(lib):
 def test_workspace_bytes_plan(lib):
     """es_spmm_workspace_bytes (host only): the slab path is asked for when a 64-float slab of B
     fits L2, F >= 128, ldb % 4 == 0 and rows sample enough slots on average; the bound covers
-    min(nnz, n*s) slots (+ values)."""
+    min(nnz, n*s) slots plus the flow layout's padding (<= 15 slots per row) (+ values) and each
+    row's unpadded k_i."""
     reddit = es.es_spmm_workspace_bytes(232965, 232965, 114615945, 602, 608, 256)
     assert reddit >= 8 * 232965 * 256 + 8 * 232966            # n*s < nnz here: n*s slots
     assert es.es_spmm_workspace_bytes(232965, 232965, 114615945, 602, 608, 256, has_val=False) < reddit
@@ -223,6 +224,7 @@ def test_workspace_bytes_plan(lib):
     assert es.es_spmm_workspace_bytes(232965, 232965, 114615945, 602, 608, 64) == 0     # s < 128
     assert es.es_spmm_workspace_bytes(232965, 232965, 114615945, 602, 602, 256) == 0    # 8-B row pitch
     small = es.es_spmm_workspace_bytes(232965, 232965, 1000, 602, 608, 256, kernel="slab")
-    assert 8 * 1000 <= small - 8 * 232966 < 8 * 1000 + 4096                             # nnz < n*s
+    n = 232965
+    assert 8 * (1000 + 15 * n) + 4 * n <= small - 8 * (n + 1) < 8 * (1000 + 15 * n) + 4 * n + 8192  # nnz < n*s
     assert es.es_spmm_workspace_bytes(10, 10, 10, 602, 600, 4) == 0                     # ldb < F
     assert es.es_spmm_workspace_bytes(100, 100, 1000, 602, 608, 256, kernel="slab") > 0
