@@ -209,9 +209,10 @@ def test_slab_ldc_padding_untouched(graph, lanes):
 def test_auto_plan_choice():
     # Reddit-shaped F=602: B (566 MB) > L2, a 64-float slab (60 MB) fits -> workspace wanted
     assert es.es_spmm_workspace_bytes(232965, 232965, 114615945, 602, 608, 256) > 0
-    # long rows with B L2-resident (Proteins-shaped) -> wanted; short rows (Arxiv-shaped), s < 128,
-    # or a B too tall for any L2-resident slab (10M rows) -> none
-    assert es.es_spmm_workspace_bytes(232965, 232965, 114615945, 602, 608, 64) == 0
+    # long rows with B L2-resident (Proteins-shaped) -> wanted; short rows (Arxiv-shaped), s < 32 for
+    # F > 128, or a B too tall for any L2-resident slab (10M rows) -> none
+    assert es.es_spmm_workspace_bytes(232965, 232965, 114615945, 602, 608, 64) > 0     # flow beats fused
+    assert es.es_spmm_workspace_bytes(232965, 232965, 114615945, 602, 608, 16) == 0
     assert es.es_spmm_workspace_bytes(132534, 132534, 79_100_000, 128, 128, 256) > 0
     assert es.es_spmm_workspace_bytes(169343, 169343, 2_330_000, 128, 128, 64) == 0
     assert es.es_spmm_workspace_bytes(10_000_000, 10_000_000, 10**9, 256, 256, 128) == 0

@@ -221,7 +221,8 @@ def test_workspace_bytes_plan(lib):
     assert es.es_spmm_workspace_bytes(169343, 169343, 2_330_000, 128, 128, 64) == 0     # short rows
     assert es.es_spmm_workspace_bytes(10_000_000, 10_000_000, 10**9, 256, 256, 128) == 0  # slab > L2
     assert es.es_spmm_workspace_bytes(232965, 232965, 114615945, 64, 64, 256) == 0      # one slice
-    assert es.es_spmm_workspace_bytes(232965, 232965, 114615945, 602, 608, 64) == 0     # s < 128
+    assert es.es_spmm_workspace_bytes(232965, 232965, 114615945, 602, 608, 64) > 0      # s >= 32, F > 128
+    assert es.es_spmm_workspace_bytes(232965, 232965, 114615945, 602, 608, 16) == 0     # s < 32
     assert es.es_spmm_workspace_bytes(232965, 232965, 114615945, 602, 602, 256) == 0    # 8-B row pitch
     small = es.es_spmm_workspace_bytes(232965, 232965, 1000, 602, 608, 256, kernel="slab")
     n = 232965
