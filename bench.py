@@ -332,9 +332,9 @@ def main():
             es.es_spmm_run_ex(rp_d, ci_d, va_d, B_d, a.s, strat_id, a.seed, red_id, F=F, C=C_d,
                               row_begin=r0, row_end=r1, n_rows=n, nnz_base=e0, workspace=ws, nnz=e1 - e0,
                               kernel=kern, reuse_sampled=reuse, stream=st)
-        else:
-            es.es_spmm_run_rows(n, rp_d, e0, ci_d, va_d, B_d, a.s, strat_id, a.seed, red_id, r0, r1,
-                                F=F, C=C_d, stream=st)
+        else:                                  # the fused path, the rows' nnz stated (plan input)
+            es.es_spmm_run_ex(rp_d, ci_d, va_d, B_d, a.s, strat_id, a.seed, red_id, F=F, C=C_d,
+                              row_begin=r0, row_end=r1, n_rows=n, nnz_base=e0, nnz=e1 - e0, stream=st)
 
     lc0 = es.es_launch_count()
     for _ in range(a.warmup):
@@ -427,7 +427,8 @@ def main():
         resident = n * ldb * b_elem <= L2_RESIDENT_BYTES
         t_launch = avg_step
         n_launch = 1
-        kname = "es::spmm_cpasync<bf16>" if a.bf16 else es.es_spmm_plan(F, ldb, C_d.stride(0), B_d, C_d)
+        kname = "es::spmm_cpasync<bf16>" if a.bf16 else es.es_spmm_plan(F, ldb, C_d.stride(0), B_d, C_d, s=a.s,
+                                                                        n_rows=r1 - r0, nnz=e1 - e0)
         what = "one fused launch per step (sampling inside the kernel)"
     else:
         # slab path: the dominant kernel is the slab pass (one launch per 256-B feature slice,

@@ -150,8 +150,10 @@ enum {
     ES_KERNEL_SLAB_TMA = 9,     /* feature-sliced path, TMA tile::gather4 into a shared-memory ring */
     ES_KERNEL_ROWSTREAM = 10,   /* short rows: R rows per warp as one flat slot stream (F <= 128)   */
     ES_KERNEL_SLAB_STREAM = 11, /* feature-sliced path, R rows per warp as one padded slot stream   */
-    ES_KERNEL_SLAB_FLOW = 12    /* feature-sliced path, persistent warps streaming slot-balanced
+    ES_KERNEL_SLAB_FLOW = 12,   /* feature-sliced path, persistent warps streaming slot-balanced
                                    row ranges across row boundaries (the plan's slab kernel)      */
+    ES_KERNEL_GROUPED = 13      /* short rows, F <= 128: 32-row batches sorted by k_i, a half-warp
+                                   per row with register-direct gathers                           */
 };
 
 /* Status word of a slab workspace (written by the device; reading it synchronises `stream`).
@@ -336,6 +338,11 @@ es_status_t es_partition_rows(const int64_t* rowptr_host, int64_t n_rows, int32_
  * writes a short NUL-terminated name into buf (e.g. "es_spmm_warp_v4x5"). */
 es_status_t es_spmm_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C,
                          char* buf, int32_t buf_len);
+/* Same for a call with sampling cap s over n_rows rows holding nnz stored entries (the fused
+ * plan depends on min(s, nnz / n_rows): short rows take the degree-sorted half-warp kernel);
+ * nnz = 0: unknown (min(s, .) = s, as es_spmm_run_rows, which states no nnz). */
+es_status_t es_spmm_plan_ex(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C, int32_t s,
+                            int64_t n_rows, int64_t nnz, char* buf, int32_t buf_len);
 
 /* Number of kernels this library has launched in this process (atomic counter). */
 int64_t es_launch_count(void);

@@ -20,11 +20,12 @@ ES_MEAN_BY_SAMPLED, ES_MEAN_BY_DEGREE = 0, 1
 ES_DTYPE_F32, ES_DTYPE_BF16 = 0, 1
 (ES_KERNEL_AUTO, ES_KERNEL_FUSED, ES_KERNEL_WARP, ES_KERNEL_TMA, ES_KERNEL_CPASYNC, ES_KERNEL_CPASYNC_HW,
  ES_KERNEL_SLAB, ES_KERNEL_SLAB_SMEM, ES_KERNEL_SLAB_LDG, ES_KERNEL_SLAB_TMA, ES_KERNEL_ROWSTREAM,
- ES_KERNEL_SLAB_STREAM, ES_KERNEL_SLAB_FLOW) = range(13)
+ ES_KERNEL_SLAB_STREAM, ES_KERNEL_SLAB_FLOW, ES_KERNEL_GROUPED) = range(14)
 KERNELS = {"auto": ES_KERNEL_AUTO, "fused": ES_KERNEL_FUSED, "warp": ES_KERNEL_WARP, "tma": ES_KERNEL_TMA,
            "cpasync": ES_KERNEL_CPASYNC, "halfwarp": ES_KERNEL_CPASYNC_HW, "slab": ES_KERNEL_SLAB,
            "slab_smem": ES_KERNEL_SLAB_SMEM, "slab_ldg": ES_KERNEL_SLAB_LDG, "slab_tma": ES_KERNEL_SLAB_TMA,
-           "rowstream": ES_KERNEL_ROWSTREAM, "slab_stream": ES_KERNEL_SLAB_STREAM, "slab_flow": ES_KERNEL_SLAB_FLOW}
+           "rowstream": ES_KERNEL_ROWSTREAM, "slab_stream": ES_KERNEL_SLAB_STREAM, "slab_flow": ES_KERNEL_SLAB_FLOW,
+           "grouped": ES_KERNEL_GROUPED}
 ES_WS_OK, ES_WS_OVERFLOW, ES_WS_SIGNATURE_MISMATCH = 0, 1, 2
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -32,7 +33,7 @@ LIB_PATH = os.path.join(_HERE, "libesspmm.so")
 EXPORTS = ("es_spmm_sample", "es_spmm_run", "es_spmm_run_rows", "es_spmm_backward",
            "es_spmm_run_ex", "es_spmm_sample_ex", "es_spmm_backward_ex", "es_spmm_host_workspace_bytes",
            "es_ipc_handle_bytes", "es_ipc_alloc", "es_ipc_free", "es_ipc_export", "es_ipc_import", "es_ipc_close",
-           "es_spmm_run_host", "es_partition_rows", "es_spmm_plan", "es_launch_count", "es_spmm_workspace_bytes",
+           "es_spmm_run_host", "es_partition_rows", "es_spmm_plan", "es_spmm_plan_ex", "es_launch_count", "es_spmm_workspace_bytes",
            "es_spmm_workspace_bytes_ex", "es_spmm_workspace_status", "es_status_string",
            "es_host_pipeline_create", "es_host_pipeline_destroy", "es_spmm_run_host_ex")
 
@@ -171,6 +172,8 @@ def load_library(path: str = LIB_PATH):
     lib.es_partition_rows.argtypes = [vp, i64, i32, i64, i32, vp]
     lib.es_spmm_plan.restype = st
     lib.es_spmm_plan.argtypes = [i64, i64, i64, vp, vp, ctypes.c_char_p, i32]
+    lib.es_spmm_plan_ex.restype = st
+    lib.es_spmm_plan_ex.argtypes = [i64, i64, i64, vp, vp, i32, i64, i64, ctypes.c_char_p, i32]
     _lib = lib
     return lib
 
@@ -223,9 +226,16 @@ def es_launch_count() -> int:
     return int(load_library().es_launch_count())
 
 
-def es_spmm_plan(F: int, ldb: int, ldc: int, B=None, C=None) -> str:
+def es_spmm_plan(F: int, ldb: int, ldc: int, B=None, C=None, s: int | None = None, n_rows: int = 0,
+                 nnz: int = 0) -> str:
+    """The fused kernel the library would launch (es_spmm_plan, or es_spmm_plan_ex with s and the
+    rows' nnz: short rows take the degree-sorted half-warp kernel)."""
     buf = ctypes.create_string_buffer(128)
-    _check(load_library().es_spmm_plan(F, ldb, ldc, _ptr(B), _ptr(C), buf, 128), "es_spmm_plan")
+    if s is None:
+        _check(load_library().es_spmm_plan(F, ldb, ldc, _ptr(B), _ptr(C), buf, 128), "es_spmm_plan")
+    else:
+        _check(load_library().es_spmm_plan_ex(F, ldb, ldc, _ptr(B), _ptr(C), s, n_rows, nnz, buf, 128),
+               "es_spmm_plan_ex")
     return buf.value.decode()
 
 

@@ -74,7 +74,7 @@ es_status_t read_opts(const es_spmm_options_t* o, Opts* out) {
         out->nnz = o->nnz;
     }
     if (ES_COVERS(o, tune)) {
-        if (o->kernel < ES_KERNEL_AUTO || o->kernel > ES_KERNEL_SLAB_FLOW) return ES_ERR_INVALID_VALUE;
+        if (o->kernel < ES_KERNEL_AUTO || o->kernel > ES_KERNEL_GROUPED) return ES_ERR_INVALID_VALUE;
         out->tune.kernel = o->kernel;
         out->tune.stages = o->tune[0];
         out->tune.width = o->tune[1];
@@ -229,7 +229,8 @@ es_status_t run_rows_impl(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
     const bool slab_layout_ok = o.workspace && bu % 16 == 0 && (ldb * esz) % 16 == 0 && slab_feasible(n_cols, F) &&
                                 tn.kernel != ES_KERNEL_FUSED && tn.kernel != ES_KERNEL_WARP &&
                                 tn.kernel != ES_KERNEL_TMA && tn.kernel != ES_KERNEL_CPASYNC &&
-                                tn.kernel != ES_KERNEL_CPASYNC_HW && tn.kernel != ES_KERNEL_ROWSTREAM;
+                                tn.kernel != ES_KERNEL_CPASYNC_HW && tn.kernel != ES_KERNEL_ROWSTREAM &&
+                                tn.kernel != ES_KERNEL_GROUPED;
     if (force_slab && !slab_layout_ok) return ES_ERR_UNSUPPORTED;
     if (slab_layout_ok) {
         // any C layout: 16-B vector stores where C's rows allow them, scalar stores otherwise
@@ -416,9 +417,19 @@ es_status_t es_spmm_workspace_status(void* workspace, int64_t workspace_bytes, i
 
 es_status_t es_spmm_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C,
                          char* buf, int32_t buf_len) {
-    if (F < 1 || ldb < F || ldc < F || !buf || buf_len < 1) return ES_ERR_INVALID_VALUE;
-    const es::Plan pl = es::make_plan(F, ldb, ldc, B, C);
-    if (pl.rowstream)
+    return es_spmm_plan_ex(F, ldb, ldc, B, C, INT32_MAX, 0, 0, buf, buf_len);
+}
+
+es_status_t es_spmm_plan_ex(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C, int32_t s,
+                            int64_t n_rows, int64_t nnz, char* buf, int32_t buf_len) {
+    if (F < 1 || ldb < F || ldc < F || !buf || buf_len < 1 || s < 1 || n_rows < 0 || nnz < 0)
+        return ES_ERR_INVALID_VALUE;
+    const int64_t k_est = (nnz > 0 && n_rows > 0) ? std::min<int64_t>(s, nnz / n_rows) : s;
+    const es::Plan pl = es::make_plan(F, ldb, ldc, B, C, s, es::Tune{}, k_est);
+    if (pl.grouped)
+        snprintf(buf, (size_t)buf_len, "es::spmm_grouped<slots4>(32-row degree-sorted batches)%s",
+                 pl.c_vec ? "" : " (scalar C)");
+    else if (pl.rowstream)
         snprintf(buf, (size_t)buf_len, "es::spmm_rowstream<stages%d,rows%d>%s", pl.stages, pl.rows_per_warp,
                  pl.c_vec ? "" : " (scalar C)");
     else if (pl.tma)

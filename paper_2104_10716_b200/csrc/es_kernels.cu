@@ -40,6 +40,10 @@ constexpr unsigned kFull = 0xffffffffu;
 // the plan would take the row stream when rows sample at most this many slots on average; 0:
 // never -- measured slower than the two-slot ring at every Arxiv-shaped s (profiles/r02.md)
 constexpr int64_t kRowStreamMaxK = 0;
+// the degree-sorted half-warp kernel (spmm_grouped): 4-warp CTAs; the plan takes it for F <= 128
+// when rows sample at most this many slots on average (profiles/r02_grouped_probe.jsonl)
+constexpr int kGroupedWarps = 4;
+constexpr int64_t kGroupedMaxK = 0;     // never by default: measured no faster than the two-slot ring (profiles/r02_grouped_probe.jsonl)
 
 template <int VEC>
 __device__ __forceinline__ void store_out(float* Crow, int64_t vidx, int64_t F, const float* r,
@@ -655,6 +659,147 @@ spmm_cpasync_hw(const SpmmParams p) {
     }
 }
 
+// ------------------------------------------------------------------ short rows: degree-sorted half-warps
+// SURVEY 8(a)'s row-to-warp mapping by degree bucket (§4.5.1 L1073-1081 thread
+// management, §4.5.3 L1100-1105 load balancing), for graphs whose rows sample few slots (Arxiv:
+// mean k 13.7, where a warp per row spends most of its instructions on per-row work).  A warp
+// takes 32 consecutive rows; lane i reads row i's (beg, d) and k_i = min(d_i, s), and the warp
+// sorts the 32 rows by k_i, descending (bitonic network over shuffles; ties by row).  Then 16
+// rounds: in round j the two 16-lane halves take the sorted rows 2j and 2j + 1 -- rows of adjacent
+// k, so the halves' slot loops have nearly equal trip counts (an unsorted pair runs as long as its
+// longer row) -- and each half streams its row's slots with register-direct 16-B gathers, U slots
+// in flight per lane, no shared memory and no cross-lane reduction: lane l of a half owns pieces
+// l and l + 16 of the row (F <= 128).  Positions (Eq. 2 / R6) are stepped 16 slots at a time
+// (pos + 16 P' mod d), the row's (col, val) staged 16 slots per chunk in the half's lanes, two
+// chunks ahead.  Per element: slot order with 32-slot-chunk partials -- spmm_warp's order, bitwise.
+template <int U, int MINB>
+__global__ void __launch_bounds__(32 * kGroupedWarps, MINB)
+spmm_grouped(const SpmmParams p) {
+    constexpr int H = 16;                                         // lanes per row
+    static_assert(H % U == 0, "slots in flight must divide the chunk");
+    const int lane = threadIdx.x & 31;
+    const int h = lane >> 4, l = lane & 15;
+    const int64_t r0 = ((int64_t)blockIdx.x * kGroupedWarps + (threadIdx.x >> 5)) * 32;
+    if (r0 >= p.n_rows) return;
+    const uint64_t pol_a = policy_evict_first(), pol_b = policy_evict_last();
+    const int NV = (int)((p.F + 3) / 4);                          // 16-B pieces (<= 32)
+    const bool act0 = l < NV, act1 = l + 16 < NV;
+    // lane i: row r0 + i
+    int64_t beg = 0, deg = 0;
+    int32_t k = -1;                                               // -1: no row
+    if (r0 + lane < p.n_rows) {
+        const int64_t a = ld_stream(p.rowptr + r0 + lane, pol_a);
+        const int64_t b = ld_stream(p.rowptr + r0 + lane + 1, pol_a);
+        beg = a - p.nnz_base;
+        deg = b - a;
+        k = deg < (int64_t)p.s ? (int32_t)deg : p.s;
+    }
+    // bitonic sort of (k, lane), descending by k then ascending by lane (a strict order, so every
+    // pair of lanes agrees on its exchange)
+    int32_t sk = k, si = lane;
+#pragma unroll
+    for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            const int32_t ok = __shfl_xor_sync(kFull, sk, stride), oi = __shfl_xor_sync(kFull, si, stride);
+            const bool other_first = ok > sk || (ok == sk && oi < si);
+            const bool desc = (lane & size) == 0 || size == 32;
+            const bool lower = (lane & stride) == 0;
+            if ((desc == lower) ? other_first : !other_first) { sk = ok; si = oi; }
+        }
+    }
+    const float* bl = p.B + l * 4;
+    for (int round = 0; round < 16; ++round) {
+        const int32_t kmax = __shfl_sync(kFull, sk, 2 * round);  // the round's longer row (sorted)
+        if (kmax < 0) break;                                      // no rows left (warp-uniform)
+        const int32_t kk = __shfl_sync(kFull, sk, 2 * round + h); // this half's row (-1: none)
+        const int ri = __shfl_sync(kFull, si, 2 * round + h);
+        const int64_t rb = __shfl_sync(kFull, beg, ri), rd = __shfl_sync(kFull, deg, ri);
+        const int64_t r = r0 + ri;
+        RowSampler rs;
+        rs.init(rb, rb + (kk >= 0 ? rd : 0), p.s, p.strategy, p.seed, p.row_base + r, p.prime);
+        // slot j = 16m + l of this lane: its CSR position, stepped by 16 slots
+        const bool step_ok = p.strategy == kBucket || (rs.narrow && rs.d < ((int64_t)1 << 31));
+        const uint32_t d32 = (uint32_t)rs.d;
+        const uint32_t delta = p.strategy == kBucket ? 16u : (rs.d > 0 ? (uint32_t)((16ull * rs.prime) % (uint64_t)rs.d) : 0u);
+        uint32_t pos = (l < kk) ? (uint32_t)rs.pos(l) : 0u;
+        auto load_chunk = [&](int32_t m, int32_t& c, float& a) {     // slot 16m + l
+            const int32_t j = 16 * m + l;
+            c = 0;
+            a = 0.0f;
+            if (j < kk) {
+                const int64_t pj = step_ok ? (int64_t)pos : rs.pos(j);
+                c = ld_stream(p.colind + rs.beg + pj, pol_a);
+                a = p.val ? ld_stream(p.val + rs.beg + pj, pol_a) : 1.0f;
+            }
+            if (step_ok) {                                        // pos of slot j + 16
+                pos += delta;
+                if (p.strategy != kBucket && pos >= d32) pos -= d32;
+            }
+        };
+        int32_t c0, c1, c2 = 0;
+        float a0, a1, a2 = 0.0f;
+        load_chunk(0, c0, a0);
+        load_chunk(1, c1, a1);
+        if (kmax > 32) load_chunk(2, c2, a2);
+        float4 v[U][2];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u][0] = v[u][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        auto issue = [&](int u, int32_t j) {                      // slot j's gathers into v[u]
+            const int32_t cj = __shfl_sync(kFull, (j >> 4) == 0 ? c0 : c1, (lane & 16) | (j & 15));
+            if (j < kk) {
+                const float* src = bl + (int64_t)cj * p.ldb;
+                if (act0) { const Vec<4> x = ld_gather<4>(src, pol_b); v[u][0] = make_float4(x.v[0], x.v[1], x.v[2], x.v[3]); }
+                if (act1) { const Vec<4> x = ld_gather<4>(src + 64, pol_b); v[u][1] = make_float4(x.v[0], x.v[1], x.v[2], x.v[3]); }
+            }
+        };
+        float part[8], tot[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) { part[q] = 0.0f; tot[q] = 0.0f; }
+#pragma unroll
+        for (int u = 0; u < U; ++u) issue(u, u);
+        for (int32_t j0 = 0; j0 < kmax; j0 += U) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int32_t j = j0 + u;                          // slots j0 .. j0+U-1: one chunk
+                const float av = __shfl_sync(kFull, a0, (lane & 16) | (j & 15));
+                if (j < kk) {
+                    part[0] = fmaf(av, v[u][0].x, part[0]); part[1] = fmaf(av, v[u][0].y, part[1]);
+                    part[2] = fmaf(av, v[u][0].z, part[2]); part[3] = fmaf(av, v[u][0].w, part[3]);
+                    part[4] = fmaf(av, v[u][1].x, part[4]); part[5] = fmaf(av, v[u][1].y, part[5]);
+                    part[6] = fmaf(av, v[u][1].z, part[6]); part[7] = fmaf(av, v[u][1].w, part[7]);
+                }
+                // slot j + U: in this chunk or the next (c1); the chunk rotates below
+                const int32_t jn = j + U;
+                const int32_t cj = __shfl_sync(kFull, ((jn >> 4) == (j >> 4)) ? c0 : c1, (lane & 16) | (jn & 15));
+                if (jn < kk) {
+                    const float* src = bl + (int64_t)cj * p.ldb;
+                    if (act0) { const Vec<4> x = ld_gather<4>(src, pol_b); v[u][0] = make_float4(x.v[0], x.v[1], x.v[2], x.v[3]); }
+                    if (act1) { const Vec<4> x = ld_gather<4>(src + 64, pol_b); v[u][1] = make_float4(x.v[0], x.v[1], x.v[2], x.v[3]); }
+                }
+            }
+            if (((j0 + U) & 15) == 0) {                             // chunk consumed
+                if (((j0 + U) & 31) == 0) {                        // a 32-slot partial
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) { tot[q] += part[q]; part[q] = 0.0f; }
+                }
+                c0 = c1; a0 = a1;
+                c1 = c2; a1 = a2;
+                if (j0 + U + 32 < kmax) load_chunk((j0 + U + 32) >> 4, c2, a2);
+            }
+        }
+        if (kk < 0) continue;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) tot[q] += part[q];
+        const int64_t div = mean_div(p, rs.d, kk);
+        float res[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) res[q] = finish(tot[q], p.reduce, div);
+        if (act0) store_c<4>(p, r, l, res, pol_a);
+        if (act1) store_c<4>(p, r, l + 16, res + 4, pol_a);
+    }
+}
+
 // ------------------------------------------------------------------ per-warp slot stream
 // A warp owns R <= 32 consecutive rows; their sampled slots form one flat stream (row by
 // row, slot order).  Row i's metadata (a1) lives in lane i; (col, val) of 32 consecutive
@@ -1091,6 +1236,21 @@ cudaError_t launch_rowstream_k(const SpmmParams& p, cudaStream_t st) {
 }
 
 // rows per warp tune.width (8, 16 or 32; default 16), ring depth tune.stages (4 default; 8)
+template <int U, int MINB>
+cudaError_t launch_grouped_k(const SpmmParams& p, cudaStream_t st) {
+    const int64_t warps = (p.n_rows + 31) / 32;
+    const int64_t blocks = (warps + kGroupedWarps - 1) / kGroupedWarps;
+    spmm_grouped<U, MINB><<<(unsigned)blocks, 32 * kGroupedWarps, 0, st>>>(p);
+    return cudaGetLastError();
+}
+
+// slots in flight per lane U = tune.stages (4 default; 2, 8)
+cudaError_t launch_grouped(const SpmmParams& p, const Tune& t, cudaStream_t st) {
+    if (t.stages == 2) return launch_grouped_k<2, 8>(p, st);
+    if (t.stages == 8) return launch_grouped_k<8, 4>(p, st);
+    return launch_grouped_k<4, 6>(p, st);
+}
+
 cudaError_t launch_rowstream(const SpmmParams& p, const Tune& t, cudaStream_t st) {
     const int R = t.width > 0 ? t.width : 16;
     if (t.stages == 8) {
@@ -1261,6 +1421,13 @@ Plan make_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C
         pl.rows_per_warp = t.width > 0 ? t.width : 16;
         return pl;
     }
+    // short rows (F <= 128): the degree-sorted half-warp kernel when rows sample few slots
+    if (rs_ok && (ov == ES_KERNEL_GROUPED ||
+                  ((ov == ES_KERNEL_AUTO || ov == ES_KERNEL_FUSED) && k_est > 0 && k_est <= kGroupedMaxK))) {
+        pl.grouped = true;
+        pl.cpasync = pl.tma = pl.halfwarp = pl.subwarp = pl.rowstream = false;
+        return pl;
+    }
     if (pl.tma) {
         pl.nch = (int)((nv4 + 31) / 32);
         pl.subwarp = false;
@@ -1277,6 +1444,7 @@ Plan make_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C
 cudaError_t launch_spmm(SpmmParams p, const Plan& plan, const Tune& t, cudaStream_t st) {
     if (p.n_rows <= 0) return cudaSuccess;
     p.c_vec = plan.c_vec ? 1 : 0;
+    if (plan.grouped) return launch_grouped(p, t, st);
     if (plan.rowstream) return launch_rowstream(p, t, st);
     if (plan.tma) return dispatch_tma(p, plan, st);
     if (plan.cpasync) return launch_cpasync(p, plan, t, st);

@@ -3,6 +3,7 @@
 es_spmm_options_t.kernel / tune[] (paper_2104_10716_b200.kernel_override).
 
   python scripts/slab_probe.py [config] [F] [s] [strategy]      # default reddit 602 256 fastrand
+  (a fused family -- halfwarp, grouped, ... -- may be listed too: no workspace, no pass timing)
   SLAB_VARIANTS="slab_ldg:4:0:4:0,slab_smem:4:8:4:0"   kernel:stages:width:cta_warps:variant
   UNIFORM_COLS=1: the same degree sequence with uniformly random columns (no popularity skew)
   CONST_DEG=d: nnz/d rows of degree d each, uniform columns (isolates per-row costs)
@@ -85,11 +86,12 @@ def main():
         kw = dict(F=F, C=C2, workspace=ws, kernel=kern, tune=tune[:4])
         try:
             ms, mn = timed(lambda: es.es_spmm_run_ex(rp, ci, va, Bd, s, strat, 0, 1, **kw))
-            pms, pmn = timed(lambda: es.es_spmm_run_ex(rp, ci, va, Bd, s, strat, 0, 1, reuse_sampled=True, **kw))
+            pms, pmn = (timed(lambda: es.es_spmm_run_ex(rp, ci, va, Bd, s, strat, 0, 1, reuse_sampled=True, **kw))
+                        if ws is not None else (ms, mn))      # fused kernels: no separate passes
         except es.EsError as exc:
             print(json.dumps({"variant": v, "error": str(exc)}), flush=True)
             continue
-        st = es.es_spmm_workspace_status(ws)
+        st = es.es_spmm_workspace_status(ws) if ws is not None else None
         d = (C2[:, :F] - C[:, :F]).abs().max().item()
         rel = ((C2[:, :F] - C[:, :F]).abs() / C[:, :F].abs().clamp_min(1e-6)).max().item()
         same = None

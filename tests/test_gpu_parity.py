@@ -133,7 +133,7 @@ KERNEL_PARAMS = {                       # name -> (kernel family, tune: stages, 
     "auto": ("auto", ()), "warp": ("warp", ()), "tma": ("tma", ()), "cpasync": ("cpasync", ()),
     "halfwarp": ("halfwarp", ()), "slab": ("slab", ()), "slab16": ("slab_smem", (0, 16)),
     "slab_ldg": ("slab_ldg", ()), "slab_tma": ("slab_tma", ()), "slab_stream": ("slab_stream", (0, 0, 0, 1024)),
-    "rowstream": ("rowstream", ()),
+    "rowstream": ("rowstream", ()), "grouped": ("grouped", ()), "grouped8": ("grouped", (8,)),
 }
 
 
@@ -184,6 +184,23 @@ def test_ones_give_exact_counts(ragged, kernel):
                 assert np.array_equal(g, np.repeat(np.minimum(d, s)[:, None], F, 1).astype(np.float32))
                 gm = run_gpu(rowptr, colind, None, B, s, strat, seed=3, reduce=ES_REDUCE_MEAN, F=F)
                 assert np.array_equal(gm, np.repeat((d > 0)[:, None], F, 1).astype(np.float32))
+
+
+@pytest.mark.parametrize("F", [65, 100, 128])
+@pytest.mark.parametrize("U", [2, 4, 8])
+def test_grouped_bitwise_warp(ragged, F, U):
+    """The degree-sorted half-warp kernel (spmm_grouped) sums each row in slot order with
+    32-slot-chunk partials, exactly as the LDG warp-per-row kernel does: bitwise, whatever the
+    sort put in each half-warp or how many slots are in flight."""
+    rowptr, colind, val = ragged
+    B = synth.dense(3001, F, seed=F, ld=(F + 3) // 4 * 4)
+    for s, strat, red in ((16, ES_FASTRAND, ES_REDUCE_MEAN), (64, ES_BUCKET, ES_REDUCE_SUM),
+                          (700, ES_FASTRAND, ES_REDUCE_MEAN), (1, ES_FASTRAND, ES_REDUCE_SUM)):
+        with es.kernel_override("warp"):
+            a = run_gpu(rowptr, colind, val, B, s, strat, 5, red, F=F)
+        with es.kernel_override("grouped", U):
+            b = run_gpu(rowptr, colind, val, B, s, strat, 5, red, F=F)
+        assert np.array_equal(a, b), (F, s, strat)
 
 
 @pytest.mark.parametrize("F", [65, 100, 128])
