@@ -555,7 +555,7 @@ spmm_slab_flow(const __grid_constant__ SlabParams p) {
     constexpr int E = SlabPiece<BF16>::kElems;
     constexpr int S = 32 / G;            // slots per step
     constexpr int U = G;                 // steps per 32-slot chunk
-    static_assert(G == 8 && (P == 2 || P == 3), "4 slots per step, 2 or 3 pieces per lane");
+    static_assert(G == 8 && P >= 2 && P <= 4, "4 slots per step, 2 to 4 pieces per lane");
     constexpr int kBlk = 4;                                      // steps per block = one padded row unit
     static_assert(S * kBlk == kFlowPad && (D == 4 || D == 8), "ring of one or two blocks");
     constexpr int kStage = 32 * P;                               // float4 per warp stage
@@ -1290,13 +1290,14 @@ template <> struct FlowCap<2, false> { static constexpr int kMinB = 8; };
 template <> struct FlowCap<3, false> { static constexpr int kMinB = 6; };
 template <> struct FlowCap<2, true> { static constexpr int kMinB = 6; };
 template <> struct FlowCap<3, true> { static constexpr int kMinB = 5; };
+template <> struct FlowCap<4, false> { static constexpr int kMinB = 5; };
 
 template <int P, int D, int W, bool BF16, bool FULL>
 cudaError_t launch_flow_k(const SlabParams& p, cudaStream_t st) {
     // one block less for the variants whose extra predicates / accumulators would otherwise spill
     // (an 8-step ring is shared-memory bound at 6 / 4 blocks: its register cap follows)
     constexpr int kMinB = D == 8 ? (P == 2 ? 6 : 4)
-                                 : FlowCap<P, BF16>::kMinB - ((BF16 || (P == 2 && !FULL)) ? 1 : 0);
+                                 : FlowCap<P, BF16>::kMinB - ((BF16 || (P == 2 && !FULL) || (P == 4 && FULL)) ? 1 : 0);
     auto k = spmm_slab_flow<8, P, D, W, kMinB * 4 / W, FULL, BF16>;
     constexpr size_t smem = (size_t)W * D * 32 * P * 16 + (size_t)W * sizeof(FlowMeta);
     // grid = SMs x resident CTAs, computed once per device (occupancy queries are not free)
@@ -1331,8 +1332,11 @@ cudaError_t launch_flow_w(const SlabParams& p, cudaStream_t st) {
 // default; 4); bf16 B: 4-step ring, 4-warp CTAs
 cudaError_t launch_slab_flow(const SlabParams& p, const Tune& t, cudaStream_t st) {
     if (p.n_rows <= 0) return cudaSuccess;
-    if (p.nv > 24 || p.nv < 1) return cudaErrorInvalidValue;
+    if (p.nv > 32 || p.nv < 1 || (p.b_bf16 && p.nv > 24)) return cudaErrorInvalidValue;
     const bool p3 = p.nv > 16;
+    // a slice of 25-32 pieces (the last one, with a short remainder merged): 4 pieces per lane,
+    // 4-warp CTAs, 4-step ring
+    if (p.nv > 24) return launch_flow_w<4, 4, 4, false>(p, st);
     if (p.b_bf16) {
         if (t.stages == 8) return cudaErrorInvalidValue;
         return p3 ? launch_flow_w<3, 4, 4, true>(p, st) : launch_flow_w<2, 4, 4, true>(p, st);

@@ -56,14 +56,14 @@ def _unsupported_ok(B):
 
 def flow_launches(F, reuse=False, bf16=False, n_cols=2300):
     """Launches of one flow-path call: count + CUB scan (2) + materialise, then one pass per
-    slice of MP 16-B pieces, a remainder of <= 24 - MP pieces merged into the last slice; MP =
+    slice of MP 16-B pieces, a remainder of <= 32 - MP (bf16: 24 - MP) pieces merged into the last slice; MP =
     tune width 8 / 16 / 24, else whichever of 16 and 24 needs fewer passes (24 while n_cols x
     384 B <= 96 MB)."""
     npieces = -(-F * (2 if bf16 else 4) // 16)
 
     def passes(mp):
         q, r = divmod(npieces, mp)
-        return q + (1 if r and not (q > 0 and mp + r <= 24) else 0)
+        return q + (1 if r and not (q > 0 and mp + r <= (24 if bf16 else 32)) else 0)
 
     mp = _OVERRIDE_WIDTH()
     if not mp:
@@ -240,10 +240,10 @@ def test_slab_launch_count(graph):
     its slots in place (slices only); reuse_sampled runs the slices only."""
     with es.kernel_override("slab_smem"):
         _slab_launch_count(graph, ((2, False, 4 + 10), (1, False, 10), (2, True, 10)))
-    # the flow kernel (the plan's): F = 602 is 151 16-B pieces -> 6 passes of 24 + one of 7;
-    # Bucket is materialised too (the padded layout)
+    # the flow kernel (the plan's): F = 602 is 151 16-B pieces -> 5 passes of 24 + one of 31
+    # (the remainder merged); Bucket is materialised too (the padded layout)
     with es.kernel_override("slab"):
-        _slab_launch_count(graph, ((2, False, 4 + 7), (1, False, 4 + 7), (2, True, 7)))
+        _slab_launch_count(graph, ((2, False, 4 + 6), (1, False, 4 + 6), (2, True, 6)))
     with es.kernel_override("slab_flow", 0, 16):                # 8 x 16 + 23 merged
         _slab_launch_count(graph, ((2, False, 4 + 9), (2, True, 9)))
 
