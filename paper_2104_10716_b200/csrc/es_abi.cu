@@ -98,15 +98,15 @@ bool slab_feasible(int64_t n_cols, int64_t F) {
 
 // es_spmm_workspace_bytes's choice (measured, profiles/r02_flow_plan.jsonl): feasible,
 // F >= 128, a 16-B row pitch, and rows that sample enough slots on average: min(s, nnz / n_rows)
-// >= 32 for F > 128 (several slices; the flow kernel beats the fused one from s = 32 on Reddit
-// F=602: 1.68 vs 1.76 ms, s = 16 1.21 vs 1.04) and >= 192 for F <= 128 (two slices: Reddit F=128
-// s=128 1.046 vs 1.039, s=256 1.61 vs 1.77; Proteins s=128 0.69 vs 0.65).  Below that the
-// fused kernels, which sample inside the gather, win.
+// >= 32 for F > 256 (Reddit F=602: s = 32 flow 1.58 vs fused 1.76 ms, s = 16 1.16 vs 1.04) and
+// >= 128 for F <= 256 (Reddit F=128 s = 128 0.91 vs 1.04, s = 64 0.61 vs 0.59; Proteins s = 128
+// 0.59 vs 0.65; F=256 s = 64 1.10 vs 1.03).  Below that the fused kernels, which sample inside
+// the gather, win.
 bool slab_wanted(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t F, int64_t ldb, int64_t s) {
     if (!slab_feasible(n_cols, F) || ldb % 4 != 0 || F < 128) return false;
     const int64_t mean_deg = n_rows > 0 ? nnz / n_rows : 0;
     const int64_t k_est = s < mean_deg ? s : mean_deg;
-    return k_est >= (F > 128 ? 32 : 192);
+    return k_est >= (F > 256 ? 32 : 128);
 }
 
 int64_t slab_align(int64_t x) { return (x + 255) & ~(int64_t)255; }
