@@ -457,6 +457,12 @@ def main():
         what = ("the slab passes alone (reuse_sampled), timed live; the step adds count + scan + sample "
                 "materialisation")
     achieved = bytes_rank / t_launch / 1e9
+    # the binding ceiling: the one the kernel runs closer to -- L2 (gathers served on chip) unless
+    # the measured DRAM traffic (ncu, profiles/ncu_traffic.json) fills more of HBM than the
+    # algorithmic bytes fill of the L2 rate; without a traffic record, by footprint
+    dram_frac_live = (traffic / (t_launch / n_launch) / 1e9 / hbm) if (traffic and hbm) else None
+    if l2 and dram_frac_live is not None:
+        resident = achieved / l2 >= dram_frac_live
     bound, peak, src = ("l2", l2, l2_src) if (resident and l2) else ("hbm", hbm, hbm_src)
     roofline = {"bound": bound, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": src,

@@ -36,6 +36,12 @@ __device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const void* src, 
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" :: "r"(dst), "l"(src), "r"(src_bytes)
                  : "memory");
 }
+// the same with an L2 eviction-policy hint (A/B: evict_last on the slab gathers)
+__device__ __forceinline__ void cp_async16_zfill_hint(uint32_t dst, const void* src, uint32_t src_bytes,
+                                                      uint64_t pol) {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;"
+                 :: "r"(dst), "l"(src), "r"(src_bytes), "l"(pol) : "memory");
+}
 
 // A 16-B piece of a B row: 4 fp32, or 8 bf16 widened exactly to fp32 (NEXT-4 storage variant).
 template <bool BF16> struct SlabPiece;
@@ -549,7 +555,7 @@ __device__ __forceinline__ int64_t flow_search(const int64_t* __restrict__ s_row
     return lo;
 }
 
-template <int G, int P, int D, int W, int MINB, bool FULL, bool BF16>
+template <int G, int P, int D, int W, int MINB, bool FULL, bool BF16, bool HINT = false>
 __global__ void __launch_bounds__(32 * W, MINB)
 spmm_slab_flow(const __grid_constant__ SlabParams p) {
     constexpr int E = SlabPiece<BF16>::kElems;
@@ -676,6 +682,7 @@ spmm_slab_flow(const __grid_constant__ SlabParams p) {
             live = fm->live;
         }
         cur = __ffs(live) - 1;
+        __syncwarp();                                            // every lane has read fm->live
         if (lane == 0) fm->live = live & (live - 1);
         cur_end = fm->endstep[cur];
         next_flush = (cur == 0 ? fm->bstart : fm->endstep[cur - 1]) + U;
@@ -699,7 +706,9 @@ spmm_slab_flow(const __grid_constant__ SlabParams p) {
 #pragma unroll
         for (int q = 0; q < P; ++q) {
             const bool on = FULL ? ok : (ok && sub + G * q < p.nv);
-            cp_async16_zfill(stage + q * 32 * 16, src + q * G * 16, on ? 16u : 0u);
+            if constexpr (HINT) cp_async16_zfill_hint(stage + q * 32 * 16, src + q * G * 16, on ? 16u : 0u,
+                                                      policy_evict_last());
+            else cp_async16_zfill(stage + q * 32 * 16, src + q * G * 16, on ? 16u : 0u);
         }
     };
     auto load_pair = [&](int32_t j, int32_t& c, float& a) {       // stream slot j (coalesced)
@@ -1292,13 +1301,14 @@ template <> struct FlowCap<2, true> { static constexpr int kMinB = 6; };
 template <> struct FlowCap<3, true> { static constexpr int kMinB = 5; };
 template <> struct FlowCap<4, false> { static constexpr int kMinB = 5; };
 
-template <int P, int D, int W, bool BF16, bool FULL>
+template <int P, int D, int W, bool BF16, bool FULL, bool HINT = false>
 cudaError_t launch_flow_k(const SlabParams& p, cudaStream_t st) {
     // one block less for the variants whose extra predicates / accumulators would otherwise spill
     // (an 8-step ring is shared-memory bound at 6 / 4 blocks: its register cap follows)
     constexpr int kMinB = D == 8 ? (P == 2 ? 6 : 4)
-                                 : FlowCap<P, BF16>::kMinB - ((BF16 || (P == 2 && !FULL) || (P == 4 && FULL)) ? 1 : 0);
-    auto k = spmm_slab_flow<8, P, D, W, kMinB * 4 / W, FULL, BF16>;
+                                 : FlowCap<P, BF16>::kMinB -
+                                       ((BF16 || (P == 2 && (!FULL || HINT)) || (P == 4 && FULL)) ? 1 : 0);
+    auto k = spmm_slab_flow<8, P, D, W, kMinB * 4 / W, FULL, BF16, HINT>;
     constexpr size_t smem = (size_t)W * D * 32 * P * 16 + (size_t)W * sizeof(FlowMeta);
     // grid = SMs x resident CTAs, computed once per device (occupancy queries are not free)
     static std::atomic<int> grid_cache[8];
@@ -1321,9 +1331,10 @@ cudaError_t launch_flow_k(const SlabParams& p, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-template <int P, int D, int W, bool BF16>
+template <int P, int D, int W, bool BF16, bool HINT = false>
 cudaError_t launch_flow_w(const SlabParams& p, cudaStream_t st) {
-    return p.nv == 8 * P ? launch_flow_k<P, D, W, BF16, true>(p, st) : launch_flow_k<P, D, W, BF16, false>(p, st);
+    return p.nv == 8 * P ? launch_flow_k<P, D, W, BF16, true, HINT>(p, st)
+                         : launch_flow_k<P, D, W, BF16, false, HINT>(p, st);
 }
 
 }  // namespace
@@ -1336,12 +1347,17 @@ cudaError_t launch_slab_flow(const SlabParams& p, const Tune& t, cudaStream_t st
     const bool p3 = p.nv > 16;
     // a slice of 25-32 pieces (the last one, with a short remainder merged): 4 pieces per lane,
     // 4-warp CTAs, 4-step ring
-    if (p.nv > 24) return launch_flow_w<4, 4, 4, false>(p, st);
+    if (p.nv > 24) return (t.variant & 1) ? launch_flow_w<4, 4, 4, false, true>(p, st)
+                                          : launch_flow_w<4, 4, 4, false>(p, st);
     if (p.b_bf16) {
         if (t.stages == 8) return cudaErrorInvalidValue;
         return p3 ? launch_flow_w<3, 4, 4, true>(p, st) : launch_flow_w<2, 4, 4, true>(p, st);
     }
     if (t.stages == 8) return p3 ? launch_flow_w<3, 8, 4, false>(p, st) : launch_flow_w<2, 8, 4, false>(p, st);
+    if (t.variant & 1) {                 // A/B: evict_last L2 policy on the slab gathers
+        if (p.nv > 24) return launch_flow_w<4, 4, 4, false, true>(p, st);
+        return p3 ? launch_flow_w<3, 4, 8, false, true>(p, st) : launch_flow_w<2, 4, 8, false, true>(p, st);
+    }
     // 8-warp CTAs by default (Reddit F=602 6.97 vs 7.16 ms, F=128 1.61 vs 1.65, Proteins 1.093 vs
     // 1.121 with 4; profiles/r02_flow_probe.jsonl)
     if (t.cta_warps == 4) return p3 ? launch_flow_w<3, 4, 4, false>(p, st) : launch_flow_w<2, 4, 4, false>(p, st);

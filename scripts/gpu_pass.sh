@@ -25,8 +25,8 @@ if [ "${SKIP_NCU:-0}" != "1" ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file "$OUT/launches_reddit602.csv" \
       python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > "$OUT/ncu_launches.log" 2>&1
   # name : bench args : kernel regex : launches of it per step
-  for spec in "reddit602::spmm_slab_flow:7" "reddit128:--config reddit --F 128:spmm_slab_flow:2" \
-              "proteins:--config proteins:spmm_slab_flow:2" "arxiv:--config arxiv:spmm:1" \
+  for spec in "reddit602::spmm_slab_flow:6" "reddit128:--config reddit --F 128:spmm_slab_flow:1" \
+              "proteins:--config proteins:spmm_slab_flow:1" "arxiv:--config arxiv:spmm:1" \
               "pubmed:--config pubmed:spmm:1" "scaled:--config scaled:spmm:1"; do
     IFS=: read -r name args kre per <<< "$spec"
     timeout 1200 ncu --set full --clock-control none --import-source on -k regex:$kre -s $((3 * per)) -c $per \

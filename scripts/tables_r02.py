@@ -1,0 +1,58 @@
+#!/usr/bin/env python3
+"""Copy a round-2 measurement pass (scripts/gpu_pass.sh <tag> -> gpurun_out/<tag>/) into profiles/
+(<tag>_bench_*.json, <tag>_ref_reddit602.json, <tag>_launches_reddit602.csv, sanitizer logs) and
+regenerate the measured tables of BASELINE.md and README.md between their <!-- x:begin/end -->
+markers.  Usage: python scripts/tables_r02.py gpurun_out/<tag> <tag>"""
+import json
+import os
+import re
+import shutil
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+P = os.path.join(ROOT, "profiles")
+CFG = [("**Reddit F=602, s=256, FastRand, mean (graded)**", "reddit602"), ("Reddit F=128, s=256, FastRand, mean", "reddit128"),
+       ("Proteins F=128, s=256, FastRand, sum", "proteins"), ("Arxiv F=128, s=64, FastRand, sum", "arxiv"),
+       ("Pubmed F=16, s=32, Bucket, sum", "pubmed"), ("Scaled 10M / 1.0B, F=256, s=128, FastRand, sum", "scaled")]
+
+
+def replace(path, tag, body):
+    s = open(path).read()
+    s = re.sub(rf"<!-- {tag}:begin -->\n.*?\n<!-- {tag}:end -->", f"<!-- {tag}:begin -->\n{body}\n<!-- {tag}:end -->",
+               s, flags=re.S)
+    open(path, "w").write(s)
+
+
+def main():
+    src, tag = sys.argv[1], sys.argv[2]
+    for f in os.listdir(src):
+        if f.startswith(("bench_", "ref_", "launches_", "sanitize_", "pytest_gpu", "smoke")):
+            shutil.copy(os.path.join(src, f), os.path.join(P, f"{tag}_{f}"))
+    rows, rrows = [], []
+    for name, n in CFG:
+        d = json.load(open(os.path.join(P, f"{tag}_bench_{n}.json")))
+        r = d["roofline"]
+        kern = r["kernel"].replace("es::", "").split(": ")[0].split("(")[0].strip()
+        if r["kernel"].startswith("slab pass"):
+            kern = f"spmm_slab_flow ×{r['launches_per_step']} + sampling"
+        K = d["config"]["K_sampled"]
+        dram = f"{r['dram_frac']:.3f}" if r.get("dram_frac") is not None else "–"
+        e2e = d.get("e2e") or {}
+        rows.append(f"| {name} | {K / 1e6:.2f}M | {d['ms_per_step']:.3f} ({d['detail']['step_ms_min']:.3f}) | "
+                    f"{d['value']:,.0f} | {r['achieved']:,.0f} ({r['launch_ms']:.3f} × {r['launches_per_step']}) | "
+                    f"**{r['frac']:.3f}** ({r['bound']}) | {dram} | {e2e.get('value', 0):,.0f} ({e2e.get('ms_per_step', 0):.3f}) | "
+                    f"{d['cpu_baseline']['value']:.1f} | `{kern}` |")
+        rrows.append(f"| {d['config']['workload']} | {d['ms_per_step']:.3f} | {d['value']:,.0f} | "
+                     f"{r['frac']:.3f} ({r['bound']}) | {dram} | {e2e.get('ms_per_step', 0):.3f} |")
+    hdr = ("| config | K sampled | ms / step (min) | GFLOP/s | gather-FMA GB/s (launch ms × launches) | roofline frac "
+           "(bound) | DRAM frac | e2e GFLOP/s (ms, host buffers) | oracle, 16 cores | kernel |\n"
+           "|---|---|---|---|---|---|---|---|---|---|\n")
+    replace(os.path.join(ROOT, "BASELINE.md"), "measured", hdr + "\n".join(rows))
+    replace(os.path.join(ROOT, "README.md"), "readme", "| workload | ms / step (median) | GFLOP/s | roofline frac of "
+            "the binding ceiling (bound) | DRAM frac | e2e ms (host buffers) |\n|---|---|---|---|---|---|\n"
+            + "\n".join(rrows))
+    print("\n".join(rows))
+
+
+if __name__ == "__main__":
+    main()
