@@ -1307,7 +1307,7 @@ cudaError_t launch_flow_k(const SlabParams& p, cudaStream_t st) {
     // (an 8-step ring is shared-memory bound at 6 / 4 blocks: its register cap follows)
     constexpr int kMinB = D == 8 ? (P == 2 ? 6 : 4)
                                  : FlowCap<P, BF16>::kMinB -
-                                       ((BF16 || (P == 2 && (!FULL || HINT)) || (P == 4 && FULL)) ? 1 : 0);
+                                       ((BF16 || (P == 2 && (!FULL || HINT)) || (P == 4 && FULL && !HINT)) ? 1 : 0);
     auto k = spmm_slab_flow<8, P, D, W, kMinB * 4 / W, FULL, BF16, HINT>;
     constexpr size_t smem = (size_t)W * D * 32 * P * 16 + (size_t)W * sizeof(FlowMeta);
     // grid = SMs x resident CTAs, computed once per device (occupancy queries are not free)
