@@ -21,6 +21,7 @@ $B --bf16 --no-e2e --no-cpu-baseline > "$OUT/bench_reddit602_bf16.json" 2>> "$OU
 $B --config reddit --F 128 > "$OUT/bench_reddit128.json" 2>> "$OUT/bench.err"
 for c in proteins arxiv pubmed scaled; do $B --config $c > "$OUT/bench_$c.json" 2>> "$OUT/bench.err"; done
 timeout 600 python bench.py --impl reference --steps 3 > "$OUT/ref_reddit602.json" 2> "$OUT/ref.err"
+timeout 1200 python scripts/s_sweep.py > "$OUT/s_sweep.jsonl" 2> "$OUT/s_sweep.err"
 if [ "${SKIP_NCU:-0}" != "1" ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file "$OUT/launches_reddit602.csv" \
       python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > "$OUT/ncu_launches.log" 2>&1

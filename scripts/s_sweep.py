@@ -17,6 +17,8 @@ import synth  # noqa: E402
 import paper_2104_10716_b200 as es  # noqa: E402
 from bench import L2_RESIDENT_BYTES, byte_model, l2_peak, ldb_for, measured_peaks  # noqa: E402
 
+L2_BYTES = 126 << 20                # the B200 L2
+
 CASES = [("pubmed", 16, 0), ("arxiv", 128, 0), ("proteins", 128, 0), ("reddit", 128, 1), ("reddit", 602, 1)]
 
 
@@ -46,6 +48,7 @@ def main():
             ws = (None if kernel == "fused" else es.es_spmm_workspace(n, n, len(colind), F, ldb, s, True, device=dev))
             for strat in (1, 2):
                 ts = []
+                lc0 = es.es_launch_count()
                 for i in range(7):
                     flush.zero_()
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -59,9 +62,13 @@ def main():
                     if i >= 2:
                         ts.append(e0.elapsed_time(e1))
                 ms = float(np.median(ts))
+                per_call = (es.es_launch_count() - lc0) // 7
                 gbs = byte_model(K, n, F) / (ms / 1e3) / 1e9
-                # the ceiling that binds (as bench.py): L2 when the gathered operand is L2-resident
-                resident = (n * 256 if ws is not None else n * ldb * 4) <= L2_RESIDENT_BYTES
+                # the ceiling that binds (as bench.py without a traffic record): L2 when the gathered
+                # operand is L2-resident -- B itself, or on the slab path its widest slab (<= 512 B of
+                # each row, within the 126 MB L2)
+                resident = ((n * min(ldb * 4, 512) <= L2_BYTES) if ws is not None else
+                            (n * ldb * 4 <= L2_RESIDENT_BYTES))
                 bound, peak = ("l2", l2) if (resident and l2) else ("hbm", hbm)
                 print(json.dumps({"graph": name, "F": F, "s": s, "strategy": "bucket" if strat == 1 else "fastrand",
                                   "reduce": "mean" if red else "sum", "K": K, "rate": round(K / d.sum(), 4),
@@ -69,8 +76,9 @@ def main():
                                   "model_GBs": round(gbs, 1), "bound": bound, "frac": round(gbs / peak, 3),
                                   "step_incl_sampling": True,
                                   "sampled_edges_per_s": round(K / (ms / 1e3)),
-                                  "plan": "slab path (spmm_slab x %d + sampling)" % ((F + 63) // 64)
-                                  if ws is not None else es.es_spmm_plan(F, ldb, ldb, B, C)}), flush=True)
+                                  "plan": "slab path (spmm_slab_flow x %d + sampling)" % (per_call - 4)
+                                  if ws is not None else es.es_spmm_plan(F, ldb, ldb, B, C, s=s, n_rows=n,
+                                                                          nnz=len(colind))}), flush=True)
 
 
 if __name__ == "__main__":

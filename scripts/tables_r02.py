@@ -26,7 +26,7 @@ def replace(path, tag, body):
 def main():
     src, tag = sys.argv[1], sys.argv[2]
     for f in os.listdir(src):
-        if f.startswith(("bench_", "ref_", "launches_", "sanitize_", "pytest_gpu", "smoke")):
+        if f.startswith(("bench_", "ref_", "launches_", "sanitize_", "pytest_gpu", "smoke", "s_sweep.jsonl")):
             shutil.copy(os.path.join(src, f), os.path.join(P, f"{tag}_{f}"))
     rows, rrows = [], []
     for name, n in CFG:
@@ -51,6 +51,27 @@ def main():
     replace(os.path.join(ROOT, "README.md"), "readme", "| workload | ms / step (median) | GFLOP/s | roofline frac of "
             "the binding ceiling (bound) | DRAM frac | e2e ms (host buffers) |\n|---|---|---|---|---|---|\n"
             + "\n".join(rrows))
+    sw = os.path.join(P, f"{tag}_s_sweep.jsonl")
+    if os.path.exists(sw) and os.path.getsize(sw) > 0:
+        from collections import defaultdict
+        t = defaultdict(dict)
+        for line in open(sw):
+            if line.startswith("{"):
+                x = json.loads(line)
+                t[(x["graph"], x["F"], x["reduce"])][(x["s"], x["strategy"])] = x
+        lines = ["| graph, F, reduce | s=16: Bucket / FastRand | s=32 | s=64 | s=128 | s=256 | s=512 |",
+                 "|---|---|---|---|---|---|---|"]
+        for (g, F, red), dd in t.items():
+            cells = []
+            for sv in (16, 32, 64, 128, 256, 512):
+                b, f = dd.get((sv, "bucket")), dd.get((sv, "fastrand"))
+                if not b or not f:
+                    cells.append("–")
+                    continue
+                mark = " †" if "slab" in b["plan"] else ""
+                cells.append(f"{b['GFLOPs']:,.0f} ({b['frac']:.2f}) / {f['GFLOPs']:,.0f} ({f['frac']:.2f}){mark}")
+            lines.append(f"| {g}, {F}, {red} | " + " | ".join(cells) + " |")
+        replace(os.path.join(ROOT, "BASELINE.md"), "ssweep", "\n".join(lines))
     print("\n".join(rows))
 
 
