@@ -226,7 +226,9 @@ es_status_t run_rows_impl(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
                             tn.kernel == ES_KERNEL_SLAB_STREAM || tn.kernel == ES_KERNEL_SLAB_FLOW;
     const uintptr_t bu = reinterpret_cast<uintptr_t>(B), cu = reinterpret_cast<uintptr_t>(C);
     const int64_t esz = o.bf16 ? 2 : 4;
-    const bool slab_layout_ok = o.workspace && bu % 16 == 0 && (ldb * esz) % 16 == 0 && slab_feasible(n_cols, F) &&
+    // a forced flow kernel runs whatever the slab's size (A/B: slabs beyond L2, e.g. the 10M-row graph)
+    const bool feasible = slab_feasible(n_cols, F) || (tn.kernel == ES_KERNEL_SLAB_FLOW && F > kSlabF / 4);
+    const bool slab_layout_ok = o.workspace && bu % 16 == 0 && (ldb * esz) % 16 == 0 && feasible &&
                                 tn.kernel != ES_KERNEL_FUSED && tn.kernel != ES_KERNEL_WARP &&
                                 tn.kernel != ES_KERNEL_TMA && tn.kernel != ES_KERNEL_CPASYNC &&
                                 tn.kernel != ES_KERNEL_CPASYNC_HW && tn.kernel != ES_KERNEL_ROWSTREAM &&
@@ -402,7 +404,7 @@ int64_t es_spmm_workspace_bytes_ex(int64_t n_rows, int64_t n_cols, int64_t nnz, 
         return es_spmm_workspace_bytes(n_rows, n_cols, nnz, F, ldb, s, has_val);
     // a slab kernel forced: a workspace wherever the path can run at all
     if (n_rows <= 0 || n_cols < 0 || nnz < 0 || F < 1 || ldb < F || s < 1) return 0;
-    if (!slab_feasible(n_cols, F) || ldb % 4 != 0) return 0;
+    if (!(slab_feasible(n_cols, F) || (k == ES_KERNEL_SLAB_FLOW && F > kSlabF / 4)) || ldb % 4 != 0) return 0;
     return slab_bytes(n_rows, slab_cap_needed(n_rows, nnz, s), has_val != 0) + 256;
 }
 
