@@ -800,6 +800,163 @@ spmm_grouped(const SpmmParams p) {
     }
 }
 
+// The same degree-sorted half-warp pairs with a cp.async ring per half instead of register-direct
+// gathers (U = 0 selects it in launch_grouped): lane l of a half copies pieces l and l + 16 of each
+// slot's B row into its own D-deep shared-memory ring and reads back only what it copied (no
+// synchronisation), so D slots of the row are in flight without holding registers; the next
+// round's first (col, val) chunk is loaded during the current round.  Per element: slot order,
+// 32-slot-chunk partials -- bitwise spmm_warp / spmm_grouped.
+template <int D, int MINB>
+__global__ void __launch_bounds__(32 * kGroupedWarps, MINB)
+spmm_grouped_ring(const SpmmParams p) {
+    extern __shared__ __align__(16) float4 gring[];              // [warps][D][2 pieces][32 lanes]
+    const int lane = threadIdx.x & 31;
+    const int h = lane >> 4, l = lane & 15;
+    const int warp = threadIdx.x >> 5;
+    const int64_t r0 = ((int64_t)blockIdx.x * kGroupedWarps + warp) * 32;
+    if (r0 >= p.n_rows) return;
+    float4* my = gring + (size_t)warp * D * 64 + lane;            // + stage * 64 (+ 32 for piece 1)
+    const uint64_t pol_a = policy_evict_first(), pol_b = policy_evict_last();
+    const int NV = (int)((p.F + 3) / 4);
+    const bool act0 = l < NV, act1 = l + 16 < NV;
+    int64_t beg = 0, deg = 0;
+    int32_t k = -1;
+    if (r0 + lane < p.n_rows) {
+        const int64_t a = ld_stream(p.rowptr + r0 + lane, pol_a);
+        const int64_t b = ld_stream(p.rowptr + r0 + lane + 1, pol_a);
+        beg = a - p.nnz_base;
+        deg = b - a;
+        k = deg < (int64_t)p.s ? (int32_t)deg : p.s;
+    }
+    int32_t sk = k, si = lane;
+#pragma unroll
+    for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            const int32_t ok = __shfl_xor_sync(kFull, sk, stride), oi = __shfl_xor_sync(kFull, si, stride);
+            const bool other_first = ok > sk || (ok == sk && oi < si);
+            const bool desc = (lane & size) == 0 || size == 32;
+            const bool lower = (lane & stride) == 0;
+            if ((desc == lower) ? other_first : !other_first) { sk = ok; si = oi; }
+        }
+    }
+    const float* bl = p.B + l * 4;
+    // a round's row for this half: sampler, stepped positions, the first (col, val) chunk
+    struct RoundRow {
+        RowSampler rs;
+        int32_t kk;
+        int64_t r;
+        uint32_t pos, delta;
+        bool step_ok;
+    };
+    auto round_row = [&](int round, RoundRow& q) {
+        q.kk = __shfl_sync(kFull, sk, 2 * round + h);
+        const int ri = __shfl_sync(kFull, si, 2 * round + h);
+        const int64_t rb = __shfl_sync(kFull, beg, ri), rd = __shfl_sync(kFull, deg, ri);
+        q.r = r0 + ri;
+        q.rs.init(rb, rb + (q.kk >= 0 ? rd : 0), p.s, p.strategy, p.seed, p.row_base + q.r, p.prime);
+        q.step_ok = p.strategy == kBucket || (q.rs.narrow && q.rs.d < ((int64_t)1 << 31));
+        q.delta = p.strategy == kBucket ? 16u : (q.rs.d > 0 ? (uint32_t)((16ull * q.rs.prime) % (uint64_t)q.rs.d) : 0u);
+        q.pos = (l < q.kk) ? (uint32_t)q.rs.pos(l) : 0u;
+    };
+    auto load_chunk = [&](RoundRow& q, int32_t m, int32_t& c, float& a) {   // slot 16m + l of q's row
+        const int32_t j = 16 * m + l;
+        c = 0;
+        a = 0.0f;
+        if (j < q.kk) {
+            const int64_t pj = q.step_ok ? (int64_t)q.pos : q.rs.pos(j);
+            c = ld_stream(p.colind + q.rs.beg + pj, pol_a);
+            a = p.val ? ld_stream(p.val + q.rs.beg + pj, pol_a) : 1.0f;
+        }
+        if (q.step_ok) {
+            q.pos += q.delta;
+            if (p.strategy != kBucket && q.pos >= (uint32_t)q.rs.d) q.pos -= (uint32_t)q.rs.d;
+        }
+    };
+    RoundRow cur, nxt;
+    int32_t nc0 = 0;
+    float na0 = 0.0f;
+    round_row(0, cur);
+    int32_t c0, c1 = 0;
+    float a0, a1 = 0.0f;
+    load_chunk(cur, 0, c0, a0);
+    for (int round = 0; round < 16; ++round) {
+        const int32_t kmax = __shfl_sync(kFull, sk, 2 * round);
+        if (kmax < 0) break;
+        // the next round's row and first chunk, loaded while this round streams
+        const bool more = round + 1 < 16 && __shfl_sync(kFull, sk, 2 * round + 2) >= 0;
+        if (more) {
+            round_row(round + 1, nxt);
+            load_chunk(nxt, 0, nc0, na0);
+        }
+        if (kmax > 16) load_chunk(cur, 1, c1, a1);
+        auto copy_slot = [&](int stage, int32_t j, int32_t cj) {
+            if (j < cur.kk) {
+                const float* src = bl + (int64_t)cj * p.ldb;
+                if (act0) cp_async16(my + stage * 64, src, pol_b);
+                if (act1) cp_async16(my + stage * 64 + 32, src + 64, pol_b);
+            }
+        };
+#pragma unroll
+        for (int t = 0; t < D; ++t) {
+            copy_slot(t, t, __shfl_sync(kFull, c0, (lane & 16) | t));
+            cp_async_commit();
+        }
+        float part[8], tot[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) { part[q] = 0.0f; tot[q] = 0.0f; }
+        for (int32_t j0 = 0; j0 < kmax; j0 += D) {
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+                const int32_t j = j0 + d;                        // stage d (j0 is a multiple of D)
+                cp_async_wait<D - 1>();
+                const float av = __shfl_sync(kFull, a0, (lane & 16) | (j & 15));
+                if (j < cur.kk) {
+                    if (act0) {
+                        const float4 x = my[d * 64];
+                        part[0] = fmaf(av, x.x, part[0]); part[1] = fmaf(av, x.y, part[1]);
+                        part[2] = fmaf(av, x.z, part[2]); part[3] = fmaf(av, x.w, part[3]);
+                    }
+                    if (act1) {
+                        const float4 x = my[d * 64 + 32];
+                        part[4] = fmaf(av, x.x, part[4]); part[5] = fmaf(av, x.y, part[5]);
+                        part[6] = fmaf(av, x.z, part[6]); part[7] = fmaf(av, x.w, part[7]);
+                    }
+                }
+                const int32_t jn = j + D;                        // refill: slot j + D
+                const int32_t cn = __shfl_sync(kFull, ((jn >> 4) == (j >> 4)) ? c0 : c1, (lane & 16) | (jn & 15));
+                copy_slot(d, jn, cn);
+                cp_async_commit();
+                if (((j + 1) & 15) == 0) {                       // chunk consumed
+                    if (((j + 1) & 31) == 0) {
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) { tot[q] += part[q]; part[q] = 0.0f; }
+                    }
+                    c0 = c1; a0 = a1;
+                    c1 = 0; a1 = 0.0f;
+                    if (j + 17 < kmax) load_chunk(cur, ((j + 1) >> 4) + 1, c1, a1);
+                }
+            }
+        }
+        cp_async_wait<0>();
+        __syncwarp();
+        if (cur.kk >= 0) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) tot[q] += part[q];
+            const int64_t div = mean_div(p, cur.rs.d, cur.kk);
+            float res[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) res[q] = finish(tot[q], p.reduce, div);
+            if (act0) store_c<4>(p, cur.r, l, res, pol_a);
+            if (act1) store_c<4>(p, cur.r, l + 16, res + 4, pol_a);
+        }
+        if (!more) break;
+        cur = nxt;
+        c0 = nc0; a0 = na0;
+        c1 = 0; a1 = 0.0f;
+    }
+}
+
 // ------------------------------------------------------------------ per-warp slot stream
 // A warp owns R <= 32 consecutive rows; their sampled slots form one flat stream (row by
 // row, slot order).  Row i's metadata (a1) lives in lane i; (col, val) of 32 consecutive
@@ -1244,8 +1401,24 @@ cudaError_t launch_grouped_k(const SpmmParams& p, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-// slots in flight per lane U = tune.stages (4 default; 2, 8)
+template <int D, int MINB>
+cudaError_t launch_grouped_ring_k(const SpmmParams& p, cudaStream_t st) {
+    const int64_t warps = (p.n_rows + 31) / 32;
+    const int64_t blocks = (warps + kGroupedWarps - 1) / kGroupedWarps;
+    const size_t smem = (size_t)kGroupedWarps * D * 64 * 16;
+    auto k = spmm_grouped_ring<D, MINB>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    k<<<(unsigned)blocks, 32 * kGroupedWarps, smem, st>>>(p);
+    return cudaGetLastError();
+}
+
+// slots in flight per lane U = tune.stages (4 default; 2, 8); tune.variant & 1: the cp.async-ring
+// form (ring depth 4, or 8 with stages 8)
 cudaError_t launch_grouped(const SpmmParams& p, const Tune& t, cudaStream_t st) {
+    if (t.variant & 1) return t.stages == 8 ? launch_grouped_ring_k<8, 5>(p, st) : launch_grouped_ring_k<4, 6>(p, st);
     if (t.stages == 2) return launch_grouped_k<2, 8>(p, st);
     if (t.stages == 8) return launch_grouped_k<8, 4>(p, st);
     return launch_grouped_k<4, 6>(p, st);

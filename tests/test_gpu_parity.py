@@ -134,6 +134,7 @@ KERNEL_PARAMS = {                       # name -> (kernel family, tune: stages, 
     "halfwarp": ("halfwarp", ()), "slab": ("slab", ()), "slab16": ("slab_smem", (0, 16)),
     "slab_ldg": ("slab_ldg", ()), "slab_tma": ("slab_tma", ()), "slab_stream": ("slab_stream", (0, 0, 0, 1024)),
     "rowstream": ("rowstream", ()), "grouped": ("grouped", ()), "grouped8": ("grouped", (8,)),
+    "grouped_ring": ("grouped", (4, 0, 0, 1)),
 }
 
 
@@ -187,8 +188,8 @@ def test_ones_give_exact_counts(ragged, kernel):
 
 
 @pytest.mark.parametrize("F", [65, 100, 128])
-@pytest.mark.parametrize("U", [2, 4, 8])
-def test_grouped_bitwise_warp(ragged, F, U):
+@pytest.mark.parametrize("U,ring", [(2, 0), (4, 0), (8, 0), (4, 1), (8, 1)])
+def test_grouped_bitwise_warp(ragged, F, U, ring):
     """The degree-sorted half-warp kernel (spmm_grouped) sums each row in slot order with
     32-slot-chunk partials, exactly as the LDG warp-per-row kernel does: bitwise, whatever the
     sort put in each half-warp or how many slots are in flight."""
@@ -198,9 +199,9 @@ def test_grouped_bitwise_warp(ragged, F, U):
                           (700, ES_FASTRAND, ES_REDUCE_MEAN), (1, ES_FASTRAND, ES_REDUCE_SUM)):
         with es.kernel_override("warp"):
             a = run_gpu(rowptr, colind, val, B, s, strat, 5, red, F=F)
-        with es.kernel_override("grouped", U):
+        with es.kernel_override("grouped", U, 0, 0, ring):
             b = run_gpu(rowptr, colind, val, B, s, strat, 5, red, F=F)
-        assert np.array_equal(a, b), (F, s, strat)
+        assert np.array_equal(a, b), (F, s, strat, ring)
 
 
 @pytest.mark.parametrize("F", [65, 100, 128])
