@@ -307,7 +307,7 @@ es_status_t run_rows_impl(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
             // default: the width with fewer passes (a pass costs about the same from 16 to 24
             // pieces on a 2.4-KB-pitch B: Reddit F=602 7 passes of 24 (+7) 7.17 ms vs 9 of 16 (+7
             // merged) 9.15 ms; F=128: 2 x 16), 24 only while its slab (n_cols x 384 B) fits L2
-            int64_t MP = (tn.width == 8 || tn.width == 16 || tn.width == 24) ? tn.width : 16;
+            int64_t MP = (tn.width == 8 || tn.width == 16 || tn.width == 24 || (tn.width == 32 && !o.bf16)) ? tn.width : 16;
             if (tn.width == 0 && passes(24) < passes(16) && n_cols * 384 <= kSlabMaxBytes24) MP = 24;
             const int64_t m = passes(MP);
             for (int64_t i = 0; err == cudaSuccess && i < m; ++i) {
