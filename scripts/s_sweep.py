@@ -15,7 +15,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import synth  # noqa: E402
 import paper_2104_10716_b200 as es  # noqa: E402
-from bench import L2_RESIDENT_BYTES, byte_model, l2_peak, ldb_for, measured_peaks  # noqa: E402
+from bench import byte_model, l2_peak, ldb_for, measured_peaks  # noqa: E402
 
 L2_BYTES = 126 << 20                # the B200 L2
 
@@ -67,8 +67,7 @@ def main():
                 # the ceiling that binds (as bench.py without a traffic record): L2 when the gathered
                 # operand is L2-resident -- B itself, or on the slab path its widest slab (<= 512 B of
                 # each row, within the 126 MB L2)
-                resident = ((n * min(ldb * 4, 512) <= L2_BYTES) if ws is not None else
-                            (n * ldb * 4 <= L2_RESIDENT_BYTES))
+                resident = (n * min(ldb * 4, 512) if ws is not None else n * ldb * 4) <= L2_BYTES
                 bound, peak = ("l2", l2) if (resident and l2) else ("hbm", hbm)
                 print(json.dumps({"graph": name, "F": F, "s": s, "strategy": "bucket" if strat == 1 else "fastrand",
                                   "reduce": "mean" if red else "sum", "K": K, "rate": round(K / d.sum(), 4),
