@@ -58,7 +58,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--kernel", default="auto",
                     choices=["auto", "fused", "slab", "slab_smem", "slab_ldg", "slab_tma", "slab_stream", "tma", "warp",
-                             "cpasync", "halfwarp", "rowstream"],
+                             "cpasync", "halfwarp", "rowstream", "grouped", "segstream"],
                     help="kernel family (A/B measurement through es_spmm_options_t.kernel; auto = the "
                          "library's plan, fused = never the feature-sliced path, slab* = that path wherever "
                          "it can run)")

@@ -152,8 +152,11 @@ enum {
     ES_KERNEL_SLAB_STREAM = 11, /* feature-sliced path, R rows per warp as one padded slot stream   */
     ES_KERNEL_SLAB_FLOW = 12,   /* feature-sliced path, persistent warps streaming slot-balanced
                                    row ranges across row boundaries (the plan's slab kernel)      */
-    ES_KERNEL_GROUPED = 13      /* short rows, F <= 128: 32-row batches sorted by k_i, a half-warp
+    ES_KERNEL_GROUPED = 13,     /* short rows, F <= 128: 32-row batches sorted by k_i, a half-warp
                                    per row with register-direct gathers                           */
+    ES_KERNEL_SEGSTREAM = 14    /* short rows, F <= 128: R rows per warp as one slot stream, row
+                                   and chunk events as lane-parallel ballots, register-direct
+                                   double-buffered gathers                                       */
 };
 
 /* Status word of a slab workspace (written by the device; reading it synchronises `stream`).

@@ -20,12 +20,12 @@ ES_MEAN_BY_SAMPLED, ES_MEAN_BY_DEGREE = 0, 1
 ES_DTYPE_F32, ES_DTYPE_BF16 = 0, 1
 (ES_KERNEL_AUTO, ES_KERNEL_FUSED, ES_KERNEL_WARP, ES_KERNEL_TMA, ES_KERNEL_CPASYNC, ES_KERNEL_CPASYNC_HW,
  ES_KERNEL_SLAB, ES_KERNEL_SLAB_SMEM, ES_KERNEL_SLAB_LDG, ES_KERNEL_SLAB_TMA, ES_KERNEL_ROWSTREAM,
- ES_KERNEL_SLAB_STREAM, ES_KERNEL_SLAB_FLOW, ES_KERNEL_GROUPED) = range(14)
+ ES_KERNEL_SLAB_STREAM, ES_KERNEL_SLAB_FLOW, ES_KERNEL_GROUPED, ES_KERNEL_SEGSTREAM) = range(15)
 KERNELS = {"auto": ES_KERNEL_AUTO, "fused": ES_KERNEL_FUSED, "warp": ES_KERNEL_WARP, "tma": ES_KERNEL_TMA,
            "cpasync": ES_KERNEL_CPASYNC, "halfwarp": ES_KERNEL_CPASYNC_HW, "slab": ES_KERNEL_SLAB,
            "slab_smem": ES_KERNEL_SLAB_SMEM, "slab_ldg": ES_KERNEL_SLAB_LDG, "slab_tma": ES_KERNEL_SLAB_TMA,
            "rowstream": ES_KERNEL_ROWSTREAM, "slab_stream": ES_KERNEL_SLAB_STREAM, "slab_flow": ES_KERNEL_SLAB_FLOW,
-           "grouped": ES_KERNEL_GROUPED}
+           "grouped": ES_KERNEL_GROUPED, "segstream": ES_KERNEL_SEGSTREAM}
 ES_WS_OK, ES_WS_OVERFLOW, ES_WS_SIGNATURE_MISMATCH = 0, 1, 2
 
 _HERE = os.path.dirname(os.path.abspath(__file__))

@@ -74,7 +74,7 @@ es_status_t read_opts(const es_spmm_options_t* o, Opts* out) {
         out->nnz = o->nnz;
     }
     if (ES_COVERS(o, tune)) {
-        if (o->kernel < ES_KERNEL_AUTO || o->kernel > ES_KERNEL_GROUPED) return ES_ERR_INVALID_VALUE;
+        if (o->kernel < ES_KERNEL_AUTO || o->kernel > ES_KERNEL_SEGSTREAM) return ES_ERR_INVALID_VALUE;
         out->tune.kernel = o->kernel;
         out->tune.stages = o->tune[0];
         out->tune.width = o->tune[1];
@@ -232,7 +232,7 @@ es_status_t run_rows_impl(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
                                 tn.kernel != ES_KERNEL_FUSED && tn.kernel != ES_KERNEL_WARP &&
                                 tn.kernel != ES_KERNEL_TMA && tn.kernel != ES_KERNEL_CPASYNC &&
                                 tn.kernel != ES_KERNEL_CPASYNC_HW && tn.kernel != ES_KERNEL_ROWSTREAM &&
-                                tn.kernel != ES_KERNEL_GROUPED;
+                                tn.kernel != ES_KERNEL_GROUPED && tn.kernel != ES_KERNEL_SEGSTREAM;
     if (force_slab && !slab_layout_ok) return ES_ERR_UNSUPPORTED;
     if (slab_layout_ok) {
         // any C layout: 16-B vector stores where C's rows allow them, scalar stores otherwise
@@ -361,10 +361,18 @@ es_status_t run_rows_impl(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
     p.n_peers = o.n_peers;
     p.c_mc = o.c_mc;
     const int64_t k_est = o.nnz > 0 ? std::min<int64_t>(s, o.nnz / n) : s;
-    const es::Plan plan = o.bf16 ? es::make_plan_bf16(F, ldb, ldc, B, C)
-                                 : es::make_plan(F, ldb, ldc, B, C, s, tn, k_est);
+    es::Plan plan = o.bf16 ? es::make_plan_bf16(F, ldb, ldc, B, C)
+                           : es::make_plan(F, ldb, ldc, B, C, s, tn, k_est);
     if (plan.unsupported) return ES_ERR_UNSUPPORTED;
     if (tn.kernel == ES_KERNEL_ROWSTREAM && !plan.rowstream) return ES_ERR_UNSUPPORTED;
+    if (plan.segstream && (uint64_t)n_cols * (uint64_t)(ldb / 4) >= (1ull << 32)) {
+        // the segmented stream addresses B rows by a 32-bit float4 index (B > 64 GB: not expressible)
+        if (tn.kernel == ES_KERNEL_SEGSTREAM) return ES_ERR_UNSUPPORTED;
+        es::Tune t2 = tn;
+        t2.kernel = ES_KERNEL_CPASYNC_HW;
+        plan = es::make_plan(F, ldb, ldc, B, C, s, t2, k_est);
+    }
+    if (tn.kernel == ES_KERNEL_SEGSTREAM && !plan.segstream) return ES_ERR_UNSUPPORTED;
     cudaError_t err = es::launch_spmm(p, plan, tn, st);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return err == cudaSuccess ? ES_OK : ES_ERR_CUDA;
@@ -432,7 +440,10 @@ es_status_t es_spmm_plan_ex(int64_t F, int64_t ldb, int64_t ldc, const void* B, 
         return ES_ERR_INVALID_VALUE;
     const int64_t k_est = (nnz > 0 && n_rows > 0) ? std::min<int64_t>(s, nnz / n_rows) : s;
     const es::Plan pl = es::make_plan(F, ldb, ldc, B, C, s, es::Tune{}, k_est);
-    if (pl.grouped)
+    if (pl.segstream)
+        snprintf(buf, (size_t)buf_len, "es::spmm_segstream<rows%d>%s", pl.rows_per_warp,
+                 pl.c_vec ? "" : " (scalar C)");
+    else if (pl.grouped)
         snprintf(buf, (size_t)buf_len, "es::spmm_grouped<slots4>(32-row degree-sorted batches)%s",
                  pl.c_vec ? "" : " (scalar C)");
     else if (pl.rowstream)

@@ -51,6 +51,7 @@ struct Plan {
     bool halfwarp;     // cp.async ring, two slots per step (spmm_cpasync_hw)
     bool rowstream;    // several short rows per warp as one slot stream (spmm_rowstream)
     bool grouped;      // short rows: degree-sorted 32-row batches, a half-warp per row (spmm_grouped)
+    bool segstream;    // short rows: R rows per warp as one register-direct slot stream (spmm_segstream)
     bool unsupported;  // no kernel for this layout (bf16 with misaligned rows)
     int stages;         // ring depth (tma)
     int rows_per_warp;  // consecutive rows per warp (tma)

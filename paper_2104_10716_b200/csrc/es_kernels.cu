@@ -44,6 +44,11 @@ constexpr int64_t kRowStreamMaxK = 0;
 // when rows sample at most this many slots on average (profiles/r02_grouped_probe.jsonl)
 constexpr int kGroupedWarps = 4;
 constexpr int64_t kGroupedMaxK = 0;     // never by default: measured no faster than the two-slot ring (profiles/r02_grouped_probe.jsonl)
+// the segmented register stream (spmm_segstream): rows per warp, register cap (4-warp CTAs per
+// SM), and the plan's threshold on the mean sampled slots per row (profiles/r02_segstream_probe.jsonl)
+constexpr int kSegRows = 8;
+constexpr int kSegMinB = 7;
+constexpr int64_t kSegMaxK = INT64_MAX;
 
 template <int VEC>
 __device__ __forceinline__ void store_out(float* Crow, int64_t vidx, int64_t F, const float* r,
@@ -657,6 +662,231 @@ spmm_cpasync_hw(const SpmmParams p) {
         if (act0) store_c<4>(p, r, sub, res, pol_a);
         if (act1) store_c<4>(p, r, sub + 16, res + 4, pol_a);
     }
+}
+
+// ------------------------------------------------------------------ short rows: segmented register stream
+// The row-to-warp mapping for short rows (§4.5.1 thread management L1073-1081, §4.5.3
+// load balancing L1100-1105), round 2: one warp owns R consecutive rows and walks their sampled
+// slots as ONE flat stream, each row padded to whole 4-slot groups, so that
+//   * every per-row and per-slot decision is made LANE-PARALLEL once per 32-slot chunk: lane l
+//     finds the row of padded slot t0 + l (binary search over the lanes' padded prefix), its
+//     position (Eq. 2 / R6), (col, val) and the B row's float4 index; warp ballots turn "slot is
+//     real", "group starts a row" and "group starts a 32-slot partial chunk of its row" into
+//     uniform bit masks.  A chunk's (index, val) pairs go to a per-warp shared-memory slot one
+//     chunk after their loads were issued (so the colind latency is hidden), and a group reads
+//     its 4 indices / 4 values with one broadcast LDS.128 each;
+//   * row ends and chunk partials fall on group boundaries: one event test per 4-slot group, no
+//     per-slot bookkeeping (padding slots: predicated-off gathers and FMAs, no memory traffic);
+//   * B rows are gathered register-direct (one LDG.128 per lane per slot; lane l owns float4 l of
+//     the row, F <= 128), 4 slots per group, double-buffered: group g+1's loads are issued before
+//     group g's FMAs, across chunk boundaries, so 4-8 gathers per warp are always in flight;
+//   * the group loop is rolled (two groups per iteration, one copy of the row epilogue per
+//     group site): the hot loop stays inside the ~6 KB L0 instruction cache.
+// Per element: the row's slots in slot order with 32-slot chunk partials (tot += part at every
+// chunk start and at the row's end) -- spmm_warp's order, bitwise.  Needs n_cols * ldb / 4 < 2^32
+// (the 32-bit float4 index; the ABI checks it).
+__device__ __forceinline__ unsigned group_bits(unsigned m) {     // bits 0, 4, .., 28 -> bits 0 .. 7
+    m &= 0x11111111u;
+    m = (m | (m >> 3)) & 0x03030303u;
+    m = (m | (m >> 6)) & 0x000F000Fu;
+    return (m | (m >> 12)) & 0xFFu;
+}
+
+template <int R, int W, int MINB, bool HAS_VAL>
+__global__ void __launch_bounds__(32 * W, MINB)
+spmm_segstream(const SpmmParams p) {
+    static_assert(R >= 1 && R <= 32, "rows per warp");
+    const int lane = threadIdx.x & 31;
+    const int w = threadIdx.x >> 5;
+    const int64_t r0 = ((int64_t)blockIdx.x * W + w) * R;
+    if (r0 >= p.n_rows) return;
+    const int nr = (int)min((int64_t)R, p.n_rows - r0);
+    const uint64_t pol_a = policy_evict_first();
+    const uint64_t pol_b = policy_evict_last();
+    // lane i < nr: row r0 + i (a1: k_i = min(d_i, s); a2: its FastRand rotation, R6)
+    RowSampler rs;
+    if (lane < nr)
+        rs.init(ld_stream(p.rowptr + r0 + lane, pol_a) - p.nnz_base,
+                ld_stream(p.rowptr + r0 + lane + 1, pol_a) - p.nnz_base, p.s, p.strategy, p.seed,
+                p.row_base + r0 + lane, p.prime);
+    else
+        rs.init(0, 0, p.s, p.strategy, 0, 0, p.prime);
+    const int32_t k_me = rs.k;
+    const int32_t kp_me = (k_me + 3) & ~3;                       // padded to whole 4-slot groups
+    int32_t incl = kp_me;                                        // inclusive prefix of the padded k
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t v = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += v;
+    }
+    const int32_t T = __shfl_sync(kFull, incl, 31);              // padded slots (multiple of 4)
+    const int NV = (int)((p.F + 3) / 4);
+    const bool active = lane < NV;                               // lane owns float4 `lane` of the row
+    // rows with k_i = 0 (empty in A): a zero row (no division), stored up front
+    unsigned empty = __ballot_sync(kFull, lane < nr && k_me == 0);
+    while (empty) {
+        const int i = __ffs(empty) - 1;
+        empty &= empty - 1;
+        const float z[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        if (active) store_c<4>(p, r0 + i, lane, z, pol_a);
+    }
+    if (T == 0) return;
+    unsigned rem = __ballot_sync(kFull, k_me > 0);               // rows not yet started, in order
+    // the rows' sampling state (read lane-parallel by the chunk searches) and two chunk slots of
+    // (B float4 index, val) pairs + masks
+    __shared__ int64_t s_beg[W][32], s_d[W][32];
+    __shared__ uint64_t s_off[W][32];
+    __shared__ int32_t s_start[W][32], s_k[W][32];
+    __shared__ __align__(16) uint32_t s_ci[W][2][32];
+    __shared__ __align__(16) float s_a[W][2][32];
+    __shared__ unsigned s_mask[W][2][2];                         // [slot][real, events]
+    s_beg[w][lane] = rs.beg;
+    s_d[w][lane] = rs.narrow ? rs.d : -rs.d;                     // sign: 64-bit position arithmetic
+    s_off[w][lane] = rs.off;
+    s_start[w][lane] = incl - kp_me;
+    s_k[w][lane] = k_me;
+    __syncwarp();
+    const uint32_t ldb4 = (uint32_t)(p.ldb >> 2);
+
+    // chunk metadata (a2 + a3, lane-parallel): padded slot t = t0 + lane.  Issues the (col, val)
+    // loads into ci / a (not waited on); returns the masks real (per slot) and events (bits 0-7:
+    // group g starts a row, bits 8-15: group g starts a 32-slot chunk of its row).
+    auto chunk = [&](int32_t t0, int32_t& col, float& a, unsigned& real, unsigned& ev) {
+        const int32_t t = t0 + lane;
+        int lo = 0;                                              // row of slot t: first i with incl_i > t
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+            const int32_t v = __shfl_sync(kFull, incl, lo + step - 1);
+            if (v <= t) lo += step;
+        }
+        const int32_t j = t - s_start[w][lo];
+        const bool valid = t < T && j < s_k[w][lo];
+        col = 0;
+        a = 0.0f;
+        if (valid) {
+            const int64_t dd = s_d[w][lo];
+            const int64_t e = s_beg[w][lo] + sample_pos(p.strategy, s_off[w][lo], dd < 0 ? -dd : dd, p.prime,
+                                                        dd > 0, j);
+            col = ld_stream(p.colind + e, pol_a);
+            if constexpr (HAS_VAL) a = ld_stream(p.val + e, pol_a);
+        }
+        real = __ballot_sync(kFull, valid);
+        ev = group_bits(__ballot_sync(kFull, t < T && j == 0)) |
+             (group_bits(__ballot_sync(kFull, t < T && j > 0 && (j & 31) == 0)) << 8);
+    };
+    auto commit = [&](int slot, int32_t col, float a, unsigned real, unsigned ev) {
+        s_ci[w][slot][lane] = (uint32_t)col * ldb4;
+        if constexpr (HAS_VAL) s_a[w][slot][lane] = a;
+        if (lane == 0) { s_mask[w][slot][0] = real; s_mask[w][slot][1] = ev; }
+        __syncwarp();
+    };
+    // the lane's piece of B row 0, held opaque (one register pair, not re-derived per gather);
+    // slot address = bl + 16 * (float4 index)
+    uint64_t bl;
+    asm("mov.b64 %0, %1;" : "=l"(bl) : "l"(reinterpret_cast<const float4*>(p.B) + (active ? lane : 0)));
+    auto load4 = [&](float4 (&x)[4], int slot, unsigned real, int g) {
+        const uint4 ci = *reinterpret_cast<const uint4*>(&s_ci[w][slot][4 * g]);
+        const uint32_t cs[4] = {ci.x, ci.y, ci.z, ci.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if ((real >> (4 * g + q)) & 1u) {
+                uint64_t addr;
+                asm("mad.wide.u32 %0, %1, 16, %2;" : "=l"(addr) : "r"(cs[q]), "l"(bl));
+                const Vec<4> v = ld_gather<4>(reinterpret_cast<const float*>(addr), pol_b);
+                x[q] = make_float4(v.v[0], v.v[1], v.v[2], v.v[3]);
+            }
+        }
+    };
+    float part[4] = {0.0f, 0.0f, 0.0f, 0.0f}, tot[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    int cur = 0;                                                 // lane (row) being accumulated
+    bool open = false;
+    // plain epilogue store: one 16-B store per lane (no peers / multicast, vector C, whole piece)
+    const bool plain_st = !p.c_mc && p.n_peers == 0 && p.c_vec && (int64_t)lane * 4 + 4 <= p.F;
+    auto flush = [&]() {                                         // a5: the current row is complete
+        float res[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            tot[q] += part[q];
+            res[q] = tot[q];
+            tot[q] = 0.0f;
+            part[q] = 0.0f;
+        }
+        if (p.reduce == kMean) {                                 // MEAN = / k_i (R5) or / d_i (NEXT-4)
+            int64_t div = s_k[w][cur];
+            if (p.mean_by_degree) {
+                const int64_t dd = s_d[w][cur];
+                div = dd < 0 ? -dd : dd;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) res[q] = finish(res[q], kMean, div);
+        }
+        if (plain_st) st_stream4(p.C + (r0 + cur) * p.ldc + lane * 4, res, pol_a);
+        else if (active) store_c<4>(p, r0 + cur, lane, res, pol_a);
+    };
+    auto consume4 = [&](const float4 (&x)[4], int slot, unsigned real, unsigned ev, int g) {
+        if ((ev >> g) & 1u) {                                    // the group starts the next non-empty row
+            if (open) flush();
+            cur = __ffs(rem) - 1;
+            rem &= rem - 1;
+            open = true;
+        } else if ((ev >> (8 + g)) & 1u) {                       // the row's next 32-slot chunk
+#pragma unroll
+            for (int e = 0; e < 4; ++e) { tot[e] += part[e]; part[e] = 0.0f; }
+        }
+        float av[4] = {1.0f, 1.0f, 1.0f, 1.0f};
+        if constexpr (HAS_VAL) {
+            const float4 a4 = *reinterpret_cast<const float4*>(&s_a[w][slot][4 * g]);
+            av[0] = a4.x; av[1] = a4.y; av[2] = a4.z; av[3] = a4.w;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if ((real >> (4 * g + q)) & 1u) {
+                part[0] = fmaf(av[q], x[q].x, part[0]);
+                part[1] = fmaf(av[q], x[q].y, part[1]);
+                part[2] = fmaf(av[q], x[q].z, part[2]);
+                part[3] = fmaf(av[q], x[q].w, part[3]);
+            }
+        }
+    };
+
+    const int n_chunks = (T + 31) >> 5;
+    int32_t pc;                                                  // chunk in flight: loads issued, not committed
+    float pa;
+    unsigned preal, pev;
+    chunk(0, pc, pa, preal, pev);
+    commit(0, pc, pa, preal, pev);
+    unsigned real = preal, ev = pev;
+    preal = pev = 0u;
+    if (n_chunks > 1) chunk(32, pc, pa, preal, pev);
+    float4 x0[4], x1[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) x0[q] = x1[q] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    load4(x0, 0, real, 0);
+    for (int k = 0; k < n_chunks; ++k) {
+        const int slot = k & 1;
+        const bool next = k + 1 < n_chunks;
+        unsigned nreal = 0u, nev = 0u;
+        if (next) {                                              // chunk k+1 -> shared memory; issue k+2
+            commit(slot ^ 1, pc, pa, preal, pev);
+            nreal = preal;
+            nev = pev;
+            preal = pev = 0u;
+            if (k + 2 < n_chunks) chunk((k + 2) * 32, pc, pa, preal, pev);
+        }
+        const int ng = min(32, T - k * 32) >> 2;                 // groups in this chunk (8 unless last)
+#pragma unroll 1
+        for (int g = 0; g < ng; g += 2) {
+            if (g + 1 < ng) load4(x1, slot, real, g + 1);
+            consume4(x0, slot, real, ev, g);
+            if (g + 1 >= ng) break;
+            if (g + 2 < ng) load4(x0, slot, real, g + 2);
+            else if (next) load4(x0, slot ^ 1, nreal, 0);        // the next chunk's first group
+            consume4(x1, slot, real, ev, g + 1);
+        }
+        real = nreal;
+        ev = nev;
+    }
+    if (open) flush();
 }
 
 // ------------------------------------------------------------------ short rows: degree-sorted half-warps
@@ -1424,6 +1654,30 @@ cudaError_t launch_grouped(const SpmmParams& p, const Tune& t, cudaStream_t st) 
     return launch_grouped_k<4, 6>(p, st);
 }
 
+template <int R, int W, int MINB>
+cudaError_t launch_segstream_k(const SpmmParams& p, cudaStream_t st) {
+    const int64_t warps = (p.n_rows + R - 1) / R;
+    const int64_t blocks = (warps + W - 1) / W;
+    if (p.val) spmm_segstream<R, W, MINB, true><<<(unsigned)blocks, 32 * W, 0, st>>>(p);
+    else spmm_segstream<R, W, MINB, false><<<(unsigned)blocks, 32 * W, 0, st>>>(p);
+    return cudaGetLastError();
+}
+
+// rows per warp tune.width (8, 16 or 32; default kSegRows), register cap tune.stages (CTAs of 4
+// warps per SM: 6 = 80 registers or 7 = 72; default kSegMinB; 8 spills)
+cudaError_t launch_segstream(const SpmmParams& p, const Tune& t, cudaStream_t st) {
+    const int R = t.width > 0 ? t.width : kSegRows;
+    const int minb = t.stages > 0 ? t.stages : kSegMinB;
+    if (minb == 6) {
+        if (R <= 8) return launch_segstream_k<8, 4, 6>(p, st);
+        if (R <= 16) return launch_segstream_k<16, 4, 6>(p, st);
+        return launch_segstream_k<32, 4, 6>(p, st);
+    }
+    if (R <= 8) return launch_segstream_k<8, 4, 7>(p, st);
+    if (R <= 16) return launch_segstream_k<16, 4, 7>(p, st);
+    return launch_segstream_k<32, 4, 7>(p, st);
+}
+
 cudaError_t launch_rowstream(const SpmmParams& p, const Tune& t, cudaStream_t st) {
     const int R = t.width > 0 ? t.width : 16;
     if (t.stages == 8) {
@@ -1594,6 +1848,14 @@ Plan make_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C
         pl.rows_per_warp = t.width > 0 ? t.width : 16;
         return pl;
     }
+    // short rows (F <= 128): the segmented register stream when rows sample few slots
+    if (rs_ok && (ov == ES_KERNEL_SEGSTREAM ||
+                  ((ov == ES_KERNEL_AUTO || ov == ES_KERNEL_FUSED) && k_est > 0 && k_est <= kSegMaxK))) {
+        pl.segstream = true;
+        pl.cpasync = pl.tma = pl.halfwarp = pl.subwarp = pl.rowstream = false;
+        pl.rows_per_warp = t.width > 0 ? t.width : kSegRows;
+        return pl;
+    }
     // short rows (F <= 128): the degree-sorted half-warp kernel when rows sample few slots
     if (rs_ok && (ov == ES_KERNEL_GROUPED ||
                   ((ov == ES_KERNEL_AUTO || ov == ES_KERNEL_FUSED) && k_est > 0 && k_est <= kGroupedMaxK))) {
@@ -1617,6 +1879,7 @@ Plan make_plan(int64_t F, int64_t ldb, int64_t ldc, const void* B, const void* C
 cudaError_t launch_spmm(SpmmParams p, const Plan& plan, const Tune& t, cudaStream_t st) {
     if (p.n_rows <= 0) return cudaSuccess;
     p.c_vec = plan.c_vec ? 1 : 0;
+    if (plan.segstream) return launch_segstream(p, t, st);
     if (plan.grouped) return launch_grouped(p, t, st);
     if (plan.rowstream) return launch_rowstream(p, t, st);
     if (plan.tma) return dispatch_tma(p, plan, st);

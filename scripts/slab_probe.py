@@ -81,7 +81,9 @@ def main():
         f = v.split(":")
         kern = f[0]
         tune = [int(x) for x in f[1:]] + [0] * (5 - len(f))
-        ws = es.es_spmm_workspace(nr, n, len(colind), F, ldb, s, va is not None, device=dev, kernel=kern)
+        fused_family = kern in ("fused", "warp", "tma", "cpasync", "halfwarp", "rowstream", "grouped", "segstream")
+        ws = None if fused_family else es.es_spmm_workspace(nr, n, len(colind), F, ldb, s, va is not None,
+                                                            device=dev, kernel=kern)
         C2.zero_()
         kw = dict(F=F, C=C2, workspace=ws, kernel=kern, tune=tune[:4])
         try:

@@ -134,7 +134,8 @@ KERNEL_PARAMS = {                       # name -> (kernel family, tune: stages, 
     "halfwarp": ("halfwarp", ()), "slab": ("slab", ()), "slab16": ("slab_smem", (0, 16)),
     "slab_ldg": ("slab_ldg", ()), "slab_tma": ("slab_tma", ()), "slab_stream": ("slab_stream", (0, 0, 0, 1024)),
     "rowstream": ("rowstream", ()), "grouped": ("grouped", ()), "grouped8": ("grouped", (8,)),
-    "grouped_ring": ("grouped", (4, 0, 0, 1)),
+    "grouped_ring": ("grouped", (4, 0, 0, 1)), "segstream": ("segstream", ()),
+    "segstream32": ("segstream", (6, 32)),
 }
 
 
@@ -202,6 +203,34 @@ def test_grouped_bitwise_warp(ragged, F, U, ring):
         with es.kernel_override("grouped", U, 0, 0, ring):
             b = run_gpu(rowptr, colind, val, B, s, strat, 5, red, F=F)
         assert np.array_equal(a, b), (F, s, strat, ring)
+
+
+@pytest.mark.parametrize("F", [65, 100, 128])
+@pytest.mark.parametrize("rows", [8, 16, 32])
+@pytest.mark.parametrize("minb", [6, 7])
+def test_segstream_bitwise_warp(ragged, F, rows, minb):
+    """The segmented register stream (R rows per warp as one slot stream, row / chunk events from
+    lane-parallel ballots) sums each row in slot order with 32-slot chunk partials from the row's
+    first slot -- the LDG warp-per-row kernel's order: bitwise, for every rows-per-warp and
+    register cap, across row ends inside and between the 4-slot groups and chunks."""
+    rowptr, colind, val = ragged
+    B = synth.dense(3001, F, seed=F, ld=(F + 3) // 4 * 4)
+    for s, strat, red, v in ((16, ES_FASTRAND, ES_REDUCE_MEAN, val), (64, ES_BUCKET, ES_REDUCE_SUM, val),
+                             (700, ES_FASTRAND, ES_REDUCE_MEAN, None), (1, ES_FASTRAND, ES_REDUCE_SUM, val),
+                             (33, ES_FASTRAND, ES_REDUCE_SUM, None)):
+        with es.kernel_override("warp"):
+            a = run_gpu(rowptr, colind, v, B, s, strat, 5, red, F=F)
+        with es.kernel_override("segstream", minb, rows):
+            b = run_gpu(rowptr, colind, v, B, s, strat, 5, red, F=F)
+        assert np.array_equal(a, b), (F, rows, minb, s, strat)
+    # Arxiv-like short rows: most rows 0-5 slots, so several rows end inside one 4-slot group
+    rp2, ci2, v2 = synth.random_csr(2011, 3001, seed=23, max_deg=6, special=(40, 33, 64))
+    for s, strat in ((64, ES_FASTRAND), (2, ES_BUCKET)):
+        with es.kernel_override("warp"):
+            a = run_gpu(rp2, ci2, v2, B, s, strat, 9, ES_REDUCE_MEAN, F=F)
+        with es.kernel_override("segstream", minb, rows):
+            b = run_gpu(rp2, ci2, v2, B, s, strat, 9, ES_REDUCE_MEAN, F=F)
+        assert np.array_equal(a, b), (F, rows, minb, s, strat, "short rows")
 
 
 @pytest.mark.parametrize("F", [65, 100, 128])

@@ -70,7 +70,7 @@ def test_host_validation_rejects_bad_arguments(lib):
 
 
 def test_plan_selection(lib):
-    assert es.es_spmm_plan(128, 128, 128).startswith("es::spmm_cpasync_hw<stages4>")
+    assert es.es_spmm_plan(128, 128, 128).startswith("es::spmm_segstream<rows8>")
     assert es.es_spmm_plan(200, 200, 200).startswith("es::spmm_cpasync<stages4>")
     assert es.es_spmm_plan(256, 256, 256).startswith("es::spmm_cpasync<stages4>")
     assert es.es_spmm_plan(512, 512, 512).startswith("es::spmm_cpasync<stages4>")
