@@ -365,8 +365,8 @@ es_status_t run_rows_impl(int64_t n_rows, int64_t n_cols, const int64_t* rowptr,
                            : es::make_plan(F, ldb, ldc, B, C, s, tn, k_est);
     if (plan.unsupported) return ES_ERR_UNSUPPORTED;
     if (tn.kernel == ES_KERNEL_ROWSTREAM && !plan.rowstream) return ES_ERR_UNSUPPORTED;
-    if (plan.segstream && (uint64_t)n_cols * (uint64_t)(ldb / 4) >= (1ull << 32)) {
-        // the segmented stream addresses B rows by a 32-bit float4 index (B > 64 GB: not expressible)
+    if (plan.segstream && (uint64_t)ldb * 4 >= (1ull << 32)) {
+        // the segmented stream multiplies a column by the row pitch in bytes as a 32-bit value
         if (tn.kernel == ES_KERNEL_SEGSTREAM) return ES_ERR_UNSUPPORTED;
         es::Tune t2 = tn;
         t2.kernel = ES_KERNEL_CPASYNC_HW;

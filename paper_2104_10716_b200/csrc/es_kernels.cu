@@ -672,9 +672,9 @@ spmm_cpasync_hw(const SpmmParams p) {
 //     finds the row of padded slot t0 + l (binary search over the lanes' padded prefix), its
 //     position (Eq. 2 / R6), (col, val) and the B row's float4 index; warp ballots turn "slot is
 //     real", "group starts a row" and "group starts a 32-slot partial chunk of its row" into
-//     uniform bit masks.  A chunk's (index, val) pairs go to a per-warp shared-memory slot one
-//     chunk after their loads were issued (so the colind latency is hidden), and a group reads
-//     its 4 indices / 4 values with one broadcast LDS.128 each;
+//     uniform bit masks.  A chunk's (col, val) pairs are copied by cp.async straight into one of
+//     three per-warp shared-memory slots two chunks ahead (the colind latency is hidden and costs
+//     no registers), and a group reads its 4 columns / 4 values with one broadcast LDS.128 each;
 //   * row ends and chunk partials fall on group boundaries: one event test per 4-slot group, no
 //     per-slot bookkeeping (padding slots: predicated-off gathers and FMAs, no memory traffic);
 //   * B rows are gathered register-direct (one LDG.128 per lane per slot; lane l owns float4 l of
@@ -683,8 +683,8 @@ spmm_cpasync_hw(const SpmmParams p) {
 //   * the group loop is rolled (two groups per iteration, one copy of the row epilogue per
 //     group site): the hot loop stays inside the ~6 KB L0 instruction cache.
 // Per element: the row's slots in slot order with 32-slot chunk partials (tot += part at every
-// chunk start and at the row's end) -- spmm_warp's order, bitwise.  Needs n_cols * ldb / 4 < 2^32
-// (the 32-bit float4 index; the ABI checks it).
+// chunk start and at the row's end) -- spmm_warp's order, bitwise.  Needs 4 ldb < 2^32 (the
+// row pitch in bytes as a 32-bit multiplier; the ABI checks it).
 __device__ __forceinline__ unsigned group_bits(unsigned m) {     // bits 0, 4, .., 28 -> bits 0 .. 7
     m &= 0x11111111u;
     m = (m | (m >> 3)) & 0x03030303u;
@@ -732,26 +732,26 @@ spmm_segstream(const SpmmParams p) {
     }
     if (T == 0) return;
     unsigned rem = __ballot_sync(kFull, k_me > 0);               // rows not yet started, in order
-    // the rows' sampling state (read lane-parallel by the chunk searches) and two chunk slots of
-    // (B float4 index, val) pairs + masks
+    // the rows' sampling state (read lane-parallel by the chunk searches) and three chunk slots of
+    // (col, val) + masks: chunk k is consumed from slot k % 3 while k+1 is ready and k+2 in flight
     __shared__ int64_t s_beg[W][32], s_d[W][32];
     __shared__ uint64_t s_off[W][32];
     __shared__ int32_t s_start[W][32], s_k[W][32];
-    __shared__ __align__(16) uint32_t s_ci[W][2][32];
-    __shared__ __align__(16) float s_a[W][2][32];
-    __shared__ unsigned s_mask[W][2][2];                         // [slot][real, events]
+    __shared__ __align__(16) int32_t s_col[W][3][32];
+    __shared__ __align__(16) float s_a[W][3][32];
+    __shared__ unsigned s_mask[W][3][2];                         // [slot][real, events]
     s_beg[w][lane] = rs.beg;
     s_d[w][lane] = rs.narrow ? rs.d : -rs.d;                     // sign: 64-bit position arithmetic
     s_off[w][lane] = rs.off;
     s_start[w][lane] = incl - kp_me;
     s_k[w][lane] = k_me;
     __syncwarp();
-    const uint32_t ldb4 = (uint32_t)(p.ldb >> 2);
 
-    // chunk metadata (a2 + a3, lane-parallel): padded slot t = t0 + lane.  Issues the (col, val)
-    // loads into ci / a (not waited on); returns the masks real (per slot) and events (bits 0-7:
-    // group g starts a row, bits 8-15: group g starts a 32-slot chunk of its row).
-    auto chunk = [&](int32_t t0, int32_t& col, float& a, unsigned& real, unsigned& ev) {
+    // chunk metadata (a2 + a3, lane-parallel): padded slot t = t0 + lane.  Its (col, val) are
+    // copied asynchronously into the slot (one cp.async group per chunk); the masks real (per
+    // slot) and events (bits 0-7: group g starts a row, bits 8-15: group g starts a 32-slot chunk
+    // of its row) are stored at once.
+    auto chunk = [&](int32_t t0, int slot) {
         const int32_t t = t0 + lane;
         int lo = 0;                                              // row of slot t: first i with incl_i > t
 #pragma unroll
@@ -761,37 +761,32 @@ spmm_segstream(const SpmmParams p) {
         }
         const int32_t j = t - s_start[w][lo];
         const bool valid = t < T && j < s_k[w][lo];
-        col = 0;
-        a = 0.0f;
         if (valid) {
             const int64_t dd = s_d[w][lo];
             const int64_t e = s_beg[w][lo] + sample_pos(p.strategy, s_off[w][lo], dd < 0 ? -dd : dd, p.prime,
                                                         dd > 0, j);
-            col = ld_stream(p.colind + e, pol_a);
-            if constexpr (HAS_VAL) a = ld_stream(p.val + e, pol_a);
+            cp_async4(&s_col[w][slot][lane], p.colind + e);
+            if constexpr (HAS_VAL) cp_async4(&s_a[w][slot][lane], p.val + e);
         }
-        real = __ballot_sync(kFull, valid);
-        ev = group_bits(__ballot_sync(kFull, t < T && j == 0)) |
-             (group_bits(__ballot_sync(kFull, t < T && j > 0 && (j & 31) == 0)) << 8);
-    };
-    auto commit = [&](int slot, int32_t col, float a, unsigned real, unsigned ev) {
-        s_ci[w][slot][lane] = (uint32_t)col * ldb4;
-        if constexpr (HAS_VAL) s_a[w][slot][lane] = a;
+        cp_async_commit();
+        const unsigned real = __ballot_sync(kFull, valid);
+        const unsigned ev = group_bits(__ballot_sync(kFull, t < T && j == 0)) |
+                            (group_bits(__ballot_sync(kFull, t < T && j > 0 && (j & 31) == 0)) << 8);
         if (lane == 0) { s_mask[w][slot][0] = real; s_mask[w][slot][1] = ev; }
-        __syncwarp();
     };
     // the lane's piece of B row 0, held opaque (one register pair, not re-derived per gather);
-    // slot address = bl + 16 * (float4 index)
+    // slot address = bl + col * (4 ldb): one IMAD.WIDE.U32 per gather
     uint64_t bl;
     asm("mov.b64 %0, %1;" : "=l"(bl) : "l"(reinterpret_cast<const float4*>(p.B) + (active ? lane : 0)));
+    const uint32_t ldb_bytes = (uint32_t)(p.ldb * 4);
     auto load4 = [&](float4 (&x)[4], int slot, unsigned real, int g) {
-        const uint4 ci = *reinterpret_cast<const uint4*>(&s_ci[w][slot][4 * g]);
-        const uint32_t cs[4] = {ci.x, ci.y, ci.z, ci.w};
+        const int4 c4 = *reinterpret_cast<const int4*>(&s_col[w][slot][4 * g]);
+        const uint32_t cs[4] = {(uint32_t)c4.x, (uint32_t)c4.y, (uint32_t)c4.z, (uint32_t)c4.w};
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             if ((real >> (4 * g + q)) & 1u) {
                 uint64_t addr;
-                asm("mad.wide.u32 %0, %1, 16, %2;" : "=l"(addr) : "r"(cs[q]), "l"(bl));
+                asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(addr) : "r"(cs[q]), "r"(ldb_bytes), "l"(bl));
                 const Vec<4> v = ld_gather<4>(reinterpret_cast<const float*>(addr), pol_b);
                 x[q] = make_float4(v.v[0], v.v[1], v.v[2], v.v[3]);
             }
@@ -824,14 +819,16 @@ spmm_segstream(const SpmmParams p) {
         else if (active) store_c<4>(p, r0 + cur, lane, res, pol_a);
     };
     auto consume4 = [&](const float4 (&x)[4], int slot, unsigned real, unsigned ev, int g) {
-        if ((ev >> g) & 1u) {                                    // the group starts the next non-empty row
-            if (open) flush();
-            cur = __ffs(rem) - 1;
-            rem &= rem - 1;
-            open = true;
-        } else if ((ev >> (8 + g)) & 1u) {                       // the row's next 32-slot chunk
+        if ((ev >> g) & 0x101u) {                                // an event: one uniform test per group
+            if ((ev >> g) & 1u) {                                // the group starts the next non-empty row
+                if (open) flush();
+                cur = __ffs(rem) - 1;
+                rem &= rem - 1;
+                open = true;
+            } else {                                             // the row's next 32-slot chunk
 #pragma unroll
-            for (int e = 0; e < 4; ++e) { tot[e] += part[e]; part[e] = 0.0f; }
+                for (int e = 0; e < 4; ++e) { tot[e] += part[e]; part[e] = 0.0f; }
+            }
         }
         float av[4] = {1.0f, 1.0f, 1.0f, 1.0f};
         if constexpr (HAS_VAL) {
@@ -850,28 +847,30 @@ spmm_segstream(const SpmmParams p) {
     };
 
     const int n_chunks = (T + 31) >> 5;
-    int32_t pc;                                                  // chunk in flight: loads issued, not committed
-    float pa;
-    unsigned preal, pev;
-    chunk(0, pc, pa, preal, pev);
-    commit(0, pc, pa, preal, pev);
-    unsigned real = preal, ev = pev;
-    preal = pev = 0u;
-    if (n_chunks > 1) chunk(32, pc, pa, preal, pev);
+    chunk(0, 0);
+    if (n_chunks > 1) chunk(32, 1);
+    if (n_chunks > 1) cp_async_wait<1>(); else cp_async_wait<0>();
+    __syncwarp();
+    unsigned real = s_mask[w][0][0], ev = s_mask[w][0][1];
     float4 x0[4], x1[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) x0[q] = x1[q] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
     load4(x0, 0, real, 0);
+    int slot = 0;
     for (int k = 0; k < n_chunks; ++k) {
-        const int slot = k & 1;
+        const int nslot = slot == 2 ? 0 : slot + 1;
         const bool next = k + 1 < n_chunks;
         unsigned nreal = 0u, nev = 0u;
-        if (next) {                                              // chunk k+1 -> shared memory; issue k+2
-            commit(slot ^ 1, pc, pa, preal, pev);
-            nreal = preal;
-            nev = pev;
-            preal = pev = 0u;
-            if (k + 2 < n_chunks) chunk((k + 2) * 32, pc, pa, preal, pev);
+        if (next) {                                              // chunk k+1 ready (issued a chunk ago); issue k+2
+            if (k + 2 < n_chunks) {
+                chunk((k + 2) * 32, nslot == 2 ? 0 : nslot + 1);
+                cp_async_wait<1>();
+            } else {
+                cp_async_wait<0>();
+            }
+            __syncwarp();
+            nreal = s_mask[w][nslot][0];
+            nev = s_mask[w][nslot][1];
         }
         const int ng = min(32, T - k * 32) >> 2;                 // groups in this chunk (8 unless last)
 #pragma unroll 1
@@ -880,11 +879,12 @@ spmm_segstream(const SpmmParams p) {
             consume4(x0, slot, real, ev, g);
             if (g + 1 >= ng) break;
             if (g + 2 < ng) load4(x0, slot, real, g + 2);
-            else if (next) load4(x0, slot ^ 1, nreal, 0);        // the next chunk's first group
+            else if (next) load4(x0, nslot, nreal, 0);           // the next chunk's first group
             consume4(x1, slot, real, ev, g + 1);
         }
         real = nreal;
         ev = nev;
+        slot = nslot;
     }
     if (open) flush();
 }
@@ -1664,7 +1664,7 @@ cudaError_t launch_segstream_k(const SpmmParams& p, cudaStream_t st) {
 }
 
 // rows per warp tune.width (8, 16 or 32; default kSegRows), register cap tune.stages (CTAs of 4
-// warps per SM: 6 = 80 registers or 7 = 72; default kSegMinB; 8 spills)
+// warps per SM: 6 = 80 registers, 7 = 72 or 8 = 64; default kSegMinB)
 cudaError_t launch_segstream(const SpmmParams& p, const Tune& t, cudaStream_t st) {
     const int R = t.width > 0 ? t.width : kSegRows;
     const int minb = t.stages > 0 ? t.stages : kSegMinB;
@@ -1672,6 +1672,11 @@ cudaError_t launch_segstream(const SpmmParams& p, const Tune& t, cudaStream_t st
         if (R <= 8) return launch_segstream_k<8, 4, 6>(p, st);
         if (R <= 16) return launch_segstream_k<16, 4, 6>(p, st);
         return launch_segstream_k<32, 4, 6>(p, st);
+    }
+    if (minb == 8) {
+        if (R <= 8) return launch_segstream_k<8, 4, 8>(p, st);
+        if (R <= 16) return launch_segstream_k<16, 4, 8>(p, st);
+        return launch_segstream_k<32, 4, 8>(p, st);
     }
     if (R <= 8) return launch_segstream_k<8, 4, 7>(p, st);
     if (R <= 16) return launch_segstream_k<16, 4, 7>(p, st);

@@ -207,7 +207,7 @@ def test_grouped_bitwise_warp(ragged, F, U, ring):
 
 @pytest.mark.parametrize("F", [65, 100, 128])
 @pytest.mark.parametrize("rows", [8, 16, 32])
-@pytest.mark.parametrize("minb", [6, 7])
+@pytest.mark.parametrize("minb", [6, 7, 8])
 def test_segstream_bitwise_warp(ragged, F, rows, minb):
     """The segmented register stream (R rows per warp as one slot stream, row / chunk events from
     lane-parallel ballots) sums each row in slot order with 32-slot chunk partials from the row's
