@@ -99,14 +99,16 @@ bool slab_feasible(int64_t n_cols, int64_t F) {
 // es_spmm_workspace_bytes's choice (measured, profiles/r02_flow_plan.jsonl): feasible,
 // F >= 128, a 16-B row pitch, and rows that sample enough slots on average: min(s, nnz / n_rows)
 // >= 32 for F > 256 (Reddit F=602: s = 32 flow 1.58 vs fused 1.76 ms, s = 16 1.16 vs 1.04) and
-// >= 128 for F <= 256 (Reddit F=128 s = 128 0.91 vs 1.04, s = 64 0.61 vs 0.59; Proteins s = 128
-// 0.59 vs 0.65; F=256 s = 64 1.10 vs 1.03).  Below that the fused kernels, which sample inside
-// the gather, win.
+// >= 128 for 128 < F <= 256 (F=256 s = 64 1.10 vs 1.03) and >= 256 for F <= 128, where the fused
+// kernel is the segmented register stream (profiles/r02_segstream_probe.jsonl seg9: Reddit F=128
+// s = 128 fused 0.89 vs flow 0.92 ms, Proteins s = 128 0.54 vs 0.59; s = 256 Proteins 0.96 vs
+// 0.93, Reddit 1.54 vs 1.39; s = 512 Proteins 1.62 vs 1.45).  Below that the fused kernels, which
+// sample inside the gather, win.
 bool slab_wanted(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t F, int64_t ldb, int64_t s) {
     if (!slab_feasible(n_cols, F) || ldb % 4 != 0 || F < 128) return false;
     const int64_t mean_deg = n_rows > 0 ? nnz / n_rows : 0;
     const int64_t k_est = s < mean_deg ? s : mean_deg;
-    return k_est >= (F > 256 ? 32 : 128);
+    return k_est >= (F > 256 ? 32 : F > 128 ? 128 : 256);
 }
 
 int64_t slab_align(int64_t x) { return (x + 255) & ~(int64_t)255; }

@@ -219,6 +219,8 @@ def test_workspace_bytes_plan(lib):
     assert es.es_spmm_workspace_bytes(232965, 232965, 114615945, 128, 128, 256) > 0     # B 119 MB
     assert es.es_spmm_workspace_bytes(132534, 132534, 79_100_000, 128, 128, 256) > 0    # long rows
     assert es.es_spmm_workspace_bytes(169343, 169343, 2_330_000, 128, 128, 64) == 0     # short rows
+    assert es.es_spmm_workspace_bytes(232965, 232965, 114615945, 128, 128, 128) == 0    # F <= 128: fused below s = 256
+    assert es.es_spmm_workspace_bytes(232965, 232965, 114615945, 256, 256, 128) > 0     # 128 < F <= 256: from s = 128
     assert es.es_spmm_workspace_bytes(10_000_000, 10_000_000, 10**9, 256, 256, 128) == 0  # slab > L2
     assert es.es_spmm_workspace_bytes(232965, 232965, 114615945, 64, 64, 256) == 0      # one slice
     assert es.es_spmm_workspace_bytes(232965, 232965, 114615945, 602, 608, 64) > 0      # s >= 32, F > 128
