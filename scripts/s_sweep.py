@@ -68,7 +68,9 @@ def main():
                 # operand is L2-resident -- B itself, or on the slab path its widest slab (<= 512 B of
                 # each row, within the 126 MB L2)
                 resident = (n * min(ldb * 4, 512) if ws is not None else n * ldb * 4) <= L2_BYTES
-                bound, peak = ("l2", l2) if (resident and l2) else ("hbm", hbm)
+                # a non-resident B whose gathers still run above the HBM copy rate is being served by
+                # L2 (hot rows re-gathered): HBM cannot be the ceiling that binds there
+                bound, peak = ("l2", l2) if (l2 and (resident or gbs > hbm)) else ("hbm", hbm)
                 print(json.dumps({"graph": name, "F": F, "s": s, "strategy": "bucket" if strat == 1 else "fastrand",
                                   "reduce": "mean" if red else "sum", "K": K, "rate": round(K / d.sum(), 4),
                                   "ms": round(ms, 4), "GFLOPs": round(2 * F * K / (ms / 1e3) / 1e9, 1),
