@@ -48,6 +48,7 @@ constexpr int64_t kGroupedMaxK = 0;     // never by default: measured no faster 
 // SM), and the plan's threshold on the mean sampled slots per row (profiles/r02_segstream_probe.jsonl)
 constexpr int kSegRows = 8;
 constexpr int kSegMinB = 7;
+constexpr int kSegCtaWarps = 2;         // 2-warp CTAs: Arxiv s=64 0.132 vs 0.135 ms with 4 (seg10)
 constexpr int64_t kSegMaxK = INT64_MAX;
 
 template <int VEC>
@@ -753,9 +754,9 @@ spmm_segstream(const SpmmParams p) {
     // of its row) are stored at once.
     auto chunk = [&](int32_t t0, int slot) {
         const int32_t t = t0 + lane;
-        int lo = 0;                                              // row of slot t: first i with incl_i > t
+        int lo = 0;                                              // row of slot t (< R): first i with incl_i > t
 #pragma unroll
-        for (int step = 16; step >= 1; step >>= 1) {
+        for (int step = R > 16 ? 16 : R > 8 ? 8 : R > 4 ? 4 : R > 2 ? 2 : 1; step >= 1; step >>= 1) {
             const int32_t v = __shfl_sync(kFull, incl, lo + step - 1);
             if (v <= t) lo += step;
         }
@@ -1664,10 +1665,27 @@ cudaError_t launch_segstream_k(const SpmmParams& p, cudaStream_t st) {
 }
 
 // rows per warp tune.width (8, 16 or 32; default kSegRows), register cap tune.stages (CTAs of 4
-// warps per SM: 6 = 80 registers, 7 = 72 or 8 = 64; default kSegMinB)
+// warps per SM: 6 = 80 registers, 7 = 72 or 8 = 64; default kSegMinB), tune.cta_warps 2 or 4 warps
+// per CTA (default kSegCtaWarps; the register caps are the same per SM)
 cudaError_t launch_segstream(const SpmmParams& p, const Tune& t, cudaStream_t st) {
     const int R = t.width > 0 ? t.width : kSegRows;
     const int minb = t.stages > 0 ? t.stages : kSegMinB;
+    const int ctaw = t.cta_warps > 0 ? t.cta_warps : kSegCtaWarps;
+    if (ctaw == 2) {                                             // 2-warp CTAs (finer tail), same register caps
+        if (minb == 6) {
+            if (R <= 8) return launch_segstream_k<8, 2, 12>(p, st);
+            if (R <= 16) return launch_segstream_k<16, 2, 12>(p, st);
+            return launch_segstream_k<32, 2, 12>(p, st);
+        }
+        if (minb == 8) {
+            if (R <= 8) return launch_segstream_k<8, 2, 16>(p, st);
+            if (R <= 16) return launch_segstream_k<16, 2, 16>(p, st);
+            return launch_segstream_k<32, 2, 16>(p, st);
+        }
+        if (R <= 8) return launch_segstream_k<8, 2, 14>(p, st);
+        if (R <= 16) return launch_segstream_k<16, 2, 14>(p, st);
+        return launch_segstream_k<32, 2, 14>(p, st);
+    }
     if (minb == 6) {
         if (R <= 8) return launch_segstream_k<8, 4, 6>(p, st);
         if (R <= 16) return launch_segstream_k<16, 4, 6>(p, st);

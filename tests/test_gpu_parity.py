@@ -206,9 +206,9 @@ def test_grouped_bitwise_warp(ragged, F, U, ring):
 
 
 @pytest.mark.parametrize("F", [65, 100, 128])
-@pytest.mark.parametrize("rows", [8, 16, 32])
-@pytest.mark.parametrize("minb", [6, 7, 8])
-def test_segstream_bitwise_warp(ragged, F, rows, minb):
+@pytest.mark.parametrize("ctaw", [2, 4])
+@pytest.mark.parametrize("rows,minb", [(8, 6), (16, 6), (32, 6), (8, 7), (16, 7), (32, 7), (8, 8), (16, 8), (32, 8)])
+def test_segstream_bitwise_warp(ragged, F, rows, minb, ctaw):
     """The segmented register stream (R rows per warp as one slot stream, row / chunk events from
     lane-parallel ballots) sums each row in slot order with 32-slot chunk partials from the row's
     first slot -- the LDG warp-per-row kernel's order: bitwise, for every rows-per-warp and
@@ -220,7 +220,7 @@ def test_segstream_bitwise_warp(ragged, F, rows, minb):
                              (33, ES_FASTRAND, ES_REDUCE_SUM, None)):
         with es.kernel_override("warp"):
             a = run_gpu(rowptr, colind, v, B, s, strat, 5, red, F=F)
-        with es.kernel_override("segstream", minb, rows):
+        with es.kernel_override("segstream", minb, rows, ctaw):
             b = run_gpu(rowptr, colind, v, B, s, strat, 5, red, F=F)
         assert np.array_equal(a, b), (F, rows, minb, s, strat)
     # Arxiv-like short rows: most rows 0-5 slots, so several rows end inside one 4-slot group
@@ -228,7 +228,7 @@ def test_segstream_bitwise_warp(ragged, F, rows, minb):
     for s, strat in ((64, ES_FASTRAND), (2, ES_BUCKET)):
         with es.kernel_override("warp"):
             a = run_gpu(rp2, ci2, v2, B, s, strat, 9, ES_REDUCE_MEAN, F=F)
-        with es.kernel_override("segstream", minb, rows):
+        with es.kernel_override("segstream", minb, rows, ctaw):
             b = run_gpu(rp2, ci2, v2, B, s, strat, 9, ES_REDUCE_MEAN, F=F)
         assert np.array_equal(a, b), (F, rows, minb, s, strat, "short rows")
 
