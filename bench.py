@@ -429,6 +429,8 @@ def main():
         n_launch = 1
         kname = "es::spmm_cpasync<bf16>" if a.bf16 else es.es_spmm_plan(F, ldb, C_d.stride(0), B_d, C_d, s=a.s,
                                                                         n_rows=r1 - r0, nnz=e1 - e0)
+        if a.kernel not in ("auto", "fused"):              # a forced family (A/B): not the plan's kernel
+            kname = f"forced family '{a.kernel}' (es_spmm_options_t.kernel)"
         what = "one fused launch per step (sampling inside the kernel)"
     else:
         # slab path: the dominant kernel is the slab pass (one launch per 256-B feature slice,

@@ -229,7 +229,7 @@ def es_launch_count() -> int:
 def es_spmm_plan(F: int, ldb: int, ldc: int, B=None, C=None, s: int | None = None, n_rows: int = 0,
                  nnz: int = 0) -> str:
     """The fused kernel the library would launch (es_spmm_plan, or es_spmm_plan_ex with s and the
-    rows' nnz: short rows take the degree-sorted half-warp kernel)."""
+    rows' nnz: the slab/fused thresholds and the short-row kernels depend on them)."""
     buf = ctypes.create_string_buffer(128)
     if s is None:
         _check(load_library().es_spmm_plan(F, ldb, ldc, _ptr(B), _ptr(C), buf, 128), "es_spmm_plan")
