@@ -23,21 +23,22 @@ from paper_2104_10716_b200 import dist as esdist  # noqa: E402
 N, NC, F = 900, 1200, 130
 
 
-def graph():
+def graph(F=F):
     rowptr, colind, val = synth.random_csr(N, NC, seed=12, max_deg=200, special=(577,))
     B = synth.dense(NC, F, seed=4, ld=132)
     return rowptr, colind, val, B
 
 
-@pytest.mark.parametrize("path", ["fused", "slab"])
+@pytest.mark.parametrize("path", ["fused", "slab", "segstream"])
 def test_two_local_peer_buffers(path):
-    # slab: the feature-sliced path's epilogue stores to the peers too
+    # slab: the feature-sliced path's epilogue stores to the peers too; segstream: the short-row
+    # fused kernel's epilogue (F <= 128)
     with es.kernel_override(path):
-        _two_local_peer_buffers(path)
+        _two_local_peer_buffers(path, 128 if path == "segstream" else F)
 
 
-def _two_local_peer_buffers(path):
-    rowptr, colind, val, B = graph()
+def _two_local_peer_buffers(path, F):
+    rowptr, colind, val, B = graph(F)
     dev = torch.device("cuda:0")
     bufs = [es.es_ipc_alloc(N * 132 * 4) for _ in range(2)]
     try:
