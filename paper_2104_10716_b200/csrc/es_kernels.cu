@@ -1664,7 +1664,8 @@ cudaError_t launch_segstream_k(const SpmmParams& p, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-// rows per warp tune.width (8, 16 or 32; default kSegRows), register cap tune.stages (CTAs of 4
+// rows per warp tune.width (8, 16 or 32, and 4 with 2-warp CTAs at the default cap; default kSegRows),
+// register cap tune.stages (CTAs of 4
 // warps per SM: 6 = 80 registers, 7 = 72 or 8 = 64; default kSegMinB), tune.cta_warps 2 or 4 warps
 // per CTA (default kSegCtaWarps; the register caps are the same per SM)
 cudaError_t launch_segstream(const SpmmParams& p, const Tune& t, cudaStream_t st) {
@@ -1682,6 +1683,7 @@ cudaError_t launch_segstream(const SpmmParams& p, const Tune& t, cudaStream_t st
             if (R <= 16) return launch_segstream_k<16, 2, 16>(p, st);
             return launch_segstream_k<32, 2, 16>(p, st);
         }
+        if (R <= 4) return launch_segstream_k<4, 2, 14>(p, st);
         if (R <= 8) return launch_segstream_k<8, 2, 14>(p, st);
         if (R <= 16) return launch_segstream_k<16, 2, 14>(p, st);
         return launch_segstream_k<32, 2, 14>(p, st);

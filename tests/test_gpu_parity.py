@@ -207,7 +207,7 @@ def test_grouped_bitwise_warp(ragged, F, U, ring):
 
 @pytest.mark.parametrize("F", [65, 100, 128])
 @pytest.mark.parametrize("ctaw", [2, 4])
-@pytest.mark.parametrize("rows,minb", [(8, 6), (16, 6), (32, 6), (8, 7), (16, 7), (32, 7), (8, 8), (16, 8), (32, 8)])
+@pytest.mark.parametrize("rows,minb", [(8, 6), (16, 6), (32, 6), (4, 7), (8, 7), (16, 7), (32, 7), (8, 8), (16, 8), (32, 8)])
 def test_segstream_bitwise_warp(ragged, F, rows, minb, ctaw):
     """The segmented register stream (R rows per warp as one slot stream, row / chunk events from
     lane-parallel ballots) sums each row in slot order with 32-slot chunk partials from the row's
